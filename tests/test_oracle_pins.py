@@ -1,0 +1,413 @@
+"""Pins of the fp64 oracle against things other than itself (no GPU).
+
+Each test names the passage / closed form it checks.  P:n = PAPER.md line n,
+S:n = SPEC.md line n (test ideas only).  These must pass before the CUDA path
+is compared against the oracle.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import (
+    NCOperator,
+    NEOperator,
+    adjacency,
+    context_weights,
+    exact_svd,
+    isvd,
+    orthonorm_cholesky,
+    orthonorm_qr,
+    philox4x32_10,
+    philox_omega,
+    sign_fix,
+    sym_norm_adj,
+    transition,
+    uniform_weights,
+)
+from oracle.isvd_oracle import DenseOperator
+from synth.graphs import edges_to_graph, powerlaw_graph
+
+
+def _A(n, edges):
+    g = edges_to_graph(n, edges)
+    return adjacency(g.n, g.row_ptr, g.col_idx)
+
+
+def _complete(n):
+    return _A(n, [(i, j) for i in range(n) for j in range(i + 1, n)])
+
+
+def _cycle(n):
+    return _A(n, [(i, (i + 1) % n) for i in range(n)])
+
+
+def _random_connected(n, extra, rng):
+    edges = {(i, int(rng.integers(0, i))) for i in range(1, n)}  # random tree
+    extra = min(extra, n * (n - 1) // 2 - (n - 1))
+    while len(edges) < n - 1 + extra:
+        u, v = (int(x) for x in rng.integers(0, n, 2))
+        if u != v and (u, v) not in edges and (v, u) not in edges:
+            edges.add((u, v))
+    return _A(n, sorted(edges))
+
+
+# --------------------------------------------------------------------- Omega
+
+
+def test_philox_known_answer_vectors(golden):
+    """Random123 KAT vectors (tests/golden/philox4x32_10_kat.txt)."""
+    for row in golden("philox4x32_10_kat.txt"):
+        v = [int(x, 16) for x in row]
+        out = philox4x32_10(np.array(v[:4]), (v[4], v[5]))
+        assert [int(x) for x in out] == v[6:]
+
+
+def test_omega_slices_are_consistent_and_standard_normal():
+    """Counter-based: any row block equals the slice of the full matrix (P-invariance of
+    the row partition); moments of N(0,1)."""
+    full = philox_omega(7, 0, 1000, 37)
+    part = philox_omega(7, 313, 101, 37)
+    assert np.array_equal(full[313:414], part)
+    z = philox_omega(11, 0, 20000, 50).astype(np.float64).ravel()
+    assert abs(z.mean()) < 5 * 1 / np.sqrt(z.size)
+    assert abs(z.var() - 1.0) < 5 * np.sqrt(2.0 / z.size)
+    assert abs((z ** 3).mean()) < 5 * np.sqrt(15.0 / z.size)
+    assert abs((z ** 4).mean() - 3.0) < 5 * np.sqrt(96.0 / z.size)
+
+
+# ----------------------------------------------------------- graph matrices
+
+
+def test_transition_path_graph():
+    """T = D^-1 A on the path 0-1-2."""
+    T = transition(_A(3, [(0, 1), (1, 2)])).toarray()
+    assert np.array_equal(T, [[0, 1, 0], [0.5, 0, 0.5], [0, 1, 0]])
+
+
+def test_transition_isolated_node_row_is_zero():
+    """0^-1 := 0 leaves the isolated node's row zero (reading O3)."""
+    T = transition(_A(4, [(0, 1), (1, 2)])).toarray()
+    assert np.array_equal(T[3], np.zeros(4))
+    assert np.allclose(T[:3].sum(axis=1), 1.0)
+
+
+def test_ahat_single_and_two_nodes():
+    """A_hat of one node = [1]; of two connected nodes = [[.5,.5],[.5,.5]]."""
+    assert np.array_equal(sym_norm_adj(_A(1, [])).toarray(), [[1.0]])
+    assert np.allclose(sym_norm_adj(_A(2, [(0, 1)])).toarray(), [[0.5, 0.5], [0.5, 0.5]], atol=1e-15)
+
+
+def test_ahat_path_graph_hand_values(golden):
+    """Middle row of A_hat on the path 0-1-2, derived by hand in tests/golden/path3_hand.txt."""
+    rows = {r[0]: [float(x) for x in r[1:]] for r in golden("path3_hand.txt")}
+    Ah = sym_norm_adj(_A(3, [(0, 1), (1, 2)])).toarray()
+    assert np.allclose(Ah[1], rows["nc_ahat_row1"], rtol=0, atol=1e-15)
+    assert np.allclose(Ah, Ah.T, atol=0)
+
+
+# ---------------------------------------------------------- context weights
+
+
+def test_context_weights_fig1(golden):
+    """C=3 -> [3,2,1]/6 exactly as Fig. 1's code."""
+    rows = golden("fig1_context_weights.txt")
+    C = int(rows[0][1])
+    want = [float(Fraction(x)) for x in rows[1]]
+    assert np.array_equal(context_weights(C), want)
+
+
+def test_context_weights_closed_forms():
+    """C=1 -> [1]; C=10 -> (11-q)/55; uniform 1/C sums to 1."""
+    assert np.array_equal(context_weights(1), [1.0])
+    assert np.allclose(context_weights(10), [(11 - q) / 55 for q in range(1, 11)], rtol=0, atol=1e-16)
+    assert abs(uniform_weights(7).sum() - 1.0) < 1e-15
+    with pytest.raises(ValueError):
+        context_weights(0)
+
+
+# -------------------------------------------------------------- NE operator
+
+
+def test_ne_path_graph_hand_values(golden):
+    """Eq. 3 on the path 0-1-2, C=2 uniform, lambda=1/3: rank 1, hand-derived entries and sigma."""
+    rows = {r[0]: [float(x) for x in r[1:]] for r in golden("path3_hand.txt")}
+    op = NEOperator(_A(3, [(0, 1), (1, 2)]), uniform_weights(2), 1.0 / 3.0)
+    M = op.dense()
+    assert np.allclose(M, np.tile(rows["ne_M_row"], (3, 1)), rtol=0, atol=1e-15)
+    U, s, V, _ = isvd(op, 1, philox_omega(5, 0, 3, 3), iterations=1)
+    assert abs(s[0] - rows["ne_sigma1"][0]) < 1e-15
+    assert np.allclose(U[:, 0], np.full(3, 1 / np.sqrt(3)), atol=1e-14)
+    assert np.allclose(V[:, 0], np.array([-1.0, 2.0, -1.0]) / np.sqrt(6), atol=1e-14)
+
+
+@pytest.mark.parametrize("C", [1, 5, 10])
+def test_ne_null_vector(C):
+    """T 1 = 1 (row-stochastic) and sum w = 1 => M 1 = (sum w - lambda n) 1 = 0."""
+    rng = np.random.default_rng(C)
+    for t in range(20):
+        n = 30
+        op = NEOperator(_random_connected(n, 25, rng), uniform_weights(C), 1.0 / n)
+        assert np.abs(op.matmul(np.ones((n, 1)))).max() < 1e-14
+        op2 = NEOperator(_random_connected(n, 25, rng), context_weights(C), 1.0 / n)
+        assert np.abs(op2.matmul(np.ones((n, 1)))).max() < 1e-14
+
+
+@pytest.mark.parametrize("C,weights", [(1, "u"), (5, "u"), (10, "u"), (3, "t"), (10, "t")])
+def test_ne_complete_graph_spectrum(C, weights):
+    """K_n: T = (J - I)/(n-1) has eigenvalues 1 (on 1) and -1/(n-1) (mult. n-1), so
+    sigma(M) = |sum_c w_c (-1/(n-1))^c| (mult. n-1) and 0 -- computed by Alg. 1 with l = n."""
+    w = uniform_weights(C) if weights == "u" else context_weights(C)
+    for n in range(5, 13):
+        op = NEOperator(_complete(n), w, 1.0 / n)
+        mu = -1.0 / (n - 1)
+        want = abs(sum(w[c - 1] * mu ** c for c in range(1, C + 1)))
+        _, s, _, s_all = isvd(op, n - 1, philox_omega(n, 0, n, n), iterations=1)
+        assert np.allclose(s, want, rtol=1e-12, atol=1e-15)
+        assert abs(s_all[-1]) < 1e-13
+
+
+@pytest.mark.parametrize("C", [1, 5, 10])
+def test_ne_cycle_spectrum(C):
+    """Cycle C_n: T = (P + P^T)/2 with eigenvalues cos(2 pi j / n), so the singular values
+    are {|sum_c w_c cos(2 pi j/n)^c| : j = 1..n-1} plus 0 (the 1-direction)."""
+    w = uniform_weights(C)
+    for n in range(6, 17):
+        op = NEOperator(_cycle(n), w, 1.0 / n)
+        lam = np.cos(2 * np.pi * np.arange(1, n) / n)
+        want = np.sort(np.abs([sum(w[c - 1] * x ** c for c in range(1, C + 1)) for x in lam]))[::-1]
+        _, _, _, s_all = isvd(op, n - 1, philox_omega(100 + n, 0, n, n), iterations=2)
+        assert np.allclose(s_all[: n - 1], want, rtol=0, atol=1e-13)
+        assert s_all[n - 1] < 1e-13
+
+
+def test_ne_degenerate_c1_lambda0_is_T():
+    """build_ne with lambda = 0, C = 1 is T itself."""
+    rng = np.random.default_rng(3)
+    A = _random_connected(12, 10, rng)
+    op = NEOperator(A, [1.0], 0.0)
+    G = rng.standard_normal((12, 4))
+    assert np.allclose(op.matmul(G), transition(A) @ G, rtol=0, atol=1e-15)
+
+
+def test_ne_lambda_adj_term():
+    """Eq. 3's -lambda(1 - A) = -lambda 1 1^T + lambda A (P:145, P:254 'row1.T @ row1 - A')."""
+    A = _A(4, [(0, 1), (1, 2), (2, 3)])
+    lam = 0.05
+    op = NEOperator(A, context_weights(3), lam, lam)
+    T = transition(A).toarray()
+    want = sum(w * np.linalg.matrix_power(T, c) for c, w in zip(range(1, 4), context_weights(3)))
+    want = want - lam * (np.ones((4, 4)) - A.toarray())
+    assert np.allclose(op.dense(), want, rtol=0, atol=1e-15)
+
+
+# -------------------------------------------------------------- NC operator
+
+
+def test_nc_path_graph_hand_values(golden):
+    """Eq. 6 with X = e_0, L = 1 on the path graph: sigma^2 are the roots of the
+    characteristic polynomial derived by hand (tests/golden/path3_hand.txt)."""
+    rows = {r[0]: [float(x) for x in r[1:]] for r in golden("path3_hand.txt")}
+    op = NCOperator(_A(3, [(0, 1), (1, 2)]), np.array([[1.0], [0.0], [0.0]]), 1)
+    want = np.sort(np.sqrt(np.roots(rows["nc_sigma_sq_poly"])))[::-1]
+    _, s, _, _ = isvd(op, 2, philox_omega(1, 0, 2, 2), iterations=2)
+    assert np.allclose(s, want, rtol=1e-14, atol=0)
+
+
+def test_nc_L0_is_X_and_shape():
+    """L = 0 gives X; L = 2, d = 3 on 5 nodes has shape (5, 9), F = d + dL."""
+    rng = np.random.default_rng(0)
+    A = _random_connected(5, 2, rng)
+    X = rng.standard_normal((5, 3))
+    assert np.array_equal(NCOperator(A, X, 0).dense(), X)
+    assert NCOperator(A, X, 2).shape == (5, 9)
+
+
+def test_nc_complete_graph_closed_form():
+    """K_n: A_hat = J/n, so A_hat^j X = 1 mean(X) for every j >= 1."""
+    rng = np.random.default_rng(1)
+    for n in (4, 7, 10):
+        X = rng.standard_normal((n, 3))
+        M = NCOperator(_complete(n), X, 3).dense()
+        mean = np.tile(X.mean(axis=0), (n, 1))
+        assert np.allclose(M[:, :3], X, atol=0)
+        for j in (1, 2, 3):
+            assert np.allclose(M[:, 3 * j : 3 * j + 3], mean, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------- implicit vs explicit, duality
+
+
+def _explicit_ne(A, w, lam_ones, lam_adj):
+    Ad = A.toarray()
+    d = Ad.sum(axis=1)
+    T = np.divide(Ad, d[:, None], out=np.zeros_like(Ad), where=d[:, None] > 0)
+    M = sum(wc * np.linalg.matrix_power(T, c + 1) for c, wc in enumerate(w))
+    return M - lam_ones * np.ones_like(Ad) + lam_adj * Ad
+
+
+def _explicit_nc(A, X, L):
+    Ad = A.toarray()
+    n = Ad.shape[0]
+    s = 1.0 / np.sqrt(Ad.sum(axis=1) + 1.0)
+    Ah = s[:, None] * (Ad + np.eye(n)) * s[None, :]
+    return np.hstack([np.linalg.matrix_power(Ah, j) @ X for j in range(L + 1)])
+
+
+def test_implicit_equals_explicit_and_transpose_duality():
+    """north_star: implicit M.x equals explicit M.x; duality <H, M G> = <M^T H, G>."""
+    rng = np.random.default_rng(42)
+    graphs = [_A(6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5), (2, 3)])]  # two triangles
+    graphs += [_random_connected(int(rng.integers(3, 13)), int(rng.integers(0, 8)), rng) for _ in range(20)]
+    for A in graphs:
+        n = A.shape[0]
+        for C in (1, 3, 5):
+            w = rng.random(C)
+            lo, la = rng.random(), rng.random() * (C == 3)
+            op = NEOperator(A, w, lo, la)
+            Me = _explicit_ne(A, w, lo, la)
+            G = rng.standard_normal((n, 3))
+            H = rng.standard_normal((n, 3))
+            assert np.allclose(op.matmul(G), Me @ G, rtol=0, atol=1e-12)
+            assert np.allclose(op.matmul_T(H), Me.T @ H, rtol=0, atol=1e-12)
+            assert abs(np.sum(H * op.matmul(G)) - np.sum(op.matmul_T(H) * G)) < 1e-12
+        X = rng.standard_normal((n, 2))
+        for L in (0, 1, 3):
+            op = NCOperator(A, X, L)
+            Me = _explicit_nc(A, X, L)
+            G = rng.standard_normal((2 * (L + 1), 3))
+            H = rng.standard_normal((n, 3))
+            assert np.allclose(op.matmul(G), Me @ G, rtol=0, atol=1e-12)
+            assert np.allclose(op.matmul_T(H), Me.T @ H, rtol=0, atol=1e-12)
+            assert abs(np.sum(H * op.matmul(G)) - np.sum(op.matmul_T(H) * G)) < 1e-12
+
+
+# ------------------------------------------------------ orthonormalisation
+
+
+def test_orthonorm_qr_matches_cholesky_and_spans():
+    """Alg. 2: both routines give Q^T Q = I and span(Q) = span(Y) (footnote P:884); the
+    thin QR factor with diag(R) > 0 is unique, so they agree."""
+    rng = np.random.default_rng(9)
+    for shape in [(200, 12), (50, 50), (1000, 42)]:
+        Y = rng.standard_normal(shape) @ np.diag(np.logspace(0, 2, shape[1]))
+        Q1 = orthonorm_qr(Y)
+        Q2 = orthonorm_cholesky(Y)
+        assert np.abs(Q1.T @ Q1 - np.eye(shape[1])).max() < 1e-13
+        assert np.abs(Q1 - Q2).max() < 1e-10
+        # span: Y = Q R with R upper triangular, positive diagonal
+        R = Q1.T @ Y
+        assert np.abs(np.tril(R, -1)).max() < 1e-10 * np.abs(R).max()
+        assert (np.diag(R) > 0).all()
+        assert np.abs(Q1 @ R - Y).max() < 1e-10 * np.abs(Y).max()
+
+
+def test_cholesky_fails_on_duplicated_column():
+    """Q with a duplicated column has a singular Gram: Cholesky breaks down."""
+    rng = np.random.default_rng(2)
+    Y = rng.standard_normal((20, 4))
+    Y[:, 3] = Y[:, 1]
+    with pytest.raises(np.linalg.LinAlgError):
+        orthonorm_cholesky(Y)
+
+
+# ------------------------------------------------------------------- Alg. 1
+
+
+def test_exact_svd_special_matrices():
+    """Identity -> s = 1; diag(3,2,1,0) -> (3,2) with basis vectors."""
+    _, s, _, _ = exact_svd(np.eye(5), 5)
+    assert np.allclose(s, 1.0, atol=1e-15)
+    U, s, V, _ = exact_svd(np.diag([3.0, 2.0, 1.0, 0.0]), 2)
+    assert np.allclose(s, [3, 2], atol=1e-15)
+    assert np.allclose(np.abs(U), np.eye(4)[:, :2]) and np.allclose(np.abs(V), np.eye(4)[:, :2])
+    U, s, V, _ = isvd(DenseOperator(np.diag([3.0, 2.0, 1.0, 0.0])), 2, philox_omega(3, 0, 4, 4), iterations=2)
+    assert np.allclose(s, [3, 2], atol=1e-14)
+    assert np.allclose(np.abs(U), np.eye(4)[:, :2], atol=1e-14)
+
+
+def test_isvd_exact_when_l_covers_rank():
+    """If k >= rank(M) the error is 0; Alg. 1 on an exact rank-20 50 x 40 matrix
+    recovers the dense spectrum and reconstructs M."""
+    rng = np.random.default_rng(4)
+    M = rng.standard_normal((50, 20)) @ rng.standard_normal((20, 40))
+    U, s, V, _ = isvd(DenseOperator(M), 20, philox_omega(4, 0, 40, 24), iterations=1)
+    _, s_ex, _, _ = exact_svd(M, 20)
+    assert np.allclose(s, s_ex, rtol=1e-12)
+    assert np.abs(U @ np.diag(s) @ V.T - M).max() < 1e-10 * np.abs(M).max()
+    assert np.abs(U.T @ U - np.eye(20)).max() < 1e-12 and np.abs(V.T @ V - np.eye(20)).max() < 1e-12
+
+
+def test_eckart_young_tail_identity():
+    """||M - U_k S_k V_k^T||_F^2 = sum_{j>k} sigma_j^2 for the exact SVD (Eckart-Young);
+    Alg. 1's randomized factors can only do worse (>= tail)."""
+    rng = np.random.default_rng(5)
+    A = _random_connected(40, 60, rng)
+    op = NEOperator(A, uniform_weights(5), 1.0 / 40)
+    M = op.dense()
+    fro2 = np.sum(M * M)
+    for k in (1, 5, 10, 20):
+        U, s, V, s_all = exact_svd(M, k)
+        res = np.sum((M - U @ np.diag(s) @ V.T) ** 2)
+        assert abs(res - np.sum(s_all[k:] ** 2)) < 1e-10 * fro2
+        Ur, sr, Vr, _ = isvd(op, k, philox_omega(k, 0, 40, k + 2), iterations=1)
+        res_r = np.sum((M - Ur @ np.diag(sr) @ Vr.T) ** 2)
+        assert res_r >= np.sum(s_all[k:] ** 2) - 1e-12 * fro2
+
+
+def test_error_decays_with_iterations():
+    """Theorem 4: the median residual gap over 10 seeds is non-increasing
+    in iterations in {1, 2, 4, 8} on low-rank-plus-noise matrices."""
+    rng = np.random.default_rng(6)
+    gaps = {q: [] for q in (1, 2, 4, 8)}
+    for seed in range(10):
+        U0, _ = np.linalg.qr(rng.standard_normal((120, 30)))
+        V0, _ = np.linalg.qr(rng.standard_normal((80, 30)))
+        M = U0 @ np.diag(np.logspace(0, -1.5, 30)) @ V0.T + 1e-3 * rng.standard_normal((120, 80))
+        _, _, _, s_all = exact_svd(M, 10)
+        opt = np.sqrt(np.sum(s_all[10:] ** 2))
+        for q in gaps:
+            U, s, V, _ = isvd(DenseOperator(M), 10, philox_omega(seed, 0, 80, 12), iterations=q)
+            gaps[q].append(np.linalg.norm(M - U @ np.diag(s) @ V.T) - opt)
+    med = [np.median(gaps[q]) for q in (1, 2, 4, 8)]
+    assert all(med[i + 1] <= med[i] + 1e-12 for i in range(3)), med
+    assert med[-1] < 0.1 * med[0]
+
+
+def test_sign_rule():
+    """Largest-|.| entry of each U column positive; ties -> lowest index."""
+    U = np.array([[0.5, -0.7], [-0.5, 0.7], [0.1, 0.1]])
+    V = np.array([[1.0, 1.0], [2.0, 2.0]])
+    U2, V2 = sign_fix(U, V)
+    assert np.array_equal(U2[:, 0], U[:, 0]) and np.array_equal(V2[:, 0], V[:, 0])
+    assert np.array_equal(U2[:, 1], -U[:, 1]) and np.array_equal(V2[:, 1], -V[:, 1])
+
+
+def test_permutation_invariance_ne_and_nc():
+    """Relabelling nodes (A' = P A P^T) leaves the singular values unchanged and permutes
+    U (and V for NE); Omega' = P Omega for NE, the same Omega for NC (north_star)."""
+    g = powerlaw_graph(600, 1500, 2.5, seed=11)
+    perm = np.random.default_rng(12).permutation(g.n)
+    gp = g.permuted(perm)
+    A, Ap = adjacency(g.n, g.row_ptr, g.col_idx), adjacency(gp.n, gp.row_ptr, gp.col_idx)
+    om = philox_omega(3, 0, g.n, 20)
+    omp = np.empty_like(om)
+    omp[perm] = om
+    U, s, V, _ = isvd(NEOperator(A, uniform_weights(5), 1 / g.n), 16, om, iterations=2)
+    Up, sp_, Vp, _ = isvd(NEOperator(Ap, uniform_weights(5), 1 / g.n), 16, omp, iterations=2)
+    assert np.allclose(s, sp_, rtol=1e-12)
+    assert np.allclose(Up[perm], U, atol=1e-9) and np.allclose(Vp[perm], V, atol=1e-9)
+    X = np.random.default_rng(13).standard_normal((g.n, 8))
+    Xp = np.empty_like(X)
+    Xp[perm] = X
+    om = philox_omega(4, 0, 32, 16)
+    U, s, V, _ = isvd(NCOperator(A, X, 3), 8, om, iterations=2)
+    Up, sp_, Vp, _ = isvd(NCOperator(Ap, Xp, 3), 8, om, iterations=2)
+    assert np.allclose(s, sp_, rtol=1e-12)
+    assert np.allclose(Up[perm], U, atol=1e-9) and np.allclose(Vp, V, atol=1e-9)
+
+
+def test_isvd_rejects_bad_rank():
+    """k > min(r, c) is an error."""
+    with pytest.raises(ValueError):
+        isvd(DenseOperator(np.eye(3)), 4, philox_omega(0, 0, 3, 4), iterations=1)
