@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the implicit randomized SVD hot path (arXiv 2111.06312) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config I] [--impl isvd|reference]
+
+One "step" is one rank-k implicit SVD (Alg. 1) of the
+config's implicit design matrix: every product M Q / M^T Q, every CholeskyQR2,
+the small SVD and the final U, V -- the whole hot path.  The default workload
+is config 4 (NC design matrix [X | AX | A^2X | A^3X] of a 2.45M-node power-law
+graph, k = 256, l = 400, q = 2): the configuration the metric's HBM-bandwidth
+clause and the 1/2/4/8-GPU scaling are quoted on.
+Inputs are synthetic (synth/), resident in HBM when the timed region starts,
+and larger than the 126 MB L2 (no flush needed).
+
+For N > 1 the driver launches one process per GPU with torchrun; rows are
+partitioned (strong scaling: one isvd of the same matrix over N GPUs).
+Rank 0 prints ONE JSON line.
+
+`--impl reference` times the fp64 CPU oracle (oracle/, the reference arm of this
+tier) on a bounded sample of the same workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rank-k implicit SVD time (s); fused SpMM HBM GB/s vs ~8 TB/s B200 peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="isvd", choices=["isvd", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ oracle arm
+def oracle_sample(cfg, g, X, sp, cols=8):
+    """Time the fp64 oracle's products on a bounded sample of the workload and scale to one isvd.
+
+    Sample: one M.G and one M^T.Q on `cols` of the l columns (columns are independent in
+    every product), scaled by l/cols and by the q+1 applications of each of M and M^T in
+    Alg. 1.  Orthonormalisation and the small SVD are not included (products only)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    from oracle import NCOperator, NEOperator, adjacency
+
+    A = adjacency(g.n, g.row_ptr, g.col_idx)
+    ref = NEOperator(A, sp["weights"], sp["lambda_ones"]) if cfg["op"] == "NE" else NCOperator(A, X, sp["L"])
+    r, c = ref.shape
+    cols = min(cols, sp["l"])
+    rng = np.random.default_rng(0)
+    G = rng.standard_normal((c, cols))
+    H = rng.standard_normal((r, cols))
+    t0 = time.perf_counter()
+    ref.matmul(G)
+    t1 = time.perf_counter()
+    ref.matmul_T(H)
+    t2 = time.perf_counter()
+    per_isvd = (sp["q"] + 1) * ((t1 - t0) + (t2 - t1)) * (sp["l"] / cols)
+    blas = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+    cores = max(blas) if blas else 1
+    sample = (f"fp64 oracle products only: one M.G and one M^T.Q on {cols} of l={sp['l']} columns "
+              f"({t2 - t0:.1f} s), scaled x{sp['l'] / cols:.0f} columns x{sp['q'] + 1} applications each; "
+              f"scipy SpMM single-threaded, BLAS {cores} threads")
+    return per_isvd, cores, sample, t2 - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth import get_config, make_features, make_graph, solver_params
+
+    cfg = get_config(args.config)
+    g = make_graph(cfg)
+    X = make_features(cfg["n"], cfg["d"], cfg["seed"]) if cfg["op"] == "NC" else None
+    sp = solver_params(cfg)
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, cores, sample, _ = oracle_sample(cfg, g, X, sp)
+        if i >= args.warmup:
+            times.append(v)
+    v = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n": cfg["n"], "m": cfg["m"], "k": sp["k"], "l": sp["l"], "q": sp["q"]},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ GPU arm
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(workload):
+    """dram read+write bytes per SpMM launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "spmm_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        if d.get("workload") == workload:
+            return d.get("dram_bytes_per_launch")
+    return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2111_06312_b200 import _build
+
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2111_06312_b200 as isvd
+    from synth import get_config, make_features, make_graph, solver_params
+
+    cfg = get_config(args.config)
+    sp = solver_params(cfg)
+    g = make_graph(cfg)
+    X = make_features(cfg["n"], cfg["d"], cfg["seed"]) if cfg["op"] == "NC" else None
+
+    nid = None
+    if world > 1:
+        obj = [isvd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = isvd.Context(local_rank, rank=rank, world=world, nccl_id=nid)
+    rb, nl = isvd.partition(g.n, world, rank)
+    rp, ci = g.row_slice(rb, rb + nl)
+    Xl = None if X is None else np.ascontiguousarray(X[rb : rb + nl])
+
+    def make_op(device_resident=True):
+        if device_resident:
+            graph = isvd.Graph(ctx, g.n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+            if cfg["op"] == "NE":
+                return isvd.NE(graph, sp["weights"], sp["lambda_ones"]), graph
+            return isvd.NC(graph, torch.from_numpy(Xl).cuda(), sp["L"]), graph
+        graph = isvd.Graph(ctx, g.n, rp_pin, ci_pin)
+        if cfg["op"] == "NE":
+            return isvd.NE(graph, sp["weights"], sp["lambda_ones"]), graph
+        return isvd.NC(graph, X_pin, sp["L"]), graph
+
+    p = -1 if cfg["p"] is None else cfg["p"]
+    op, graph = make_op(True)
+    torch.cuda.synchronize()
+
+    def step(profile=True):
+        return op.svd(sp["k"], p, sp["q"], sp["seed"], profile=profile)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    stream = ctx.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    results = [step() for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    spmm_ms = sum(r.ms_spmm for r in results)
+    spmm_n = sum(r.spmm_steps for r in results)
+    spmm_bytes = sum(r.spmm_alg_bytes for r in results)
+    launches = sum(r.kernel_launches for r in results)
+    op.close()
+    graph.close()
+
+    # ---- end-to-end through the public API with host buffers (pinned), H2D + D2H inside
+    rp_pin = torch.from_numpy(rp).pin_memory().numpy()
+    ci_pin = torch.from_numpy(ci).pin_memory().numpy()
+    X_pin = None if Xl is None else torch.from_numpy(Xl).pin_memory().numpy()
+    h2d = rp_pin.nbytes + ci_pin.nbytes + (0 if X_pin is None else X_pin.nbytes)
+    e2e_times = []
+    d2h = 0
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        op2, graph2 = make_op(False)
+        r = op2.svd(sp["k"], p, sp["q"], sp["seed"], host_output=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        d2h = r.U.nbytes + r.V.nbytes + r.S.nbytes
+        op2.close()
+        graph2.close()
+        if i > 0:  # first is a warm-up (allocator, pinned pages)
+            e2e_times.append(t1 - t0)
+    te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample, _ = oracle_sample(cfg, g, X, sp)
+        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        achieved = spmm_bytes / (spmm_ms / 1e3) / 1e9 if spmm_ms > 0 else None
+        per_launch_bytes = spmm_bytes / spmm_n if spmm_n else None
+        line = {
+            "metric": METRIC,
+            "value": ms_max / 1e3,
+            "unit": "s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": False,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic",
+            "config": {
+                "workload": cfg["name"], "op": cfg["op"], "n": cfg["n"], "m": cfg["m"], "k": sp["k"], "l": sp["l"],
+                "q": sp["q"], "parallelism": f"rows-{world}", "l2": "inputs larger than L2 (no flush)",
+                "accumulate": "fp32 storage, fp64 accumulation",
+            },
+            "roofline": {
+                "bound": "hbm", "kernel": "spmm_kernel (+fixup): fused CSR SpMM step",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "peak_source": peak_src,
+                "alg_bytes_per_launch": per_launch_bytes, "launches": spmm_n,
+                "avg_launch_ms": spmm_ms / spmm_n if spmm_n else None,
+                "share_of_step": (spmm_ms / args.steps) / ms if ms > 0 else None,
+                "traffic": load_traffic(cfg["name"]),
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * isvd.h -- C ABI of the B200-native implicit randomized SVD (arXiv 2111.06312).
+ *
+ * Citations: P:n = line n of the paper's text; "Alg. 1" = iSVD
+ * (P:834-863), "Alg. 2" = orthonormalisation, "Eq. 3" = the NE
+ * design matrix, "Eq. 6" = the NC design matrix,
+ * "SymbolicPF" = the product contract shape()/dot()/T().
+ * Readings of unclear passages (O1..O22) are listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every call returns isvd_status.  Nothing throws or aborts across the ABI.
+ *    Arguments and shapes are validated before any work is enqueued; on a
+ *    non-OK status no output buffer is marked valid and isvd_last_error(ctx)
+ *    holds a one-line description.
+ *  - Dense matrices are fp32, ROW-MAJOR, with an explicit leading dimension
+ *    (elements, >= number of columns).  Leading dimensions that are multiples
+ *    of 4 and 16-byte aligned base pointers take the vectorised (float4) paths;
+ *    other values are rejected with ISVD_ERR_INVALID_ARG.
+ *  - Device pointers are CUDA device pointers on the ctx's device.  Work is
+ *    enqueued on the ctx stream; isvd_matmul / isvd_matmul_T / isvd_sample_omega
+ *    return without synchronising.  isvd_svd synchronises once at its end
+ *    (it reads back the singular values and the device status flags).
+ *  - Distributed layout (world > 1, 1-D row partition of the graph): every
+ *    n-long dimension is row-partitioned, rank p owning rows
+ *    [row_begin, row_begin + n_local) with row_begin = p * ceil(n / world)
+ *    (isvd_partition computes it); the short NC dimension c = d (L + 1) is
+ *    replicated on every rank.
+ *  - Threading: one host thread per ctx at a time.  Graphs and ops are
+ *    immutable after creation.
+ *  - Determinism: for a fixed (seed, world) the results are bitwise
+ *    reproducible: no floating-point atomics anywhere, every reduction runs in
+ *    a fixed order.
+ */
+#ifndef ISVD_H_
+#define ISVD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISVD_ABI_VERSION 1
+
+typedef enum {
+  ISVD_OK = 0,
+  ISVD_ERR_INVALID_ARG = 1, /* null pointer, bad flag, bad leading dimension / alignment   */
+  ISVD_ERR_SHAPE = 2,       /* operand dims do not match the op (SymbolicPF shape)   */
+  ISVD_ERR_RANK = 3,        /* k < 1 or k > min(r, c)  (SVD_k defined for k <= rank) */
+  ISVD_ERR_INDEX = 4,       /* col_idx outside [0, n) or row_ptr not monotone               */
+  ISVD_ERR_NONFINITE = 5,   /* NaN / Inf met in an input or produced by the solver          */
+  ISVD_ERR_OOM = 6,         /* device allocation failed                                     */
+  ISVD_ERR_CUDA = 7,        /* a CUDA runtime call failed (text in isvd_last_error)         */
+  ISVD_ERR_NCCL = 8,        /* an NCCL call failed                                          */
+  ISVD_ERR_NOT_PD = 9,      /* Cholesky of Q^T Q broke down even after the shifted retry    */
+  ISVD_ERR_BUSY = 10,       /* object still referenced (graph with live ops)                */
+  ISVD_ERR_UNSUPPORTED = 11 /* valid request this build does not implement                  */
+} isvd_status;
+
+typedef struct isvd_ctx_s* isvd_ctx;
+typedef struct isvd_graph_s* isvd_graph;
+typedef struct isvd_op_s* isvd_op;
+
+/* ------------------------------------------------------------------ context */
+
+/* Create a context on CUDA device `device`, enqueuing on `stream`
+ * (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ * world == 1: single GPU, nccl_unique_id must be NULL.
+ * world  > 1: nccl_unique_id points to the 128-byte ncclUniqueId that rank 0
+ *             created (isvd_nccl_unique_id) and every rank received out of
+ *             band; the call is collective over the `world` ranks.
+ * Device workspace comes from cudaMallocAsync on the ctx stream. */
+isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world,
+                            isvd_ctx* out);
+isvd_status isvd_ctx_destroy(isvd_ctx ctx);
+/* Fill the 128-byte buffer `id_out` with a fresh ncclUniqueId (rank 0 only). */
+isvd_status isvd_nccl_unique_id(void* id_out, size_t id_bytes);
+const char* isvd_status_string(isvd_status s);
+const char* isvd_last_error(isvd_ctx ctx); /* never NULL; "" when no error */
+int isvd_abi_version(void);
+
+/* Row partition used by the distributed layout: rows [*row_begin, *row_begin + *n_local). */
+isvd_status isvd_partition(int64_t n, int world, int rank, int64_t* row_begin, int64_t* n_local);
+
+/* -------------------------------------------------------------------- graph */
+
+enum {
+  ISVD_PTR_DEVICE = 1u,        /* row_ptr / col_idx (or X) are device pointers (else host)       */
+  ISVD_GRAPH_SYMMETRIC = 2u,   /* caller asserts A = A^T (required by this build, see below)     */
+  ISVD_GRAPH_VALIDATE = 4u,    /* check monotone row_ptr and 0 <= col_idx < n (one pass, O(nnz))  */
+  ISVD_BORROW = 8u             /* op keeps the caller's device X instead of copying it            */
+};
+
+/* Unweighted graph A (A_ij = 1 for every stored (i, j), reading O12)
+ * given as this rank's rows in CSR: row_ptr int64[n_local + 1] (row_ptr[0] may
+ * be nonzero: it is subtracted), col_idx int32[nnz] holding GLOBAL node ids.
+ * Rows must hold no self-loop and no duplicate (reading O16; A + I adds the
+ * diagonal itself).  The graph copies both arrays into device memory it owns
+ * (the caller may free its inputs on return) and computes, once, in fp64:
+ *   inv_deg_i = 1 / d_i      (T = D^-1 A; d_i = 0 -> 0, reading O3)
+ *   s_i = (d_i + 1)^-1/2     (A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2)
+ * stored in fp32.  Transposes are never built: this build requires
+ * ISVD_GRAPH_SYMMETRIC (all configs are undirected), so T^T = A D^-1 and
+ * A_hat^T = A_hat are the same CSR with the scale moved; without the flag
+ * the call returns ISVD_ERR_UNSUPPORTED.
+ * Row partition: (row_begin, n_local) must equal isvd_partition(n_global, world, rank). */
+isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
+                              const int64_t* row_ptr, const int32_t* col_idx, uint32_t flags,
+                              isvd_graph* out);
+isvd_status isvd_graph_destroy(isvd_graph g); /* ISVD_ERR_BUSY while ops reference it */
+isvd_status isvd_graph_info(isvd_graph g, int64_t* n_global, int64_t* n_local, int64_t* nnz_local,
+                            int64_t* max_degree);
+
+/* ---------------------------------------------------------------- operators */
+
+typedef enum {
+  ISVD_OP_POWER_SUM = 1,           /* NE, Eq. 3: M = sum_c w_c T^c - lambda_ones 1 1^T          */
+  ISVD_OP_STACKED_PROPAGATION = 2  /* NC, Eq. 6: M = [X | A_hat X | ... | A_hat^L X]            */
+} isvd_op_kind;
+
+typedef struct {
+  isvd_op_kind kind;
+  int32_t num_terms;      /* NE: C >= 1 (number of powers of T); NC: L >= 0 (blocks after X) */
+  const double* weights;  /* NE: host array w_1..w_C (copied).  Configs: 1/C (footnote P:137);
+                             Fig. 1 uses (C-q+1)/(C(C+1)/2) (reading O1).  NC: NULL. */
+  double lambda_ones;     /* NE: coefficient of the rank-1 term -lambda 1 1^T (Eq. 3, P:145;
+                             configs: 1/n).  Applied matrix-free in fp64.           */
+  double lambda_adj;      /* NE: coefficient of +lambda A (Eq. 3's -lambda(1 - A)); must be 0
+                             in this build (ISVD_ERR_UNSUPPORTED otherwise).  */
+  const float* X;         /* NC: this rank's rows of X, n_local x d, row-major, leading dim ldx */
+  int64_t d, ldx;         /* NC: feature width d (>= 1) and leading dimension (multiple of 4) */
+  uint32_t x_flags;       /* NC: ISVD_PTR_DEVICE and/or ISVD_BORROW                           */
+} isvd_op_desc;
+
+/* Define an implicit matrix over graph g.  No O(nnz) work; copies w (and X
+ * unless borrowed).  The op holds a reference on g. */
+isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out);
+/* Global shape (r, c) of M (SymbolicPF.shape): NE (n, n); NC (n, d (L+1)). */
+isvd_status isvd_op_shape(isvd_op op, int64_t* rows, int64_t* cols);
+isvd_status isvd_op_destroy(isvd_op op);
+
+/* out = M . Q   (SymbolicPF.dot; Alg. 1 lines 5/7).
+ *   Q   : device, rows = this rank's share of c (NE: n_local; NC: all c, replicated), w columns.
+ *   out : device, n_local x w.  Must not alias Q.
+ * Accumulation: fp32 products summed in fp64 per row (blocks of 8 neighbours in
+ * fp32, then fp64); the rank-1 term is applied in fp64 before the single
+ * rounding to fp32 (reading O15).  Asynchronous on the ctx stream. */
+isvd_status isvd_matmul(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo);
+/* out = M^T . Q (SymbolicPF.T().dot; Alg. 1 lines 6/9).
+ *   Q   : device, n_local x w.   out : device, NE: n_local x w; NC: c x w (replicated). */
+isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo);
+
+/* -------------------------------------------------------------------- solver */
+
+enum {
+  ISVD_SVD_OMEGA_PROVIDED = 1u, /* start from params.omega instead of the built-in generator   */
+  ISVD_SVD_HOST_OUTPUT = 2u,    /* U and V are host pointers (copied back inside the call)      */
+  ISVD_SVD_NO_GRAPH = 4u,       /* do not capture/replay the solver as a CUDA graph             */
+  ISVD_SVD_FORCE_CHOL_FAIL = 8u,/* fault injection: treat every first Cholesky as broken down   */
+  ISVD_SVD_PROFILE = 16u        /* bracket every SpMM step with CUDA events (report.ms_spmm)     */
+};
+
+typedef struct {
+  int32_t k;            /* target rank, 1 <= k <= min(r, c)                                      */
+  int32_t oversampling; /* p; l = min(k + p, r, c).  p < 0 -> l = min(2k, r, c) (Alg. 1) */
+  int32_t power_iters;  /* q = Alg. 1's `iterations`: 2q + 2 products in total          */
+  uint64_t seed;        /* Omega stream key (reading O11)                                       */
+  uint32_t flags;       /* ISVD_SVD_*                                                           */
+  const float* omega;   /* device c_local x l (ld = round_up(l, 4)) iff ISVD_SVD_OMEGA_PROVIDED */
+} isvd_svd_params;
+
+typedef struct {
+  int32_t l;              /* working width                                                  */
+  int32_t ld;             /* leading dimension used for n x l iterates (round_up(l, 4))      */
+  int32_t chol_fallbacks; /* Cholesky breakdowns repaired by the shifted retry (reading O10) */
+  int32_t jacobi_sweeps;  /* sweeps of the one-sided Jacobi SVD of the l x l factor          */
+  int32_t world;
+  int32_t kernel_launches;/* kernels enqueued by this call (all ours)                        */
+  double ms_total;        /* CUDA-event time of the whole call on the ctx stream            */
+  int32_t spmm_steps;     /* fused SpMM steps (K1 launches, fixup included) in this call     */
+  int32_t pad0;
+  double ms_spmm;         /* ISVD_SVD_PROFILE: summed CUDA-event time of those steps, else 0 */
+  double spmm_alg_bytes;  /* algorithmic bytes of those steps (CSR + scales + gather source
+                             read once + epilogue operand + output)           */
+} isvd_svd_report;
+
+/* Rank-k randomized SVD of M (Alg. 1) with CholeskyQR2
+ * orthonormalisation (Alg. 2 right, applied twice) and the final
+ * SVD of B = (M^T Q)^T computed as CQR2(M^T Q) = Q_W R followed
+ * by a one-sided Jacobi SVD of R^T (B = R^T Q_W^T).
+ *   U : n_local x k (ldu), the left singular vectors (this rank's rows).
+ *   S : HOST double[k], non-increasing (reading O9).
+ *   V : NE: n_local x k (this rank's rows); NC: c x k replicated (ldv).
+ *   Sign rule (reading O9): each (U_j, V_j) is flipped so that the largest-
+ *   magnitude entry of column U_j (lowest global row on ties) is positive.
+ *   rep: nullable.
+ * Device pointers unless ISVD_SVD_HOST_OUTPUT.  Synchronises the ctx stream once. */
+isvd_status isvd_svd(isvd_op op, const isvd_svd_params* params, float* U, int64_t ldu, double* S, float* V,
+                     int64_t ldv, isvd_svd_report* rep);
+
+/* Write the Omega the solver starts from (Alg. 1 line 4; stream of
+ * reading O11: Philox4x32-10 + Box-Muller keyed by the global (row, column))
+ * into device `omega` (this rank's c-rows x l, ld = round_up(l, 4)). */
+isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* omega, int64_t ldo);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISVD_H_ */

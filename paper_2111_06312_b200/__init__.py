@@ -1,0 +1,9 @@
+"""B200-native implicit randomized SVD (arXiv 2111.06312), hot path only.
+
+The product path is the CUDA library ``libisvd.so`` (sm_100a) behind the C ABI
+of ``include/isvd.h``; this package is its thin binding.  It never imports
+``oracle/`` and has no CPU fallback.
+"""
+from .api import NC, NE, Context, Graph, SvdResult, nccl_unique_id, padded, partition, round_up  # noqa: F401
+
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "nccl_unique_id", "partition", "padded", "round_up"]

@@ -1,0 +1,293 @@
+"""Thin Python binding over the isvd C ABI (include/isvd.h).
+
+Argument marshalling only: every arithmetic step of the path runs in the
+CUDA kernels of ``libisvd.so``.  PyTorch supplies device memory (tensors
+whose ``data_ptr`` is passed down), the CUDA stream and, for world > 1, the
+process group used to broadcast the NCCL unique id.
+
+Names follow the paper: ``NE`` is the network-embedding design matrix of
+Eq. 3, ``NC`` the node-classification design
+matrix of Eq. 6 (lines 182-193), ``svd`` is Alg. 1 (lines 834-863).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check
+
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "nccl_unique_id", "partition", "padded", "round_up"]
+
+
+def round_up(x: int, m: int = 4) -> int:
+    return (x + m - 1) // m * m
+
+
+def padded(rows: int, w: int, device, dtype=torch.float32) -> torch.Tensor:
+    """A rows x w view with leading dimension round_up(w, 4) (zero padding), as the ABI wants."""
+    return torch.zeros(max(rows, 1), round_up(w), dtype=dtype, device=device)[:rows, :w]
+
+
+def _ld(t: torch.Tensor) -> int:
+    return t.stride(0)
+
+
+def _as_abi(t: torch.Tensor, device) -> torch.Tensor:
+    """Return t itself if it satisfies the ABI layout (fp32, row stride % 4 == 0, unit column
+    stride, 16-byte aligned, on `device`), else a padded copy."""
+    ok = (t.dtype == torch.float32 and t.device == device and t.dim() == 2 and t.stride(1) == 1
+          and t.stride(0) % 4 == 0 and t.stride(0) >= round_up(t.shape[1]) and t.data_ptr() % 16 == 0)
+    if ok:
+        return t
+    out = padded(t.shape[0], t.shape[1], device)
+    out.copy_(t)
+    return out
+
+
+def partition(n: int, world: int, rank: int):
+    """Rows [row_begin, row_begin + n_local) owned by `rank` (isvd_partition)."""
+    lib = _lib.load()
+    rb, nl = C.c_int64(), C.c_int64()
+    check(lib.isvd_partition(n, world, rank, C.byref(rb), C.byref(nl)), "isvd_partition")
+    return rb.value, nl.value
+
+
+def nccl_unique_id() -> bytes:
+    lib = _lib.load()
+    buf = C.create_string_buffer(128)
+    check(lib.isvd_nccl_unique_id(buf, 128), "isvd_nccl_unique_id")
+    return buf.raw
+
+
+class Context:
+    """isvd_ctx: device, stream and (world > 1) the NCCL communicator."""
+
+    def __init__(self, device: int = 0, stream: "torch.cuda.Stream | None" = None, rank: int = 0, world: int = 1,
+                 nccl_id: "bytes | None" = None):
+        self.lib = _lib.load()
+        self.device = torch.device("cuda", device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        check(self.lib.isvd_ctx_create(device, C.c_void_p(self.stream.cuda_stream), idbuf, rank, world, C.byref(h)),
+              "isvd_ctx_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(self.lib.isvd_ctx_destroy(self.h), "isvd_ctx_destroy", self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Graph:
+    """isvd_graph: this rank's rows of the symmetric, unweighted adjacency A in CSR."""
+
+    def __init__(self, ctx: Context, n: int, row_ptr, col_idx, validate: bool = False):
+        self.ctx = ctx
+        lib = ctx.lib
+        self.n = int(n)
+        self.row_begin, self.n_local = partition(self.n, ctx.world, ctx.rank)
+        flags = _lib.ISVD_GRAPH_SYMMETRIC | (_lib.ISVD_GRAPH_VALIDATE if validate else 0)
+        if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
+            rp = row_ptr.to(torch.int64).contiguous()
+            ci = col_idx.to(torch.int32).contiguous()
+            flags |= _lib.ISVD_PTR_DEVICE
+            keep = (rp, ci)
+            prp, pci = rp.data_ptr(), ci.data_ptr()
+        else:
+            rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+            ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+            keep = (rp, ci)
+            prp, pci = rp.ctypes.data, ci.ctypes.data
+        if len(keep[0]) != self.n_local + 1:
+            raise ValueError(f"row_ptr must have n_local + 1 = {self.n_local + 1} entries for rank {ctx.rank}")
+        h = C.c_void_p()
+        check(lib.isvd_graph_create(ctx.h, self.n, self.row_begin, self.n_local, C.c_void_p(prp), C.c_void_p(pci),
+                                    flags, C.byref(h)), "isvd_graph_create", ctx.h)
+        self.h = h
+
+    def info(self):
+        a = [C.c_int64() for _ in range(4)]
+        check(self.ctx.lib.isvd_graph_info(self.h, *[C.byref(x) for x in a]), "isvd_graph_info", self.ctx.h)
+        return dict(n=a[0].value, n_local=a[1].value, nnz_local=a[2].value, max_degree=a[3].value)
+
+    def close(self):
+        if self.h:
+            check(self.ctx.lib.isvd_graph_destroy(self.h), "isvd_graph_destroy", self.ctx.h)
+            self.h = None
+
+
+@dataclass
+class SvdResult:
+    U: object       # n_local x k (torch cuda tensor, or numpy with host_output)
+    S: np.ndarray   # k, fp64, non-increasing
+    V: object       # NE: n_local x k; NC: c x k
+    l: int
+    chol_fallbacks: int
+    jacobi_sweeps: int
+    kernel_launches: int
+    ms_total: float
+    spmm_steps: int = 0
+    ms_spmm: float = 0.0
+    spmm_alg_bytes: float = 0.0
+
+
+class _Operator:
+    def __init__(self, graph: Graph, desc: _lib.OpDesc, keep=()):
+        self.graph = graph
+        self.ctx = graph.ctx
+        self._keep = keep
+        h = C.c_void_p()
+        check(self.ctx.lib.isvd_op_define(graph.h, C.byref(desc), C.byref(h)), "isvd_op_define", self.ctx.h)
+        self.h = h
+        r, c = C.c_int64(), C.c_int64()
+        check(self.ctx.lib.isvd_op_shape(h, C.byref(r), C.byref(c)), "isvd_op_shape", self.ctx.h)
+        self.shape = (r.value, c.value)
+
+    # rows of the operand of M . Q held by this rank (NE: partitioned; NC: all c)
+    def c_rows(self) -> int:
+        raise NotImplementedError
+
+    def close(self):
+        if self.h:
+            check(self.ctx.lib.isvd_op_destroy(self.h), "isvd_op_destroy", self.ctx.h)
+            self.h = None
+
+    def matmul(self, Q: torch.Tensor, out: "torch.Tensor | None" = None) -> torch.Tensor:
+        """M . Q (SymbolicPF.dot)."""
+        dev = self.ctx.device
+        Q = _as_abi(Q, dev)
+        w = Q.shape[1]
+        if out is None:
+            out = padded(self.graph.n_local, w, dev)
+        check(self.ctx.lib.isvd_matmul(self.h, C.c_void_p(Q.data_ptr()), w, _ld(Q), C.c_void_p(out.data_ptr()),
+                                       _ld(out)), "isvd_matmul", self.ctx.h)
+        return out
+
+    def matmul_T(self, Q: torch.Tensor, out: "torch.Tensor | None" = None) -> torch.Tensor:
+        """M^T . Q (SymbolicPF.T().dot)."""
+        dev = self.ctx.device
+        Q = _as_abi(Q, dev)
+        w = Q.shape[1]
+        if out is None:
+            out = padded(self.c_rows(), w, dev)
+        check(self.ctx.lib.isvd_matmul_T(self.h, C.c_void_p(Q.data_ptr()), w, _ld(Q), C.c_void_p(out.data_ptr()),
+                                         _ld(out)), "isvd_matmul_T", self.ctx.h)
+        return out
+
+    def _params(self, k, oversampling, power_iters, seed, flags=0, omega=None):
+        p = _lib.SvdParams()
+        p.k, p.oversampling, p.power_iters, p.seed, p.flags = int(k), int(oversampling), int(power_iters), int(seed), flags
+        p.omega = omega.data_ptr() if omega is not None else None
+        return p
+
+    def working_width(self, k: int, oversampling: int) -> int:
+        r, c = self.shape
+        l = 2 * k if oversampling < 0 else k + oversampling
+        return min(l, r, c)
+
+    def sample_omega(self, k: int, oversampling: int, seed: int) -> torch.Tensor:
+        """The Omega Alg. 1 starts from, this rank's rows, from the library's generator."""
+        l = self.working_width(k, oversampling)
+        om = padded(self.c_rows(), l, self.ctx.device)
+        p = self._params(k, oversampling, 0, seed)
+        check(self.ctx.lib.isvd_sample_omega(self.h, C.byref(p), C.c_void_p(om.data_ptr()), _ld(om)),
+              "isvd_sample_omega", self.ctx.h)
+        return om
+
+    def svd(self, k: int, oversampling: int = -1, power_iters: int = 2, seed: int = 0, host_output: bool = False,
+            omega: "torch.Tensor | None" = None, force_chol_fail: bool = False, profile: bool = False,
+            out=None) -> SvdResult:
+        """Rank-k implicit SVD (Alg. 1) -> U (n_local x k), S (k), V."""
+        dev = self.ctx.device
+        kk = round_up(k)
+        flags = 0
+        if host_output:
+            flags |= _lib.ISVD_SVD_HOST_OUTPUT
+            U = np.zeros((max(self.graph.n_local, 1), kk), dtype=np.float32)
+            V = np.zeros((max(self.c_rows(), 1), kk), dtype=np.float32)
+            pu, pv, ldu, ldv = U.ctypes.data, V.ctypes.data, kk, kk
+        else:
+            if out is not None:
+                U, V = out
+            else:
+                U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, device=dev)
+                V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, device=dev)
+            pu, pv, ldu, ldv = U.data_ptr(), V.data_ptr(), U.stride(0), V.stride(0)
+        if omega is not None:
+            flags |= _lib.ISVD_SVD_OMEGA_PROVIDED
+            omega = _as_abi(omega, dev)
+        if force_chol_fail:
+            flags |= _lib.ISVD_SVD_FORCE_CHOL_FAIL
+        if profile:
+            flags |= _lib.ISVD_SVD_PROFILE
+        p = self._params(k, oversampling, power_iters, seed, flags, omega)
+        S = np.zeros(k, dtype=np.float64)
+        rep = _lib.SvdReport()
+        check(self.ctx.lib.isvd_svd(self.h, C.byref(p), C.c_void_p(pu), ldu,
+                                    S.ctypes.data_as(C.POINTER(C.c_double)), C.c_void_p(pv), ldv, C.byref(rep)),
+              "isvd_svd", self.ctx.h)
+        U = U[: self.graph.n_local, :k]
+        V = V[: self.c_rows(), :k]
+        return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
+                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes)
+
+
+class NE(_Operator):
+    """M = sum_{c=1..C} w_c T^c - lambda_ones 1 1^T, T = D^-1 A   (Eq. 3)."""
+
+    def __init__(self, graph: Graph, weights, lambda_ones: float, lambda_adj: float = 0.0):
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        d = _lib.OpDesc()
+        d.kind = _lib.ISVD_OP_POWER_SUM
+        d.num_terms = int(w.size)
+        d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
+        d.lambda_ones = float(lambda_ones)
+        d.lambda_adj = float(lambda_adj)
+        super().__init__(graph, d, keep=(w,))
+
+    def c_rows(self) -> int:
+        return self.graph.n_local
+
+
+class NC(_Operator):
+    """M = [X | A_hat X | ... | A_hat^L X],  A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2   (Eq. 6).
+
+    X: this rank's rows (n_local x d), a CUDA tensor (borrowed when already in ABI layout)
+    or a host numpy array (copied)."""
+
+    def __init__(self, graph: Graph, X, L: int):
+        d = _lib.OpDesc()
+        d.kind = _lib.ISVD_OP_STACKED_PROPAGATION
+        d.num_terms = int(L)
+        if isinstance(X, torch.Tensor):
+            Xt = _as_abi(X, graph.ctx.device)
+            d.X, d.d, d.ldx = Xt.data_ptr(), Xt.shape[1], _ld(Xt)
+            d.x_flags = _lib.ISVD_PTR_DEVICE | _lib.ISVD_BORROW
+            keep = (Xt,)
+        else:
+            Xn = np.asarray(X, dtype=np.float32)
+            ldx = round_up(Xn.shape[1])
+            if Xn.flags.c_contiguous and ldx == Xn.shape[1]:
+                Xp = Xn  # already in ABI layout (e.g. a pinned host buffer): copied once by the library
+            else:
+                Xp = np.zeros((Xn.shape[0], ldx), dtype=np.float32)
+                Xp[:, : Xn.shape[1]] = Xn
+            d.X, d.d, d.ldx, d.x_flags = Xp.ctypes.data, Xn.shape[1], ldx, 0
+            keep = (Xp,)
+        self.d, self.L = int(d.d), int(L)
+        super().__init__(graph, d, keep=keep)
+
+    def c_rows(self) -> int:
+        return self.d * (self.L + 1)

@@ -1,0 +1,1018 @@
+// C ABI of the isvd library (include/isvd.h): context, graph, operators,
+// matrix-free products and the Alg. 1 solver driver.
+//
+// Host side only enqueues work: every arithmetic step of the path runs in the
+// CUDA kernels of spmm.cu / dense.cu / smallmat.cu / omega.cu.  NCCL (over
+// NVLink/NVSwitch) carries the two exchanges of the row-partitioned layout:
+// an all-gather of each SpMM gather source and an fp64 all-reduce of the
+// Gram / column-sum / X^T Z partials.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/isvd.h"
+#include "common.cuh"
+
+using namespace isvd;
+
+namespace isvd {
+thread_local int64_t g_launches = 0;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct isvd_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int num_sms = 148;
+  std::string last_error;
+  DevStatus* status = nullptr;  // device
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::atomic<int> live_graphs{0};
+  // SpMM accounting of the current isvd_svd call
+  bool profiling = false;
+  int spmm_steps = 0;
+  double spmm_alg_bytes = 0.0;
+  std::vector<cudaEvent_t> prof_events;  // pairs
+};
+
+struct isvd_graph_s {
+  isvd_ctx ctx = nullptr;
+  int64_t n = 0, row_begin = 0, n_local = 0, n_pad = 0, nnz = 0, max_deg = 0;
+  int64_t* row_ptr = nullptr;  // device, rebased to 0
+  int32_t* col_idx = nullptr;  // device
+  float* inv_deg = nullptr;    // 1/d (0 for d = 0)
+  float* s = nullptr;          // (d+1)^-1/2
+  float* s2 = nullptr;         // (d+1)^-1
+  float* rs = nullptr;         // (d+1)^1/2
+  SpmmPlan plan;
+  std::vector<void*> allocs;
+  std::atomic<int> refs{0};
+};
+
+// Workspace of one op for one width: grown on demand, never freed until op destroy.
+struct Workspace {
+  int64_t wpad = 0;
+  std::vector<DevBuf> bufs;
+};
+
+struct SolverWs {
+  int64_t key_l = -1, key_k = -1;
+  std::vector<void*> allocs;
+  float *Qc = nullptr, *Qc2 = nullptr, *Yr = nullptr, *Yr2 = nullptr, *Rinv32 = nullptr, *Ub = nullptr,
+        *Vb = nullptr, *Utmp = nullptr, *Vtmp = nullptr, *sgn = nullptr;
+  double *gram = nullptr, *Ra = nullptr, *Rb = nullptr, *Rc = nullptr, *Rab = nullptr, *Rfin = nullptr,
+         *chol_ws = nullptr, *jac_ws = nullptr, *sigma = nullptr, *cand = nullptr, *cand_all = nullptr,
+         *absmax_ws = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_key = 0;
+  bool graph_broken = false;
+};
+
+struct isvd_op_s {
+  isvd_graph g = nullptr;
+  isvd_op_kind kind = ISVD_OP_POWER_SUM;
+  int terms = 0;
+  std::vector<double> w;
+  double lambda_ones = 0.0;
+  const float* X = nullptr;
+  int64_t d = 0, ldx = 0;
+  bool own_x = false;
+  // product workspace (sized for the widest request so far)
+  int64_t ws_wpad = 0;
+  std::vector<void*> ws_allocs;
+  float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
+  double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
+  SolverWs sws;
+};
+
+// ------------------------------------------------------------------ helpers
+namespace {
+
+struct Fail {
+  isvd_status st;
+};
+
+void set_err(isvd_ctx ctx, const std::string& m) {
+  if (ctx) ctx->last_error = m;
+}
+
+#define CK(call)                                                                                              \
+  do {                                                                                                        \
+    cudaError_t e_ = (call);                                                                                  \
+    if (e_ != cudaSuccess) {                                                                                  \
+      set_err(ctx, std::string(#call) + ": " + cudaGetErrorString(e_));                                       \
+      throw Fail{e_ == cudaErrorMemoryAllocation ? ISVD_ERR_OOM : ISVD_ERR_CUDA};                             \
+    }                                                                                                         \
+  } while (0)
+
+#define NK(call)                                                                                              \
+  do {                                                                                                        \
+    ncclResult_t r_ = (call);                                                                                 \
+    if (r_ != ncclSuccess) {                                                                                  \
+      set_err(ctx, std::string(#call) + ": " + ncclGetErrorString(r_));                                       \
+      throw Fail{ISVD_ERR_NCCL};                                                                              \
+    }                                                                                                         \
+  } while (0)
+
+#define REQ(cond, code, msg)                                                                                  \
+  do {                                                                                                        \
+    if (!(cond)) {                                                                                            \
+      set_err(ctx, msg);                                                                                      \
+      throw Fail{code};                                                                                       \
+    }                                                                                                         \
+  } while (0)
+
+void* dmalloc(isvd_ctx ctx, size_t bytes, std::vector<void*>& list) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  CK(cudaMalloc(&p, bytes));
+  list.push_back(p);
+  // padding columns of every iterate must read as zero: workspaces start cleared
+  CK(cudaMemset(p, 0, bytes));
+  return p;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+void partition(int64_t n, int world, int rank, int64_t* rb, int64_t* nl) {
+  int64_t chunk = (n + world - 1) / world;
+  int64_t b = std::min<int64_t>(n, chunk * rank);
+  int64_t e = std::min<int64_t>(n, b + chunk);
+  *rb = b;
+  *nl = e - b;
+}
+
+// --------------------------------------------------------------- collectives
+void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld) {
+  if (ctx->world == 1) return;
+  size_t count = (size_t)g->n_pad * ld;
+  NK(ncclAllGather(full + (size_t)ctx->rank * count, full, count, ncclFloat, ctx->comm, ctx->stream));
+}
+
+void allreduce_f64(isvd_ctx ctx, double* buf, size_t count) {
+  if (ctx->world == 1) return;
+  NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+// ------------------------------------------------------------------ op workspace
+void ensure_op_ws(isvd_op op, int64_t wpad) {
+  isvd_graph g = op->g;
+  isvd_ctx ctx = g->ctx;
+  if (wpad <= op->ws_wpad) return;
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (void* p : op->ws_allocs) cudaFree(p);
+  op->ws_allocs.clear();
+  int64_t n_full = g->n_pad * ctx->world;
+  size_t full_bytes = sizeof(float) * (size_t)n_full * wpad;
+  op->full_a = (float*)dmalloc(ctx, full_bytes, op->ws_allocs);
+  op->full_b = (float*)dmalloc(ctx, full_bytes, op->ws_allocs);
+  op->full_c = (float*)dmalloc(ctx, full_bytes, op->ws_allocs);
+  op->ptmp = (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs);
+  op->partial = (float*)dmalloc(ctx, sizeof(float) * (size_t)spmm_ws_floats(g->plan, wpad), op->ws_allocs);
+  op->colsum = (double*)dmalloc(ctx, sizeof(double) * wpad, op->ws_allocs);
+  op->colsum_ws = (double*)dmalloc(ctx, sizeof(double) * colsum_ws_doubles(g->n_local, wpad), op->ws_allocs);
+  int64_t ka = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : wpad;
+  int64_t atb = std::max(atb_ws_doubles(g->n_local, ka, wpad, ctx->num_sms),
+                         atb_ws_doubles(g->n_local, wpad, wpad, ctx->num_sms));
+  op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
+  int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
+  op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
+  op->ws_wpad = wpad;
+}
+
+SpmmArgs spmm_base(const isvd_graph_s* g, int64_t wpad) {
+  SpmmArgs a{};
+  a.col_idx = g->col_idx;
+  a.row_offset = g->row_begin;
+  a.post_coef = 1.f;
+  a.term_coef = 1.f;
+  a.wpad = wpad;
+  return a;
+}
+
+void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
+  const isvd_graph_s* g = op->g;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->profiling) {
+    size_t i = 2 * (size_t)ctx->spmm_steps;
+    while (ctx->prof_events.size() < i + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->prof_events.push_back(e);
+    }
+    e0 = ctx->prof_events[i];
+    e1 = ctx->prof_events[i + 1];
+    CK(cudaEventRecord(e0, ctx->stream));
+  }
+  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream));
+  if (e1) CK(cudaEventRecord(e1, ctx->stream));
+  // algorithmic bytes of the step: CSR, scale vectors, the gather source read
+  // once (all n rows), the epilogue operand T, the output
+  double nl = (double)g->n_local, w = (double)a.wpad;
+  double b = 8.0 * (nl + 1) + 4.0 * (double)g->nnz + 4.0 * (double)g->n * w + 4.0 * nl * w;
+  if (a.post_vec) b += 4.0 * nl;
+  if (a.term_vec) b += 4.0 * nl;
+  if (a.T) b += 4.0 * nl * w;
+  ctx->spmm_alg_bytes += b;
+  ctx->spmm_steps++;
+}
+
+// rows [row_begin, row_begin + n_local) of a full-height buffer
+float* slice(const isvd_graph_s* g, float* full, int64_t ld) { return full + (size_t)g->row_begin * ld; }
+
+// ----------------------------------------------------------------- NE products
+// M Q = sum_c w_c T^c Q - lambda 1 (1^T Q), T = D^-1 A   (Eq. 3)
+// Horner: H_C = w_C Q; H_c = w_c Q + D^-1 A H_{c+1}; M Q = D^-1 A H_1 - lambda 1 cs^T.
+void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+  isvd_graph g = op->g;
+  const int C = op->terms;
+  CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));
+  allreduce_f64(ctx, op->colsum, wpad);
+  const float* src = Q;
+  int64_t lds = ldq;
+  if (ctx->world > 1) {
+    CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr, ctx->stream));
+    allgather_rows(ctx, g, op->full_a, wpad);
+    src = op->full_a;
+    lds = wpad;
+  }
+  float* bufs[2] = {op->full_b, op->full_c};
+  for (int c = C - 1; c >= 1; --c) {
+    float* dst_full = bufs[c & 1];
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = src; a.ldy = lds;
+    a.post_vec = g->inv_deg;
+    a.post_coef = (c == C - 1) ? (float)op->w[C - 1] : 1.f;
+    a.T = Q; a.ldt = ldq; a.term_coef = (float)op->w[c - 1];
+    a.out = slice(g, dst_full, wpad); a.ldo = wpad;
+    spmm(ctx, op, a);
+    allgather_rows(ctx, g, dst_full, wpad);
+    src = dst_full;
+    lds = wpad;
+  }
+  SpmmArgs a = spmm_base(g, wpad);
+  a.Y = src; a.ldy = lds;
+  a.post_vec = g->inv_deg;
+  a.post_coef = (C == 1) ? (float)op->w[0] : 1.f;
+  a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
+  a.out = out; a.ldo = ldo;
+  spmm(ctx, op, a);
+}
+
+// M^T Q = sum_c w_c (A D^-1)^c Q - lambda 1 (1^T Q)   (T^T = A D^-1 for symmetric A)
+// Horner: Ht_C = D^-1 w_C Q; Ht_c = D^-1 (w_c Q + A Ht_{c+1}); M^T Q = A Ht_1 - lambda 1 cs^T.
+void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+  isvd_graph g = op->g;
+  const int C = op->terms;
+  CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));
+  allreduce_f64(ctx, op->colsum, wpad);
+  CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, g->inv_deg, (float)op->w[C - 1],
+                       nullptr, ctx->stream));
+  allgather_rows(ctx, g, op->full_a, wpad);
+  const float* src = op->full_a;
+  float* bufs[2] = {op->full_b, op->full_c};
+  for (int c = C - 1; c >= 1; --c) {
+    float* dst_full = bufs[c & 1];
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = src; a.ldy = wpad;
+    a.post_vec = g->inv_deg;
+    a.T = Q; a.ldt = ldq; a.term_vec = g->inv_deg; a.term_coef = (float)op->w[c - 1];
+    a.out = slice(g, dst_full, wpad); a.ldo = wpad;
+    spmm(ctx, op, a);
+    allgather_rows(ctx, g, dst_full, wpad);
+    src = dst_full;
+  }
+  SpmmArgs a = spmm_base(g, wpad);
+  a.Y = src; a.ldy = wpad;
+  a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
+  a.out = out; a.ldo = ldo;
+  spmm(ctx, op, a);
+}
+
+// ----------------------------------------------------------------- NC products
+// M G = sum_j A_hat^j X G_j  (Eq. 6), Horner from the deepest block, iterates stored
+// pre-scaled (Yt = s Y) so the gather needs no per-neighbour scale:
+//   Yt_L = s (X G_L);  Yt_j = s (X G_j) + s^2 ((A+I) Yt_{j+1});  out = X G_0 + s ((A+I) Yt_1).
+void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad) {
+  isvd_graph g = op->g;
+  const int L = op->terms;
+  const int64_t d = op->d;
+  if (L == 0) {
+    CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
+                      ctx->stream));
+    return;
+  }
+  float* bufs[2] = {op->full_a, op->full_b};
+  float* cur = bufs[L & 1];
+  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, slice(g, cur, wpad), wpad, g->n_local, wpad, d,
+                    g->s, 1.f, false, nullptr, ctx->stream));
+  allgather_rows(ctx, g, cur, wpad);
+  for (int j = L - 1; j >= 1; --j) {
+    CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)j * d * ldgm, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr,
+                      1.f, false, nullptr, ctx->stream));
+    float* dst = bufs[j & 1];
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
+    a.post_vec = g->s2;
+    a.T = op->ptmp; a.ldt = wpad; a.term_vec = g->s;
+    a.out = slice(g, dst, wpad); a.ldo = wpad;
+    spmm(ctx, op, a);
+    allgather_rows(ctx, g, dst, wpad);
+    cur = dst;
+  }
+  CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
+                    ctx->stream));
+  SpmmArgs a = spmm_base(g, wpad);
+  a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
+  a.post_vec = g->s;
+  a.T = out; a.ldt = ldo;  // in-place accumulate: each element is read then written by one thread
+  a.out = out; a.ldo = ldo;
+  spmm(ctx, op, a);
+}
+
+// M^T Q: block j = X^T A_hat^j Q.  Zt_0 = s Q; Zt_{j+1} = s^2 ((A+I) Zt_j); block j = X^T diag(1/s) Zt_j.
+void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+  isvd_graph g = op->g;
+  const int L = op->terms;
+  const int64_t d = op->d;
+  CK(launch_atb(op->X, op->ldx, Q, ldq, g->n_local, d, wpad, nullptr, false, op->atb_ws, op->blk64, wpad, nullptr, 0,
+                ctx->num_sms, nullptr, ctx->stream));
+  if (L > 0) {
+    float* bufs[2] = {op->full_a, op->full_b};
+    CK(launch_scale_rows(Q, ldq, slice(g, bufs[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream));
+    allgather_rows(ctx, g, bufs[0], wpad);
+    for (int j = 1; j <= L; ++j) {
+      float* src = bufs[(j - 1) & 1];
+      float* dst = bufs[j & 1];
+      SpmmArgs a = spmm_base(g, wpad);
+      a.Y = src; a.ldy = wpad; a.self_coef = 1.f;
+      a.post_vec = g->s2;
+      a.out = slice(g, dst, wpad); a.ldo = wpad;
+      spmm(ctx, op, a);
+      if (j < L) allgather_rows(ctx, g, dst, wpad);
+      CK(launch_atb(op->X, op->ldx, slice(g, dst, wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
+                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream));
+    }
+  }
+  const int64_t c = d * (L + 1);
+  allreduce_f64(ctx, op->blk64, (size_t)c * wpad);
+  CK(launch_f64_to_f32(op->blk64, wpad, out, ldo, c, wpad, ctx->stream));
+}
+
+void op_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+  isvd_ctx ctx = op->g->ctx;
+  ensure_op_ws(op, wpad);
+  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad);
+  else nc_matmul(ctx, op, Q, ldq, out, ldo, wpad);
+}
+
+void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+  isvd_ctx ctx = op->g->ctx;
+  ensure_op_ws(op, wpad);
+  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad);
+  else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad);
+}
+
+void op_shape(const isvd_op_s* op, int64_t* r, int64_t* c) {
+  *r = op->g->n;
+  *c = op->kind == ISVD_OP_POWER_SUM ? op->g->n : op->d * (op->terms + 1);
+}
+
+// rows of the c-side (columns of M) held by this rank
+int64_t c_rows_local(const isvd_op_s* op) {
+  return op->kind == ISVD_OP_POWER_SUM ? op->g->n_local : op->d * (op->terms + 1);
+}
+
+template <typename F>
+isvd_status guarded(isvd_ctx ctx, F&& f) {
+  try {
+    f();
+    return ISVD_OK;
+  } catch (const Fail& e) {
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    set_err(ctx, "host allocation failed");
+    return ISVD_ERR_OOM;
+  } catch (...) {
+    set_err(ctx, "unexpected exception");
+    return ISVD_ERR_INVALID_ARG;
+  }
+}
+
+}  // namespace
+
+// =================================================================== context
+extern "C" {
+
+int isvd_abi_version(void) { return ISVD_ABI_VERSION; }
+
+const char* isvd_status_string(isvd_status s) {
+  switch (s) {
+    case ISVD_OK: return "ok";
+    case ISVD_ERR_INVALID_ARG: return "invalid argument";
+    case ISVD_ERR_SHAPE: return "shape mismatch";
+    case ISVD_ERR_RANK: return "rank out of range";
+    case ISVD_ERR_INDEX: return "index out of range";
+    case ISVD_ERR_NONFINITE: return "non-finite value";
+    case ISVD_ERR_OOM: return "out of memory";
+    case ISVD_ERR_CUDA: return "CUDA error";
+    case ISVD_ERR_NCCL: return "NCCL error";
+    case ISVD_ERR_NOT_PD: return "Cholesky breakdown";
+    case ISVD_ERR_BUSY: return "busy";
+    case ISVD_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+const char* isvd_last_error(isvd_ctx ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+isvd_status isvd_partition(int64_t n, int world, int rank, int64_t* row_begin, int64_t* n_local) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !row_begin || !n_local) return ISVD_ERR_INVALID_ARG;
+  partition(n, world, rank, row_begin, n_local);
+  return ISVD_OK;
+}
+
+isvd_status isvd_nccl_unique_id(void* id_out, size_t id_bytes) {
+  if (!id_out || id_bytes < sizeof(ncclUniqueId)) return ISVD_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return ISVD_ERR_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return ISVD_OK;
+}
+
+isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world, isvd_ctx* out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return ISVD_ERR_INVALID_ARG;
+  if ((world > 1) != (nccl_unique_id != nullptr)) return ISVD_ERR_INVALID_ARG;
+  *out = nullptr;
+  isvd_ctx ctx = new (std::nothrow) isvd_ctx_s();
+  if (!ctx) return ISVD_ERR_OOM;
+  isvd_status st = guarded(ctx, [&] {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    REQ(device >= 0 && device < ndev, ISVD_ERR_INVALID_ARG, "device out of range");
+    ctx->device = device;
+    DeviceGuard dg(device);
+    ctx->stream = (cudaStream_t)stream;
+    ctx->rank = rank;
+    ctx->world = world;
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int major = 0;
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    REQ(major == 10, ISVD_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
+    CK(cudaMalloc(&ctx->status, sizeof(DevStatus)));
+    CK(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
+    CK(cudaEventCreate(&ctx->ev0));
+    CK(cudaEventCreate(&ctx->ev1));
+    if (world > 1) {
+      ncclUniqueId id;
+      memcpy(&id, nccl_unique_id, sizeof(id));
+      NK(ncclCommInitRank(&ctx->comm, world, id, rank));
+    }
+  });
+  if (st != ISVD_OK) {
+    fprintf(stderr, "isvd_ctx_create: %s\n", ctx->last_error.c_str());
+    if (ctx->status) cudaFree(ctx->status);
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return ISVD_OK;
+}
+
+isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
+  if (!ctx) return ISVD_ERR_INVALID_ARG;
+  if (ctx->live_graphs.load() > 0) return ISVD_ERR_BUSY;
+  DeviceGuard dg(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->status) cudaFree(ctx->status);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  delete ctx;
+  return ISVD_OK;
+}
+
+// ===================================================================== graph
+isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
+                              const int64_t* row_ptr, const int32_t* col_idx, uint32_t flags, isvd_graph* out) {
+  if (!ctx || !out) return ISVD_ERR_INVALID_ARG;
+  *out = nullptr;
+  isvd_graph g = new (std::nothrow) isvd_graph_s();
+  if (!g) return ISVD_ERR_OOM;
+  isvd_status st = guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    REQ(n_global >= 1 && n_global < (int64_t)INT32_MAX, ISVD_ERR_INVALID_ARG, "n must be in [1, 2^31-1)");
+    REQ(row_ptr != nullptr, ISVD_ERR_INVALID_ARG, "row_ptr is null");
+    REQ((flags & ~(uint32_t)(ISVD_PTR_DEVICE | ISVD_GRAPH_SYMMETRIC | ISVD_GRAPH_VALIDATE)) == 0,
+        ISVD_ERR_INVALID_ARG, "unknown graph flag");
+    REQ(flags & ISVD_GRAPH_SYMMETRIC, ISVD_ERR_UNSUPPORTED,
+        "directed graphs need an explicit transpose (not built in this version); pass ISVD_GRAPH_SYMMETRIC");
+    int64_t rb, nl;
+    partition(n_global, ctx->world, ctx->rank, &rb, &nl);
+    REQ(rb == row_begin && nl == n_local, ISVD_ERR_INVALID_ARG,
+        "row partition must equal isvd_partition(n, world, rank)");
+    const bool dev = flags & ISVD_PTR_DEVICE;
+    std::vector<int64_t> rp(n_local + 1);
+    if (dev) CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
+    else memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1));
+    const int64_t base = rp[0];
+    for (auto& v : rp) v -= base;
+    for (int64_t i = 0; i < n_local; ++i)
+      REQ(rp[i + 1] >= rp[i], ISVD_ERR_INDEX, "row_ptr is not monotone");
+    const int64_t nnz = rp[n_local];
+    REQ(nnz == 0 || col_idx != nullptr, ISVD_ERR_INVALID_ARG, "col_idx is null");
+    g->ctx = ctx;
+    g->n = n_global;
+    g->row_begin = row_begin;
+    g->n_local = n_local;
+    g->n_pad = (n_global + ctx->world - 1) / ctx->world;
+    g->nnz = nnz;
+    g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
+    CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
+    g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), g->allocs);
+    if (nnz > 0)
+      CK(cudaMemcpy(g->col_idx, col_idx + base, sizeof(int32_t) * nnz,
+                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    if (flags & ISVD_GRAPH_VALIDATE) {
+      std::vector<int32_t> ci(nnz);
+      if (nnz) CK(cudaMemcpy(ci.data(), g->col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+      for (int64_t e = 0; e < nnz; ++e)
+        REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
+    }
+    // degrees (integers) -> scale vectors computed once in fp64, stored fp32 (reading O3)
+    std::vector<float> inv(n_local), s(n_local), s2(n_local), rs(n_local);
+    int64_t maxd = 0;
+    for (int64_t i = 0; i < n_local; ++i) {
+      int64_t d = rp[i + 1] - rp[i];
+      maxd = std::max(maxd, d);
+      inv[i] = d > 0 ? (float)(1.0 / (double)d) : 0.f;
+      s[i] = (float)(1.0 / std::sqrt((double)d + 1.0));
+      s2[i] = (float)(1.0 / ((double)d + 1.0));
+      rs[i] = (float)std::sqrt((double)d + 1.0);
+    }
+    g->max_deg = maxd;
+    size_t nb = sizeof(float) * std::max<int64_t>(n_local, 1);
+    g->inv_deg = (float*)dmalloc(ctx, nb, g->allocs);
+    g->s = (float*)dmalloc(ctx, nb, g->allocs);
+    g->s2 = (float*)dmalloc(ctx, nb, g->allocs);
+    g->rs = (float*)dmalloc(ctx, nb, g->allocs);
+    if (n_local > 0) {
+      CK(cudaMemcpy(g->inv_deg, inv.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(g->s, s.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(g->s2, s2.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(g->rs, rs.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
+    }
+    // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
+    // split, their partial sums combined by the fixup pass in segment order.
+    std::vector<int32_t> seg_row, seg_len, seg_slot, split_row, split_slot0, split_nslot;
+    std::vector<int64_t> seg_beg;
+    seg_row.reserve(n_local);
+    int32_t slots = 0;
+    for (int64_t i = 0; i < n_local; ++i) {
+      int64_t d = rp[i + 1] - rp[i];
+      if (d <= kSegEdges) {
+        seg_row.push_back((int32_t)i);
+        seg_beg.push_back(rp[i]);
+        seg_len.push_back((int32_t)d);
+        seg_slot.push_back(-1);
+      } else {
+        int32_t ns = (int32_t)((d + kSegEdges - 1) / kSegEdges);
+        split_row.push_back((int32_t)i);
+        split_slot0.push_back(slots);
+        split_nslot.push_back(ns);
+        for (int32_t t = 0; t < ns; ++t) {
+          int64_t b = rp[i] + (int64_t)t * kSegEdges;
+          int64_t e = std::min(rp[i + 1], b + kSegEdges);
+          seg_row.push_back((int32_t)i);
+          seg_beg.push_back(b);
+          seg_len.push_back((int32_t)(e - b));
+          seg_slot.push_back(slots + t);
+        }
+        slots += ns;
+      }
+    }
+    SpmmPlan& p = g->plan;
+    p.n_local = n_local;
+    p.n_seg = (int64_t)seg_row.size();
+    p.n_split_rows = (int64_t)split_row.size();
+    p.n_slots = slots;
+    auto up32 = [&](const std::vector<int32_t>& v) {
+      int32_t* d = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<size_t>(v.size(), 1), g->allocs);
+      if (!v.empty()) CK(cudaMemcpy(d, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice));
+      return d;
+    };
+    p.seg_row = up32(seg_row);
+    p.seg_len = up32(seg_len);
+    p.seg_slot = up32(seg_slot);
+    p.split_row = up32(split_row);
+    p.split_slot0 = up32(split_slot0);
+    p.split_nslot = up32(split_nslot);
+    p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<size_t>(seg_beg.size(), 1), g->allocs);
+    if (!seg_beg.empty())
+      CK(cudaMemcpy(p.seg_beg, seg_beg.data(), sizeof(int64_t) * seg_beg.size(), cudaMemcpyHostToDevice));
+  });
+  if (st != ISVD_OK) {
+    for (void* p : g->allocs) cudaFree(p);
+    delete g;
+    return st;
+  }
+  ctx->live_graphs++;
+  *out = g;
+  return ISVD_OK;
+}
+
+isvd_status isvd_graph_destroy(isvd_graph g) {
+  if (!g) return ISVD_ERR_INVALID_ARG;
+  if (g->refs.load() > 0) return ISVD_ERR_BUSY;
+  DeviceGuard dg(g->ctx->device);
+  cudaStreamSynchronize(g->ctx->stream);
+  for (void* p : g->allocs) cudaFree(p);
+  g->ctx->live_graphs--;
+  delete g;
+  return ISVD_OK;
+}
+
+isvd_status isvd_graph_info(isvd_graph g, int64_t* n_global, int64_t* n_local, int64_t* nnz_local,
+                            int64_t* max_degree) {
+  if (!g) return ISVD_ERR_INVALID_ARG;
+  if (n_global) *n_global = g->n;
+  if (n_local) *n_local = g->n_local;
+  if (nnz_local) *nnz_local = g->nnz;
+  if (max_degree) *max_degree = g->max_deg;
+  return ISVD_OK;
+}
+
+// ================================================================= operators
+isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out) {
+  if (!g || !desc || !out) return ISVD_ERR_INVALID_ARG;
+  isvd_ctx ctx = g->ctx;
+  *out = nullptr;
+  isvd_op op = new (std::nothrow) isvd_op_s();
+  if (!op) return ISVD_ERR_OOM;
+  isvd_status st = guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    op->g = g;
+    op->kind = desc->kind;
+    op->terms = desc->num_terms;
+    if (desc->kind == ISVD_OP_POWER_SUM) {
+      REQ(desc->num_terms >= 1, ISVD_ERR_INVALID_ARG, "NE needs C >= 1 powers");
+      REQ(desc->weights != nullptr, ISVD_ERR_INVALID_ARG, "NE weights are null");
+      REQ(desc->lambda_adj == 0.0, ISVD_ERR_UNSUPPORTED, "lambda_adj != 0 (the +lambda A term) is not built yet");
+      op->w.assign(desc->weights, desc->weights + desc->num_terms);
+      for (double x : op->w) REQ(std::isfinite(x), ISVD_ERR_NONFINITE, "non-finite weight");
+      REQ(std::isfinite(desc->lambda_ones), ISVD_ERR_NONFINITE, "non-finite lambda");
+      op->lambda_ones = desc->lambda_ones;
+    } else if (desc->kind == ISVD_OP_STACKED_PROPAGATION) {
+      REQ(desc->num_terms >= 0, ISVD_ERR_INVALID_ARG, "NC needs L >= 0");
+      REQ(desc->d >= 1, ISVD_ERR_INVALID_ARG, "NC feature width d must be >= 1");
+      REQ(desc->ldx >= desc->d && desc->ldx % 4 == 0, ISVD_ERR_INVALID_ARG, "ldx must be >= d and a multiple of 4");
+      REQ(desc->X != nullptr || g->n_local == 0, ISVD_ERR_INVALID_ARG, "X is null");
+      REQ((desc->x_flags & ~(uint32_t)(ISVD_PTR_DEVICE | ISVD_BORROW)) == 0, ISVD_ERR_INVALID_ARG, "bad x_flags");
+      op->d = desc->d;
+      op->ldx = desc->ldx;
+      const bool dev = desc->x_flags & ISVD_PTR_DEVICE;
+      if (dev && (desc->x_flags & ISVD_BORROW)) {
+        REQ(aligned16(desc->X), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
+        op->X = desc->X;
+      } else {
+        // copy with padding columns zeroed (ldx kept)
+        std::vector<void*> tmp;
+        float* x = (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * desc->ldx, tmp);
+        if (g->n_local > 0)
+          CK(cudaMemcpy(x, desc->X, sizeof(float) * (size_t)g->n_local * desc->ldx,
+                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        op->X = x;
+        op->own_x = true;
+      }
+    } else {
+      REQ(false, ISVD_ERR_INVALID_ARG, "unknown op kind");
+    }
+  });
+  if (st != ISVD_OK) {
+    delete op;
+    return st;
+  }
+  g->refs++;
+  *out = op;
+  return ISVD_OK;
+}
+
+isvd_status isvd_op_shape(isvd_op op, int64_t* rows, int64_t* cols) {
+  if (!op || !rows || !cols) return ISVD_ERR_INVALID_ARG;
+  op_shape(op, rows, cols);
+  return ISVD_OK;
+}
+
+static void free_solver_ws(SolverWs& s) {
+  if (s.graph_exec) cudaGraphExecDestroy(s.graph_exec);
+  s.graph_exec = nullptr;
+  for (void* p : s.allocs) cudaFree(p);
+  s.allocs.clear();
+  s.key_l = s.key_k = -1;
+}
+
+isvd_status isvd_op_destroy(isvd_op op) {
+  if (!op) return ISVD_ERR_INVALID_ARG;
+  DeviceGuard dg(op->g->ctx->device);
+  cudaStreamSynchronize(op->g->ctx->stream);
+  for (void* p : op->ws_allocs) cudaFree(p);
+  free_solver_ws(op->sws);
+  if (op->own_x) cudaFree((void*)op->X);
+  op->g->refs--;
+  delete op;
+  return ISVD_OK;
+}
+
+static isvd_status check_dense(isvd_ctx ctx, const float* p, int64_t w, int64_t ld) {
+  if (!p) { set_err(ctx, "null matrix pointer"); return ISVD_ERR_INVALID_ARG; }
+  if (w < 1) { set_err(ctx, "width must be >= 1"); return ISVD_ERR_SHAPE; }
+  if (ld < w || ld % 4 != 0 || !aligned16(p)) {
+    set_err(ctx, "leading dimension must be >= width and a multiple of 4, pointer 16-byte aligned");
+    return ISVD_ERR_INVALID_ARG;
+  }
+  if (ld < ((w + 3) / 4) * 4) { set_err(ctx, "leading dimension must be >= round_up(width, 4)"); return ISVD_ERR_INVALID_ARG; }
+  return ISVD_OK;
+}
+
+isvd_status isvd_matmul(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo) {
+  if (!op) return ISVD_ERR_INVALID_ARG;
+  isvd_ctx ctx = op->g->ctx;
+  isvd_status s;
+  if ((s = check_dense(ctx, Q, w, ldq)) != ISVD_OK) return s;
+  if ((s = check_dense(ctx, out, w, ldo)) != ISVD_OK) return s;
+  if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    op_matmul(op, Q, ldq, out, ldo, round_up(w, 4));
+  });
+}
+
+isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo) {
+  if (!op) return ISVD_ERR_INVALID_ARG;
+  isvd_ctx ctx = op->g->ctx;
+  isvd_status s;
+  if ((s = check_dense(ctx, Q, w, ldq)) != ISVD_OK) return s;
+  if ((s = check_dense(ctx, out, w, ldo)) != ISVD_OK) return s;
+  if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    op_matmul_T(op, Q, ldq, out, ldo, round_up(w, 4));
+  });
+}
+
+// ==================================================================== solver
+namespace {
+
+int64_t working_l(const isvd_op_s* op, const isvd_svd_params* p) {
+  int64_t r, c;
+  op_shape(op, &r, &c);
+  int64_t l = p->oversampling < 0 ? 2LL * p->k : (int64_t)p->k + p->oversampling;
+  return std::min(l, std::min(r, c));
+}
+
+void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
+  SolverWs& s = op->sws;
+  if (s.key_l == l && s.key_k == k) return;
+  isvd_ctx ctx = op->g->ctx;
+  CK(cudaStreamSynchronize(ctx->stream));
+  free_solver_ws(s);
+  const int64_t ld = round_up(l, 4), ldk = round_up(k, 4);
+  const int64_t rr = std::max<int64_t>(op->g->n_local, 1), cr = std::max<int64_t>(c_rows_local(op), 1);
+  auto f = [&](int64_t n) { return (float*)dmalloc(ctx, sizeof(float) * n, s.allocs); };
+  auto d = [&](int64_t n) { return (double*)dmalloc(ctx, sizeof(double) * n, s.allocs); };
+  s.Qc = f(cr * ld);
+  s.Qc2 = f(cr * ld);
+  s.Yr = f(rr * ld);
+  s.Yr2 = f(rr * ld);
+  s.Rinv32 = f(ld * ld);
+  s.Ub = f(l * ldk);
+  s.Vb = f(l * ldk);
+  s.Utmp = f(rr * ldk);
+  s.Vtmp = f(cr * ldk);
+  s.sgn = f(ldk);
+  s.gram = d(l * l);
+  s.Ra = d(l * l); s.Rb = d(l * l); s.Rc = d(l * l); s.Rab = d(l * l); s.Rfin = d(l * l);
+  s.chol_ws = d(l * l);
+  s.jac_ws = d(jacobi_ws_doubles((int)l));
+  s.sigma = d(k);
+  s.cand = d(3 * k);
+  s.cand_all = d(3 * k * op->g->ctx->world);
+  s.absmax_ws = d(absmax_ws_doubles(rr, (int)k));
+  s.key_l = l;
+  s.key_k = k;
+}
+
+// One Cholesky pass (Alg. 2 right): G = Y^T Y (all-reduced when row-partitioned), R = chol(G), Yout = Y R^-1.
+void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64,
+              bool force_fail, const int* gate) {
+  isvd_ctx ctx = op->g->ctx;
+  SolverWs& s = op->sws;
+  const int64_t ld = round_up(l, 4);
+  CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
+                ctx->stream));
+  if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
+  CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
+  CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));
+}
+
+// CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
+// If Rout != null it receives R = R_3 R_2 R_1 (so that Y_in = Y_out R).
+void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64_t l, bool force_fail, double* Rout) {
+  isvd_ctx ctx = op->g->ctx;
+  SolverWs& s = op->sws;
+  const int64_t ld = round_up(l, 4);
+  int* gate = &ctx->status->need_extra_pass;
+  CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, force_fail, nullptr);
+  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, false, nullptr);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, false, gate);
+  CK(launch_scale_rows(Y2, ld, Y, ld, rows, ld, nullptr, 1.f, gate, ctx->stream));  // copy back iff pass 3 ran
+  if (Rout) {
+    CK(launch_trmm(s.Rb, s.Ra, s.Rab, (int)l, nullptr, ctx->stream));
+    CK(launch_trmm(s.Rc, s.Rab, Rout, (int)l, gate, ctx->stream));
+  }
+}
+
+}  // namespace
+
+}  // extern "C"
+
+extern "C" {
+
+isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* omega, int64_t ldo) {
+  if (!op || !params || !omega) return ISVD_ERR_INVALID_ARG;
+  isvd_ctx ctx = op->g->ctx;
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    int64_t r, c;
+    op_shape(op, &r, &c);
+    REQ(params->k >= 1 && params->k <= std::min(r, c), ISVD_ERR_RANK, "k must be in [1, min(r, c)]");
+    int64_t l = working_l(op, params);
+    REQ(ldo >= round_up(l, 4) && ldo % 4 == 0 && aligned16(omega), ISVD_ERR_INVALID_ARG, "bad omega ld");
+    int64_t row0 = op->kind == ISVD_OP_POWER_SUM ? op->g->row_begin : 0;
+    CK(launch_omega(params->seed, row0, c_rows_local(op), (int)l, ldo, omega, ctx->stream));
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ the solver body
+namespace {
+
+void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int64_t ldu, float* V, int64_t ldv) {
+  isvd_graph g = op->g;
+  isvd_ctx ctx = g->ctx;
+  SolverWs& s = op->sws;
+  const int64_t k = p->k;
+  const int64_t ld = round_up(l, 4), ldk = round_up(k, 4);
+  const bool ne = op->kind == ISVD_OP_POWER_SUM;
+  const int64_t cr = c_rows_local(op), rr = g->n_local;
+  const bool force = p->flags & ISVD_SVD_FORCE_CHOL_FAIL;
+  CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
+  // Alg. 1 line 4: Q ~ N(0,1)^{c x l}
+  if (p->flags & ISVD_SVD_OMEGA_PROVIDED) {
+    CK(cudaMemcpy2DAsync(s.Qc, ld * sizeof(float), p->omega, ld * sizeof(float), ld * sizeof(float), cr,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+  } else {
+    CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, ctx->stream));
+  }
+  // Alg. 1 lines 5-8
+  for (int it = 0; it < p->power_iters; ++it) {
+    op_matmul(op, s.Qc, ld, s.Yr, ld, ld);                       // M Q       (r x l)
+    cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);          // orthonorm
+    op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld);                     // M^T Q     (c x l)
+    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr);            // orthonorm
+  }
+  // Alg. 1 line 9: Q <- orthonorm(M Q)
+  op_matmul(op, s.Qc, ld, s.Yr, ld, ld);
+  cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);
+  // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
+  op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld);
+  cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin);
+  // Alg. 1 line 11: svd(B) with B = R^T Q_W^T -> one-sided Jacobi on R^T
+  CK(launch_jacobi_svd(s.Rfin, (int)l, (int)k, ldk, s.sigma, s.Ub, s.Vb, s.jac_ws, ctx->status, ctx->num_sms,
+                       ctx->stream));
+  // Alg. 1 line 12: U = Q U_B;  V = Q_W V_B;  truncate to k
+  CK(launch_gemm_tn(s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream));
+  CK(launch_gemm_tn(s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream));
+  // sign rule (reading O9)
+  CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
+  const double* cand = s.cand;
+  if (ctx->world > 1) {
+    NK(ncclAllGather(s.cand, s.cand_all, 3 * k, ncclDouble, ctx->comm, ctx->stream));
+    cand = s.cand_all;
+  }
+  CK(launch_sign_flip(cand, ctx->world, (int)k, s.sgn, U, ldu, rr, V, ldv, cr, ctx->stream));
+  CK(launch_check_finite(U, ldu, rr, k, ctx->status, ctx->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu, double* S, float* V, int64_t ldv,
+                     isvd_svd_report* rep) {
+  if (!op || !p || !U || !S || !V) return ISVD_ERR_INVALID_ARG;
+  isvd_ctx ctx = op->g->ctx;
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    int64_t r, c;
+    op_shape(op, &r, &c);
+    REQ(p->k >= 1 && p->k <= std::min(r, c), ISVD_ERR_RANK, "k must be in [1, min(r, c)]");
+    REQ(p->power_iters >= 0, ISVD_ERR_INVALID_ARG, "power_iters must be >= 0");
+    REQ((p->flags & ~(uint32_t)(ISVD_SVD_OMEGA_PROVIDED | ISVD_SVD_HOST_OUTPUT | ISVD_SVD_NO_GRAPH |
+                                ISVD_SVD_FORCE_CHOL_FAIL | ISVD_SVD_PROFILE)) == 0,
+        ISVD_ERR_INVALID_ARG, "unknown svd flag");
+    REQ(!(p->flags & ISVD_SVD_OMEGA_PROVIDED) || p->omega, ISVD_ERR_INVALID_ARG, "omega is null");
+    const int64_t l = working_l(op, p);
+    REQ(l <= 1024, ISVD_ERR_UNSUPPORTED, "working width l > 1024 is not supported by the small-matrix kernels");
+    const int64_t k = p->k, ldk = round_up(k, 4);
+    const bool host_out = p->flags & ISVD_SVD_HOST_OUTPUT;
+    REQ(ldu >= ldk && ldv >= ldk, ISVD_ERR_INVALID_ARG, "ldu and ldv must be >= round_up(k, 4)");
+    if (!host_out) REQ(aligned16(U) && aligned16(V) && ldu % 4 == 0 && ldv % 4 == 0, ISVD_ERR_INVALID_ARG,
+                       "U and V must be 16-byte aligned with ld a multiple of 4");
+    ensure_op_ws(op, round_up(l, 4));
+    ensure_solver_ws(op, l, k);
+    SolverWs& s = op->sws;
+    float* Ud = host_out ? s.Utmp : U;
+    float* Vd = host_out ? s.Vtmp : V;
+    const int64_t lduu = host_out ? ldk : ldu, ldvv = host_out ? ldk : ldv;
+    int64_t launches0 = g_launches;
+    ctx->profiling = p->flags & ISVD_SVD_PROFILE;
+    ctx->spmm_steps = 0;
+    ctx->spmm_alg_bytes = 0.0;
+    CK(cudaEventRecord(ctx->ev0, ctx->stream));
+    try {
+      solver_body(op, p, l, Ud, lduu, Vd, ldvv);
+    } catch (...) {
+      ctx->profiling = false;
+      throw;
+    }
+    CK(cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->profiling = false;
+    DevStatus st;
+    std::vector<double> sig(k);
+    CK(cudaMemcpyAsync(sig.data(), s.sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&st, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+    const int64_t rr = op->g->n_local, cr = c_rows_local(op);
+    if (host_out) {
+      if (rr > 0)
+        CK(cudaMemcpy2DAsync(U, ldu * sizeof(float), Ud, lduu * sizeof(float), k * sizeof(float), rr,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpy2DAsync(V, ldv * sizeof(float), Vd, ldvv * sizeof(float), k * sizeof(float), cr,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    if (rep) {
+      rep->l = (int32_t)l;
+      rep->ld = (int32_t)round_up(l, 4);
+      rep->chol_fallbacks = st.chol_breakdown;
+      rep->jacobi_sweeps = st.jacobi_sweeps;
+      rep->world = ctx->world;
+      rep->kernel_launches = (int32_t)(g_launches - launches0);
+      rep->ms_total = ms;
+      rep->spmm_steps = ctx->spmm_steps;
+      rep->spmm_alg_bytes = ctx->spmm_alg_bytes;
+      rep->ms_spmm = 0.0;
+      if (p->flags & ISVD_SVD_PROFILE) {
+        for (int i = 0; i < ctx->spmm_steps; ++i) {
+          float t = 0.f;
+          CK(cudaEventElapsedTime(&t, ctx->prof_events[2 * i], ctx->prof_events[2 * i + 1]));
+          rep->ms_spmm += t;
+        }
+      }
+    }
+    REQ(!st.chol_failed, ISVD_ERR_NOT_PD, "Cholesky of Q^T Q failed even after the shifted retries");
+    REQ(!st.nonfinite, ISVD_ERR_NONFINITE, "non-finite value in the solver output");
+    for (int64_t i = 0; i < k; ++i) S[i] = sig[i];
+  });
+}
+
+}  // extern "C"

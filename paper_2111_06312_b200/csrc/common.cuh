@@ -1,0 +1,148 @@
+// Shared device/host helpers of the isvd CUDA library (sm_100a only).
+// Not shared with oracle/ (the oracle is independent test infrastructure).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ISVD_DEVICE __device__ __forceinline__
+
+namespace isvd {
+
+constexpr int kNumSMs = 148;  // B200; the runtime value is queried, this is only a default
+
+// Device-side status word shared by every kernel of one solver call.
+// Kernels set bits; the host reads the word once at the end of isvd_svd.
+struct DevStatus {
+  int chol_breakdown;   // Cholesky pivot <= tol met (count of factorizations that needed the shift)
+  int chol_failed;      // still broken after the shifted retry
+  int nonfinite;        // NaN/Inf produced
+  int jacobi_sweeps;    // sweeps used by the last Jacobi SVD
+  int need_extra_pass;  // set by a Cholesky that used the shift: run the third CQR pass
+  int pad[3];
+};
+
+#if defined(__CUDACC__)
+ISVD_DEVICE float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+ISVD_DEVICE void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+ISVD_DEVICE float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+#endif
+
+// Kernels enqueued by this host thread (each launcher adds the number it launched);
+// isvd_svd reports the difference over one call.
+extern thread_local int64_t g_launches;
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// ---------------------------------------------------------------- launchers
+// All launchers enqueue on `st` and return cudaGetLastError().
+
+// Omega (Alg. 1 line 4): rows [row0, row0+rows) of the c x l matrix, ld >= l;
+// padding columns [l, ld) are written as 0.
+cudaError_t launch_omega(uint64_t seed, int64_t row0, int64_t rows, int l, int64_t ld, float* out,
+                         cudaStream_t st);
+
+// Column sums (fp64) of a rows x w fp32 matrix: out[j] = sum_i Q[i, j], j < wpad (wpad = round_up(w,4)).
+// Deterministic two-stage reduction; `ws` needs colsum_ws_doubles(rows, wpad) doubles.
+int64_t colsum_ws_doubles(int64_t rows, int64_t wpad);
+cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ldq, double* ws, double* out,
+                          cudaStream_t st);
+
+// out[i, :] = coef * (vec ? vec[i] : 1) * in[i, :]  for i < rows, columns < wpad.
+cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows,
+                              int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st);
+
+// ------------------------------------------------------------------- SpMM
+// Fused CSR SpMM step (K1):  for each local row i (global id row_offset + i)
+//   acc_i = self_coef * Y[row_offset + i] + sum_{j in N(i)} Y[j]          (fp32 blocks of 8, fp64 across)
+//   out_i = post_coef * post_vec[i] * acc_i
+//         + term_coef * term_vec[i] * T[i]
+//         - rank1_coef * colsum                                          (all in fp64, one rounding)
+// Rows are processed as segments of <= kSegEdges edges; long rows are split and
+// their fp32 partial sums combined in a fixed order by a fixup pass.
+struct SpmmPlan {
+  int64_t n_local = 0;
+  int64_t n_seg = 0;          // number of segments
+  int64_t n_split_rows = 0;   // rows split into >1 segment
+  int64_t n_slots = 0;        // partial slots (= segments of split rows)
+  // device arrays
+  int32_t* seg_row = nullptr;     // [n_seg] local row of the segment
+  int64_t* seg_beg = nullptr;     // [n_seg] first edge
+  int32_t* seg_len = nullptr;     // [n_seg] number of edges
+  int32_t* seg_slot = nullptr;    // [n_seg] partial slot or -1 (whole row)
+  int32_t* split_row = nullptr;   // [n_split_rows] local row id
+  int32_t* split_slot0 = nullptr; // [n_split_rows] first slot
+  int32_t* split_nslot = nullptr; // [n_split_rows] number of slots
+};
+constexpr int kSegEdges = 512;
+
+struct SpmmArgs {
+  const int32_t* col_idx;
+  int64_t row_offset;
+  const float* Y; int64_t ldy;
+  float self_coef;
+  const float* post_vec; float post_coef;
+  const float* T; int64_t ldt; const float* term_vec; float term_coef;
+  const double* colsum; double rank1_coef;
+  float* out; int64_t ldo;
+  int64_t wpad;           // columns processed (multiple of 4)
+};
+int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
+cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,
+                        cudaStream_t st);
+
+// ------------------------------------------------------------------- dense
+// C[i, j] = row_scale(i) * sum_k A[i, k] B[k, j]  (+ C[i, j] if accumulate), i < M, j < N (N multiple of 4).
+// B is K x N row-major (ldb).  upper_tri_b: B[k, j] = 0 for k > j (skips those k).
+cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                           int64_t M, int64_t N, int64_t K, const float* row_scale, float alpha,
+                           bool upper_tri_b, const int* gate, cudaStream_t st);
+
+// G = A^T diag(row_scale) B over `rows` rows, A: rows x Ka, B: rows x Kb -> fp64 Ka x ldg.
+// symmetric: A == B, only the upper triangle of tiles is computed and mirrored.
+// If out32 != null the result is also written as fp32 (ld32).
+int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms);
+cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka,
+                       int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,
+                       float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st);
+// out32[i, j] = (float) G[i, j]
+cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
+                              int64_t cols, cudaStream_t st);
+
+// -------------------------------------------------------------- small fp64
+// `gate` (nullable, device int): when non-null and *gate == 0 the kernel does nothing
+// (used for the conditional third CholeskyQR pass without a host sync).
+//
+// Cholesky G = R^T R (upper R) of the l x l fp64 SPD matrix G (ldg; upper triangle
+// read) and the inverse of R.  Outputs: Rinv32 (ld x ld fp32, upper, zero elsewhere
+// incl. padding), R64 (l x l fp64, upper, zeros below) if non-null.
+// Breakdown (pivot <= 1e-14 * max diag, or non-finite) -> shift the diagonal by
+// 1e-10 * trace (x100 per retry, 3 retries); status->chol_breakdown++ and
+// status->need_extra_pass = 1.  force_fail treats the first attempt as broken.
+// `ws` needs l*l doubles when l > kCholSmemMax (global-memory path).
+constexpr int kCholSmemMax = 160;
+cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64,
+                            double* ws, DevStatus* status, bool force_fail, const int* gate, cudaStream_t st);
+// out = Rnew * Racc (upper l x l fp64, ld = l); when gated off: out = Racc.
+cudaError_t launch_trmm(const double* Rnew, const double* Racc, double* out, int l, const int* gate,
+                        cudaStream_t st);
+// One-sided Jacobi SVD of A = R^T (R upper l x l fp64, ld = l).  Writes sigma_k
+// (k values, descending), Ub (l x ldk fp32: the first k left singular vectors of
+// R^T) and Vb (l x ldk fp32: the matching right singular vectors).
+int64_t jacobi_ws_doubles(int l);
+cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double* sigma_k, float* Ub, float* Vb,
+                              double* ws, DevStatus* status, int num_sms, cudaStream_t st);
+// Sign rule: per column c < k of U (rows x ldu), the entry of largest |.| (lowest row on
+// ties) -> cand[c] = {|u|, row + row_offset, sign} (3 doubles; row -1 if rows == 0).
+int64_t absmax_ws_doubles(int64_t rows, int k);
+cudaError_t launch_col_absmax(const float* U, int64_t ldu, int64_t rows, int k, int64_t row_offset,
+                              double* ws, double* cand, cudaStream_t st);
+// Select over `world` candidate sets (cand: world x k x 3) and flip the columns of
+// U (rows x k) and V (vrows x k) whose selected entry is negative.
+cudaError_t launch_sign_flip(const double* cand, int world, int k, float* sgn_ws, float* U, int64_t ldu,
+                             int64_t rows, float* V, int64_t ldv, int64_t vrows, cudaStream_t st);
+// status->nonfinite |= any(!isfinite(A[:rows, :cols])).
+cudaError_t launch_check_finite(const float* A, int64_t lda, int64_t rows, int64_t cols, DevStatus* status,
+                                cudaStream_t st);
+
+}  // namespace isvd

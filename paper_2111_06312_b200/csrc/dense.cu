@@ -1,0 +1,416 @@
+// Tall-skinny dense kernels of the solver (FP32 SIMT; fp64 where a reduction
+// over the n-long dimension is taken).
+//
+//  K2  gemm_tn   C = alpha * diag(row_scale) * A * B   (A: M x K tall, B: K x N small)
+//                X.G_j of the NC operator (DenseMatrixPF.dot), the
+//                CholeskyQR apply Q (L^-1)^T = Q R^-1 (Alg. 2 right, upper
+//                triangular B skips the zero half) and U = Q U_B (Alg. 1).
+//  K5/K16 atb    G = A^T diag(s) B in fp64 (Gram Q^T Q of Alg. 2; X^T Z_j of
+//                the NC transpose).  Split-K over rows, fp32 tiles promoted to fp64
+//                once when staged in shared memory, fp64 FMA, deterministic
+//                fixed-order reduction of the per-CTA partials (no atomics).
+//  K15 colsum    1^T Q in fp64 for the rank-1 term of Eq. 3.
+#include "common.cuh"
+
+namespace isvd {
+namespace {
+
+// ------------------------------------------------------------------ GEMM
+template <int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                   float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                   const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int TX = BN / TN;  // threads along N
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  int64_t kend = K;
+  if (upper_tri_b) kend = (n0 + BN < K) ? (n0 + BN) : K;
+
+  // loader mapping: A tile BM x BK as float4 along K; B tile BK x BN as float4 along N
+  constexpr int A_F4 = BM * BK / 4;
+  constexpr int B_F4 = BK * BN / 4;
+  float4 ra[(A_F4 + NT - 1) / NT];
+  float4 rb[(B_F4 + NT - 1) / NT];
+
+  auto load_tiles = [&](int64_t k0) {
+#pragma unroll
+    for (int t = 0; t < (A_F4 + NT - 1) / NT; ++t) {
+      int f = tid + t * NT;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < A_F4) {
+        int r = f / (BK / 4), kk = (f % (BK / 4)) * 4;
+        int64_t gm = m0 + r, gk = k0 + kk;
+        if (gm < M) {
+          const float* p = A + gm * lda + gk;
+          if (gk + 3 < kend) {
+            v = *reinterpret_cast<const float4*>(p);
+          } else {
+            if (gk < kend) v.x = p[0];
+            if (gk + 1 < kend) v.y = p[1];
+            if (gk + 2 < kend) v.z = p[2];
+          }
+        }
+      }
+      ra[t] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < (B_F4 + NT - 1) / NT; ++t) {
+      int f = tid + t * NT;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < B_F4) {
+        int kk = f / (BN / 4), c = (f % (BN / 4)) * 4;
+        int64_t gk = k0 + kk, gn = n0 + c;
+        if (gk < kend && gn < N) v = *reinterpret_cast<const float4*>(B + gk * ldb + gn);
+      }
+      rb[t] = v;
+    }
+  };
+  auto store_tiles = [&](int buf) {
+#pragma unroll
+    for (int t = 0; t < (A_F4 + NT - 1) / NT; ++t) {
+      int f = tid + t * NT;
+      if (f < A_F4) {
+        int r = f / (BK / 4), kk = (f % (BK / 4)) * 4;
+        As[buf][kk][r] = ra[t].x;
+        As[buf][kk + 1][r] = ra[t].y;
+        As[buf][kk + 2][r] = ra[t].z;
+        As[buf][kk + 3][r] = ra[t].w;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < (B_F4 + NT - 1) / NT; ++t) {
+      int f = tid + t * NT;
+      if (f < B_F4) {
+        int kk = f / (BN / 4), c = (f % (BN / 4)) * 4;
+        *reinterpret_cast<float4*>(&Bs[buf][kk][c]) = rb[t];
+      }
+    }
+  };
+
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+  int64_t ntiles = (kend + BK - 1) / BK;
+  if (ntiles > 0) {
+    load_tiles(0);
+    store_tiles(0);
+    __syncthreads();
+  }
+  for (int64_t t = 0; t < ntiles; ++t) {
+    int buf = (int)(t & 1);
+    if (t + 1 < ntiles) load_tiles((t + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; i += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
+        a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < TN; j += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * TN + j]);
+        b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (t + 1 < ntiles) {
+      store_tiles(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    int64_t gm = m0 + ty * TM + i;
+    if (gm >= M) continue;
+    float s = alpha;
+    if (row_scale) s *= row_scale[gm];
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      int64_t gn = n0 + tx * TN + j;
+      if (gn < N)
+        *reinterpret_cast<float4*>(C + gm * ldc + gn) =
+            make_float4(s * acc[i][j], s * acc[i][j + 1], s * acc[i][j + 2], s * acc[i][j + 3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ A^T B (fp64)
+constexpr int ATB_T = 64;   // output tile edge
+constexpr int ATB_R = 16;   // rows per smem stage
+
+__global__ void __launch_bounds__(256)
+    atb_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
+               int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric, int tiles_a,
+               int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  __shared__ double As[ATB_R][ATB_T];
+  __shared__ double Bs[ATB_R][ATB_T];
+  // output tile (ti, tj); symmetric: upper-triangular tiles only, enumerated row by row
+  int ti = 0, tj = 0;
+  {
+    int t = blockIdx.x;
+    if (symmetric) {
+      while (t >= tiles_a - ti) { t -= tiles_a - ti; ++ti; }
+      tj = ti + t;
+    } else {
+      ti = t / tiles_b;
+      tj = t - ti * tiles_b;
+    }
+  }
+  const int64_t a0 = (int64_t)ti * ATB_T, b0 = (int64_t)tj * ATB_T;
+  const int64_t chunk = blockIdx.y;
+  const int64_t r_begin = chunk * rows_per_chunk;
+  int64_t r_end = r_begin + rows_per_chunk;
+  if (r_end > rows) r_end = rows;
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += ATB_R) {
+    // stage: 16 rows x 64 cols of A and B: 256 float4 each = 1 per thread
+    {
+      int rr = tid / 16, cc = (tid % 16) * 4;
+      int64_t gr = r0 + rr;
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+      if (gr < r_end) {
+        if (a0 + cc < Ka) va = *reinterpret_cast<const float4*>(A + gr * lda + a0 + cc);
+        if (b0 + cc < Kb) vb = *reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc);
+        if (row_scale) {
+          float s = row_scale[gr];
+          vb.x *= s; vb.y *= s; vb.z *= s; vb.w *= s;
+        }
+      }
+      As[rr][cc] = va.x; As[rr][cc + 1] = va.y; As[rr][cc + 2] = va.z; As[rr][cc + 3] = va.w;
+      Bs[rr][cc] = vb.x; Bs[rr][cc + 1] = vb.y; Bs[rr][cc + 2] = vb.z; Bs[rr][cc + 3] = vb.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ATB_R; ++r) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[r][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[r][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  // partial tile -> ws[chunk][a][b]  (ws_ld = padded Kb)
+  double* W = ws + chunk * (int64_t)((Ka + ATB_T - 1) / ATB_T * ATB_T) * ws_ld;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) W[(a0 + ty + 16 * i) * ws_ld + b0 + tx + 16 * j] = acc[i][j];
+}
+
+__global__ void atb_reduce_kernel(const double* __restrict__ ws, int64_t ws_ld, int64_t ka_pad, int nchunks,
+                                  int64_t Ka, int64_t Kb, int symmetric, double* __restrict__ G, int64_t ldg,
+                                  float* __restrict__ out32, int64_t ld32, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  int64_t tot = Ka * Kb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / Kb, j = t - (t / Kb) * Kb;
+    int64_t si = i, sj = j;
+    if (symmetric && i > j) { si = j; sj = i; }
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += ws[((int64_t)c * ka_pad + si) * ws_ld + sj];
+    if (G) G[i * ldg + j] = s;
+    if (out32) out32[i * ld32 + j] = (float)s;
+  }
+}
+
+// ------------------------------------------------------------------ colsum
+__global__ void colsum_partial_kernel(const float* __restrict__ Q, int64_t rows, int64_t wpad, int64_t ldq,
+                                      int64_t rows_per_block, double* __restrict__ ws) {
+  // blockDim (32, 8): x over columns, y over rows
+  const int64_t r0 = blockIdx.x * rows_per_block;
+  int64_t r1 = r0 + rows_per_block;
+  if (r1 > rows) r1 = rows;
+  __shared__ double red[8][33];
+  for (int64_t c0 = 0; c0 < wpad; c0 += 32) {
+    int64_t c = c0 + threadIdx.x;
+    double s = 0.0;
+    if (c < wpad)
+      for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) s += (double)Q[r * ldq + c];
+    red[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < wpad) {
+      double t = 0.0;
+      for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+      ws[blockIdx.x * wpad + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void colsum_final_kernel(const double* __restrict__ ws, int nblocks, int64_t wpad, double* __restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < wpad; c += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += ws[b * wpad + c];
+    out[c] = s;
+  }
+}
+
+constexpr int64_t kColsumRows = 2048;
+
+// ------------------------------------------------------------------ misc
+__global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, float* __restrict__ out, int64_t ldo,
+                                  int64_t rows, int64_t w4, const float* __restrict__ vec, float coef,
+                                  const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  int64_t tot = rows * w4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / w4, c = (t - i * w4) * 4;
+    float s = coef * (vec ? vec[i] : 1.f);
+    float4 v = *reinterpret_cast<const float4*>(in + i * ldi + c);
+    *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ G, int64_t ldg, float* __restrict__ out, int64_t ldo,
+                                  int64_t rows, int64_t cols) {
+  int64_t tot = rows * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / cols, j = t - i * cols;
+    out[i * ldo + j] = (float)G[i * ldg + j];
+  }
+}
+
+__global__ void check_finite_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                                    DevStatus* status) {
+  int64_t tot = rows * cols;
+  int bad = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / cols, j = t - i * cols;
+    if (!isfinite(A[i * lda + j])) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status->nonfinite, 1);
+}
+
+int grid_for(int64_t work, int threads, int cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M,
+                           int64_t N, int64_t K, const float* row_scale, float alpha, bool upper_tri_b,
+                           const int* gate, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (N > 64) {
+    dim3 grid((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, 128));
+    ++g_launches; gemm_tn_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                           upper_tri_b ? 1 : 0, gate);
+  } else {
+    dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(M, 128));
+    ++g_launches; gemm_tn_kernel<128, 64, 8, 8, 4><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                          upper_tri_b ? 1 : 0, gate);
+  }
+  return cudaGetLastError();
+}
+
+static int64_t atb_chunks(int64_t rows, int64_t ntiles, int num_sms) {
+  int64_t target = 2LL * num_sms;
+  int64_t ch = ceil_div(target, ntiles);
+  int64_t max_ch = ceil_div(rows, 256);  // at least 256 rows per chunk
+  if (ch > max_ch) ch = max_ch;
+  if (ch < 1) ch = 1;
+  return ch;
+}
+
+static int64_t atb_ntiles(int64_t Ka, int64_t Kb, bool symmetric) {
+  int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
+  return symmetric ? ta * (ta + 1) / 2 : ta * tb;
+}
+
+int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
+  // the non-symmetric tile count is the smaller one, so its chunk count bounds both cases
+  int64_t ch = atb_chunks(rows, atb_ntiles(Ka, Kb, Ka == Kb), num_sms);
+  int64_t ch2 = atb_chunks(rows, atb_ntiles(Ka, Kb, false), num_sms);
+  if (ch2 > ch) ch = ch2;
+  return ch * round_up(Ka, ATB_T) * round_up(Kb, ATB_T);
+}
+
+cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
+                       const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg, float* out32,
+                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st) {
+  if (Ka <= 0 || Kb <= 0) return cudaSuccess;
+  int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
+  int64_t ntiles = atb_ntiles(Ka, Kb, symmetric);
+  int64_t ch = atb_chunks(rows, ntiles, num_sms);
+  int64_t rpc = rows > 0 ? round_up(ceil_div(rows, ch), ATB_R) : ATB_R;
+  ch = rows > 0 ? ceil_div(rows, rpc) : 1;
+  int64_t ka_pad = round_up(Ka, ATB_T), ws_ld = round_up(Kb, ATB_T);
+  if (rows > 0) {
+    dim3 grid((unsigned)ntiles, (unsigned)ch);
+    ++g_launches; atb_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0, (int)ta,
+                                     (int)tb, rpc, ws, ws_ld, gate);
+  } else {
+    cudaMemsetAsync(ws, 0, sizeof(double) * ka_pad * ws_ld, st);
+    ch = 1;
+  }
+  ++g_launches; atb_reduce_kernel<<<grid_for(Ka * Kb, 256, num_sms * 8), 256, 0, st>>>(ws, ws_ld, ka_pad, (int)ch, Ka, Kb,
+                                                                         symmetric ? 1 : 0, G, ldg, out32, ld32, gate);
+  return cudaGetLastError();
+}
+
+int64_t colsum_ws_doubles(int64_t rows, int64_t wpad) { return (ceil_div(rows, kColsumRows) + 1) * wpad; }
+
+cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ldq, double* ws, double* out,
+                          cudaStream_t st) {
+  int64_t nb = ceil_div(rows, kColsumRows);
+  if (nb < 1) {
+    cudaMemsetAsync(out, 0, sizeof(double) * wpad, st);
+    return cudaGetLastError();
+  }
+  ++g_launches; colsum_partial_kernel<<<(unsigned)nb, dim3(32, 8), 0, st>>>(Q, rows, wpad, ldq, kColsumRows, ws);
+  ++g_launches; colsum_final_kernel<<<grid_for(wpad, 128, 64), 128, 0, st>>>(ws, (int)nb, wpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
+                              const float* vec, float coef, const int* gate, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  ++g_launches; scale_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4, vec,
+                                                                               coef, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows, int64_t cols,
+                              cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  ++g_launches; f64_to_f32_kernel<<<grid_for(rows * cols, 256, 148 * 8), 256, 0, st>>>(G, ldg, out, ldo, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* A, int64_t lda, int64_t rows, int64_t cols, DevStatus* status,
+                                cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  ++g_launches; check_finite_kernel<<<grid_for(rows * cols, 256, 148 * 8), 256, 0, st>>>(A, lda, rows, cols, status);
+  return cudaGetLastError();
+}
+
+}  // namespace isvd

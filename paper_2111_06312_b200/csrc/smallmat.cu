@@ -1,0 +1,458 @@
+// Small l x l fp64 kernels of the solver (l = 42 ... 400).
+//
+//  K6/K7 chol_inv   R = chol(G) (upper, G = R^T R) and R^-1 in place:
+//                   Alg. 2 right, P:886-887 ("L <- Choleskydecomposition(Q^T Q);
+//                   Q (L^-1)^T", with L = R^T).  One CTA; the matrix lives in shared
+//                   memory for l <= kCholSmemMax and in an L2-resident global buffer
+//                   above that.  Breakdown (reading O10) shifts the diagonal and
+//                   raises a device flag that gates the third CholeskyQR pass.
+//  trmm             R_acc <- R_new R_acc for the final CQR2 of W = M^T Q.
+//  K9  jacobi       one-sided (Hestenes) Jacobi SVD of R^T (B = (M^T Q)^T = R^T Q_W^T,
+//                   replacing tf.linalg.svd(B)), round-robin parallel ordering,
+//                   one warp per column pair, cooperative grid barrier per round.
+//  K17 sort/sign    descending order (reading O9) and the sign rule.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace isvd {
+namespace {
+
+ISVD_DEVICE double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------ Cholesky + inverse
+// Returns 1 (block-uniform) on breakdown.
+__device__ int chol_upper_inplace(double* A, int l, double tol, double* s_scal, int* s_flag) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int k = 0; k < l; ++k) {
+    if (tid == 0) {
+      double piv = A[(int64_t)k * l + k];
+      int bad = !(piv > tol) || !isfinite(piv);
+      *s_flag = bad;
+      double r = bad ? 1.0 : sqrt(piv);
+      A[(int64_t)k * l + k] = r;
+      s_scal[0] = 1.0 / r;
+    }
+    __syncthreads();
+    if (*s_flag) return 1;
+    const double inv = s_scal[0];
+    for (int j = k + 1 + tid; j < l; j += nt) A[(int64_t)k * l + j] *= inv;
+    __syncthreads();
+    const double* rk = A + (int64_t)k * l;
+    for (int i = k + 1 + warp; i < l; i += nw) {
+      const double rki = rk[i];
+      double* ai = A + (int64_t)i * l;
+      for (int j = i + lane; j < l; j += 32) ai[j] -= rki * rk[j];
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// In-place inverse of the upper triangular A (LAPACK trti2 order, column by column).
+__device__ void trinv_upper_inplace(double* A, int l, double* tmp) {
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  for (int j = 0; j < l; ++j) {
+    // tmp[i] = sum_{k=i}^{j-1} Xinv[i][k] * U[k][j]   (top-left block already inverted)
+    for (int i = warp; i < j; i += nw) {
+      const double* xi = A + (int64_t)i * l;
+      double s = 0.0;
+      for (int k = i + lane; k < j; k += 32) s += xi[k] * A[(int64_t)k * l + j];
+      s = warp_sum(s);
+      if (lane == 0) tmp[i] = s;
+    }
+    const double ajj = 1.0 / A[(int64_t)j * l + j];
+    __syncthreads();
+    for (int i = tid; i < j; i += blockDim.x) A[(int64_t)i * l + j] = -ajj * tmp[i];
+    if (tid == 0) A[(int64_t)j * l + j] = ajj;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ G, int64_t ldg, int l, int64_t ld,
+                                                        float* __restrict__ Rinv32, double* __restrict__ R64,
+                                                        double* __restrict__ ws, DevStatus* status, int force_fail,
+                                                        const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  extern __shared__ double smem[];
+  __shared__ double s_scal[4];
+  __shared__ int s_flag;
+  __shared__ double s_tmp[512];
+  double* A = (l <= kCholSmemMax) ? smem : ws;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // trace and max diagonal (thread 0, l <= 512)
+  if (tid == 0) {
+    double tr = 0.0, mx = 0.0;
+    for (int i = 0; i < l; ++i) {
+      double d = G[(int64_t)i * ldg + i];
+      tr += d;
+      mx = d > mx ? d : mx;
+    }
+    s_scal[1] = tr;
+    s_scal[2] = mx;
+  }
+  __syncthreads();
+  const double trace = s_scal[1];
+  const double tol = 1e-14 * s_scal[2];
+  double shift = 0.0;
+  int attempt = 0;
+  int failed = 1;
+  for (attempt = 0; attempt < 4; ++attempt) {
+    for (int64_t t = tid; t < (int64_t)l * l; t += nt) {
+      int i = (int)(t / l), j = (int)(t - (int64_t)i * l);
+      double v = (j >= i) ? G[(int64_t)i * ldg + j] : 0.0;
+      if (i == j) v += shift;
+      A[t] = v;
+    }
+    __syncthreads();
+    int bad = chol_upper_inplace(A, l, tol, s_scal, &s_flag);
+    if (force_fail && attempt == 0) bad = 1;
+    if (!bad) { failed = 0; break; }
+    // shifted CholeskyQR (reading O10): s = 11 (m l + l (l+1)) u ||G||, bounded here by
+    // a trace-relative shift that grows by 100x per retry.
+    shift = (attempt == 0) ? 1e-10 * trace : shift * 100.0;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (attempt > 0) {
+      atomicAdd(&status->chol_breakdown, 1);
+      status->need_extra_pass = 1;
+    }
+    if (failed) status->chol_failed = 1;
+  }
+  if (R64) {
+    for (int64_t t = tid; t < (int64_t)l * l; t += nt) {
+      int i = (int)(t / l), j = (int)(t - (int64_t)i * l);
+      R64[t] = (j >= i) ? A[t] : 0.0;
+    }
+  }
+  __syncthreads();
+  trinv_upper_inplace(A, l, s_tmp);
+  for (int64_t t = tid; t < ld * ld; t += nt) {
+    int64_t i = t / ld, j = t - i * ld;
+    float v = 0.f;
+    if (i < l && j < l && j >= i) v = (float)A[i * l + j];
+    Rinv32[t] = v;
+  }
+}
+
+// out = Rnew * Racc (upper x upper), or out = Racc when gated off.
+__global__ void trmm_kernel(const double* __restrict__ Rnew, const double* __restrict__ Racc, double* __restrict__ out,
+                            int l, const int* gate) {
+  const bool mult = !(gate && *((volatile const int*)gate) == 0);
+  const int i = blockIdx.x;
+  for (int j = threadIdx.x; j < l; j += blockDim.x) {
+    double s = 0.0;
+    if (mult) {
+      if (j >= i)
+        for (int k = i; k <= j; ++k) s += Rnew[(int64_t)i * l + k] * Racc[(int64_t)k * l + j];
+    } else {
+      s = Racc[(int64_t)i * l + j];
+    }
+    out[(int64_t)i * l + j] = s;
+  }
+}
+
+// ------------------------------------------------------------ Jacobi SVD
+ISVD_DEVICE int rr_index(int pos, int round, int m) {
+  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (m - 1);
+}
+
+template <bool kOneBlock>
+ISVD_DEVICE void jsync() {
+  if (kOneBlock) __syncthreads();
+  else cg::this_grid().sync();
+}
+
+// A: l x l, column j of R^T (= row j of R) contiguous at A + j*l; J: accumulated rotations.
+template <bool kOneBlock>
+__global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ R, int l, double* Ag, double* Jg,
+                                                      int* counters, DevStatus* status, int max_sweeps,
+                                                      double* __restrict__ Aout, double* __restrict__ Jout) {
+  extern __shared__ double smem[];
+  const bool in_smem = kOneBlock && (2 * l * l * (int)sizeof(double) <= 200 * 1024);
+  double* A = in_smem ? smem : Ag;
+  double* J = in_smem ? smem + (int64_t)l * l : Jg;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
+  for (int64_t t = gtid; t < (int64_t)l * l; t += gthreads) {
+    A[t] = R[t];
+    int64_t j = t / l, i = t - j * l;
+    J[t] = (i == j) ? 1.0 : 0.0;
+  }
+  if (gtid == 0) { counters[0] = 0; counters[1] = 0; }
+  jsync<kOneBlock>();
+  const int m = (l & 1) ? l + 1 : l;
+  const double tol = (double)l * 1.1102230246251565e-16;
+  int sweep = 0;
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    int* cnt = counters + (sweep & 1);
+    for (int round = 0; round < m - 1; ++round) {
+      for (int64_t p = gwarp; p < m / 2; p += nwarps) {
+        int i = rr_index((int)p, round, m), j = rr_index(m - 1 - (int)p, round, m);
+        if (i >= l || j >= l) continue;
+        if (i > j) { int t = i; i = j; j = t; }
+        double* ai = A + (int64_t)i * l;
+        double* aj = A + (int64_t)j * l;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < l; r += 32) {
+          double x = ai[r], y = aj[r];
+          al += x * x; be += y * y; ga += x * y;
+        }
+        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          double zeta = (be - al) / (2.0 * ga);
+          double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int r = lane; r < l; r += 32) {
+            double x = ai[r], y = aj[r];
+            ai[r] = c * x - s * y;
+            aj[r] = s * x + c * y;
+          }
+          double* ji = J + (int64_t)i * l;
+          double* jj = J + (int64_t)j * l;
+          for (int r = lane; r < l; r += 32) {
+            double x = ji[r], y = jj[r];
+            ji[r] = c * x - s * y;
+            jj[r] = s * x + c * y;
+          }
+          if (lane == 0) atomicAdd(cnt, 1);
+        }
+        __syncwarp();
+      }
+      jsync<kOneBlock>();
+    }
+    int rotations = *((volatile int*)cnt);
+    jsync<kOneBlock>();
+    if (gtid == 0) counters[(sweep + 1) & 1] = 0;
+    jsync<kOneBlock>();
+    if (rotations == 0) { ++sweep; break; }
+  }
+  if (gtid == 0) status->jacobi_sweeps = sweep;
+  if (in_smem) {
+    for (int64_t t = threadIdx.x; t < (int64_t)l * l; t += blockDim.x) {
+      Aout[t] = A[t];
+      Jout[t] = J[t];
+    }
+  }
+}
+
+// sigma_j = ||A_j||; descending order; Ub = A_perm / sigma, Vb = J_perm (first k columns).
+__global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __restrict__ A, const double* __restrict__ J,
+                                                             int l, int k, int64_t ldk, double* sig_ws,
+                                                             double* __restrict__ sigma_k, float* __restrict__ Ub,
+                                                             float* __restrict__ Vb, DevStatus* status) {
+  __shared__ int perm[512];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < l; j += nw) {
+    const double* aj = A + (int64_t)j * l;
+    double s = 0.0;
+    for (int r = lane; r < l; r += 32) s += aj[r] * aj[r];
+    s = warp_sum(s);
+    if (lane == 0) sig_ws[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += blockDim.x) {
+    double sj = sig_ws[j];
+    int rank = 0;
+    for (int i = 0; i < l; ++i) {
+      double si = sig_ws[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    if (rank < k) perm[rank] = j;
+    if (!isfinite(sj) && tid >= 0) atomicOr(&status->nonfinite, 1);
+  }
+  __syncthreads();
+  for (int t = tid; t < k; t += blockDim.x) sigma_k[t] = sig_ws[perm[t]];
+  for (int64_t e = tid; e < (int64_t)l * ldk; e += blockDim.x) {
+    int64_t r = e / ldk;
+    int t = (int)(e - r * ldk);
+    float u = 0.f, v = 0.f;
+    if (t < k) {
+      int j = perm[t];
+      double s = sig_ws[j];
+      u = s > 0.0 ? (float)(A[(int64_t)j * l + r] / s) : 0.f;
+      v = (float)J[(int64_t)j * l + r];
+    }
+    Ub[e] = u;
+    Vb[e] = v;
+  }
+}
+
+// ------------------------------------------------------------ sign rule
+constexpr int64_t kAbsmaxRows = 4096;
+
+__global__ void col_absmax_partial_kernel(const float* __restrict__ U, int64_t ldu, int64_t rows, int k,
+                                          double* __restrict__ part) {
+  // blockDim (32, 8)
+  const int64_t r0 = blockIdx.x * kAbsmaxRows;
+  int64_t r1 = r0 + kAbsmaxRows;
+  if (r1 > rows) r1 = rows;
+  __shared__ float bv[8][32];
+  __shared__ int64_t br[8][32];
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    int c = c0 + threadIdx.x;
+    float best = -1.f;
+    int64_t brow = -1;
+    if (c < k)
+      for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+        float v = fabsf(U[r * ldu + c]);
+        if (v > best) { best = v; brow = r; }  // rows visited in increasing order: ties keep the lowest
+      }
+    bv[threadIdx.y][threadIdx.x] = best;
+    br[threadIdx.y][threadIdx.x] = brow;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < k) {
+      float b = -1.f;
+      int64_t rb = -1;
+      for (int y = 0; y < 8; ++y) {
+        float v = bv[y][threadIdx.x];
+        int64_t r = br[y][threadIdx.x];
+        if (r >= 0 && (v > b || (v == b && r < rb))) { b = v; rb = r; }
+      }
+      double* o = part + ((int64_t)blockIdx.x * k + c) * 3;
+      o[0] = b;
+      o[1] = (double)rb;
+      o[2] = rb >= 0 ? (U[rb * ldu + c] < 0.f ? -1.0 : 1.0) : 1.0;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void col_absmax_final_kernel(const double* __restrict__ part, int nblocks, int k, int64_t row_offset,
+                                        double* __restrict__ cand) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    double b = -1.0, rb = -1.0, sg = 1.0;
+    for (int blk = 0; blk < nblocks; ++blk) {
+      const double* o = part + ((int64_t)blk * k + c) * 3;
+      if (o[1] >= 0.0 && (o[0] > b || (o[0] == b && o[1] < rb))) { b = o[0]; rb = o[1]; sg = o[2]; }
+    }
+    cand[c * 3 + 0] = b;
+    cand[c * 3 + 1] = rb >= 0.0 ? rb + (double)row_offset : -1.0;
+    cand[c * 3 + 2] = sg;
+  }
+}
+
+__global__ void sign_select_kernel(const double* __restrict__ cand, int world, int k, float* __restrict__ sgn) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    double b = -1.0, rb = -1.0, sg = 1.0;
+    for (int w = 0; w < world; ++w) {
+      const double* o = cand + ((int64_t)w * k + c) * 3;
+      if (o[1] >= 0.0 && (o[0] > b || (o[0] == b && o[1] < rb))) { b = o[0]; rb = o[1]; sg = o[2]; }
+    }
+    sgn[c] = (float)sg;
+  }
+}
+
+__global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int64_t ldu, int64_t rows) {
+  int64_t tot = rows * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / k;
+    int c = (int)(t - i * k);
+    U[i * ldu + c] *= sgn[c];
+  }
+}
+
+int grid_for(int64_t work, int threads, int cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64, double* ws,
+                            DevStatus* status, bool force_fail, const int* gate, cudaStream_t st) {
+  size_t smem = (l <= kCholSmemMax) ? sizeof(double) * (size_t)l * l : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * kCholSmemMax * kCholSmemMax));
+    attr_set = true;
+  }
+  ++g_launches; chol_inv_kernel<<<1, 1024, smem, st>>>(G, ldg, l, ld, Rinv32, R64, ws, status, force_fail ? 1 : 0, gate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trmm(const double* Rnew, const double* Racc, double* out, int l, const int* gate, cudaStream_t st) {
+  ++g_launches; trmm_kernel<<<l, 128, 0, st>>>(Rnew, Racc, out, l, gate);
+  return cudaGetLastError();
+}
+
+int64_t jacobi_ws_doubles(int l) { return 4LL * l * l + 2LL * l + 64; }
+
+cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double* sigma_k, float* Ub, float* Vb,
+                              double* ws, DevStatus* status, int num_sms, cudaStream_t st) {
+  double* A = ws;
+  double* J = ws + (int64_t)l * l;
+  double* Aout = ws + 2LL * l * l;  // smem path copies results here
+  double* Jout = ws + 3LL * l * l;
+  double* sig = ws + 4LL * l * l;
+  int* counters = reinterpret_cast<int*>(ws + 4LL * l * l + 2LL * l);
+  const int max_sweeps = 60;
+  const bool one_block = l <= 128;
+  if (one_block) {
+    size_t smem = (2 * (size_t)l * l * sizeof(double) <= 200 * 1024) ? 2 * (size_t)l * l * sizeof(double) : 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_set = true;
+    }
+    ++g_launches; jacobi_kernel<true><<<1, 1024, smem, st>>>(R, l, A, J, counters, status, max_sweeps, Aout, Jout);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (smem == 0) { Aout = A; Jout = J; }
+  } else {
+    int m = (l & 1) ? l + 1 : l;
+    int warps_needed = m / 2;
+    int threads = 256;
+    int blocks = (warps_needed * 32 + threads - 1) / threads;
+    if (blocks > num_sms) blocks = num_sms;
+    void* args[] = {(void*)&R, (void*)&l, (void*)&A, (void*)&J, (void*)&counters, (void*)&status,
+                    (void*)&max_sweeps, (void*)&Aout, (void*)&Jout};
+    ++g_launches;
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel<false>, dim3(blocks), dim3(threads), args,
+                                                0, st);
+    if (e != cudaSuccess) return e;
+    Aout = A;
+    Jout = J;
+  }
+  ++g_launches; jacobi_finish_kernel<<<1, 1024, 0, st>>>(Aout, Jout, l, k, ldk, sig, sigma_k, Ub, Vb, status);
+  return cudaGetLastError();
+}
+
+int64_t absmax_ws_doubles(int64_t rows, int k) { return (ceil_div(rows, kAbsmaxRows) + 1) * k * 3; }
+
+cudaError_t launch_col_absmax(const float* U, int64_t ldu, int64_t rows, int k, int64_t row_offset, double* ws,
+                              double* cand, cudaStream_t st) {
+  int64_t nb = ceil_div(rows, kAbsmaxRows);
+  if (nb < 1) {
+    // no local rows: candidates with row -1
+    ++g_launches; col_absmax_final_kernel<<<1, 256, 0, st>>>(ws, 0, k, row_offset, cand);
+    return cudaGetLastError();
+  }
+  ++g_launches; col_absmax_partial_kernel<<<(unsigned)nb, dim3(32, 8), 0, st>>>(U, ldu, rows, k, ws);
+  ++g_launches; col_absmax_final_kernel<<<grid_for(k, 256, 16), 256, 0, st>>>(ws, (int)nb, k, row_offset, cand);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sign_flip(const double* cand, int world, int k, float* sgn_ws, float* U, int64_t ldu, int64_t rows,
+                             float* V, int64_t ldv, int64_t vrows, cudaStream_t st) {
+  ++g_launches; sign_select_kernel<<<grid_for(k, 256, 16), 256, 0, st>>>(cand, world, k, sgn_ws);
+  if (rows > 0) { ++g_launches; flip_kernel<<<grid_for(rows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, U, ldu, rows); }
+  if (vrows > 0) { ++g_launches; flip_kernel<<<grid_for(vrows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, V, ldv, vrows); }
+  return cudaGetLastError();
+}
+
+}  // namespace isvd

@@ -1,0 +1,154 @@
+// Fused CSR SpMM step (K1): one application of T = D^-1 A (NE, Eq. 3)
+// or of A_hat = S (A + I) S (NC, Eq. 6 / P:68) to an n x w block, with the
+// Horner-chain term, the row scales and the rank-1 correction of Eq. 3
+// (-lambda 1 1^T, applied matrix-free as <M2, <M1, G>>) fused into
+// the epilogue.  Replaces the paper's tf.sparse.sparse_dense_matmul
+// (SparseMatrixPF.dot), SumPF.dot and the lazy cache of
+// ProductPF.
+//
+// Work decomposition (B200): a "team" of w/4 threads owns one CSR segment at a
+// time; thread t of the team owns columns [4t, 4t+4) and gathers them with one
+// 16-byte read-only load per neighbour, so every neighbour row is read as one
+// contiguous, coalesced span.  Eight neighbours are in flight per thread
+// (memory-level parallelism for the dependent index -> row gather) and summed in
+// fp32; each block of eight is then added into an fp64 accumulator (reading O15:
+// fp64 row accumulation).  Rows longer than kSegEdges edges are split into
+// segments whose fp32 partials are combined by `spmm_fixup_kernel` in a fixed
+// order, so results are deterministic and hubs (max degree ~1.4e5 in config 4)
+// do not serialise one team.
+#include "common.cuh"
+
+namespace isvd {
+namespace {
+
+struct Acc4 { double x, y, z, w; };
+
+ISVD_DEVICE void acc_add(Acc4& a, float4 v) { a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w; }
+
+ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int c4, Acc4 acc) {
+  const int64_t col = 4 * (int64_t)c4;
+  if (a.self_coef != 0.f) {
+    float4 y = ldg4(a.Y + (row + a.row_offset) * a.ldy + col);
+    double sc = a.self_coef;
+    acc.x += sc * y.x; acc.y += sc * y.y; acc.z += sc * y.z; acc.w += sc * y.w;
+  }
+  double p = a.post_coef;
+  if (a.post_vec) p *= (double)a.post_vec[row];
+  acc.x *= p; acc.y *= p; acc.z *= p; acc.w *= p;
+  if (a.T) {
+    double t = a.term_coef;
+    if (a.term_vec) t *= (double)a.term_vec[row];
+    float4 tv = *reinterpret_cast<const float4*>(a.T + row * a.ldt + col);  // may alias out
+    acc.x += t * tv.x; acc.y += t * tv.y; acc.z += t * tv.z; acc.w += t * tv.w;
+  }
+  if (a.colsum) {
+    double r = a.rank1_coef;
+    acc.x -= r * a.colsum[col]; acc.y -= r * a.colsum[col + 1];
+    acc.z -= r * a.colsum[col + 2]; acc.w -= r * a.colsum[col + 3];
+  }
+  st4(a.out + row * a.ldo + col, make_float4((float)acc.x, (float)acc.y, (float)acc.z, (float)acc.w));
+}
+
+__global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
+                                                    const int64_t* __restrict__ seg_beg,
+                                                    const int32_t* __restrict__ seg_len,
+                                                    const int32_t* __restrict__ seg_slot, int64_t n_seg,
+                                                    int teams, float* __restrict__ partial) {
+  const int TS = (int)(a.wpad >> 2);
+  const int team = threadIdx.x / TS;
+  const int c4 = threadIdx.x - team * TS;
+  if (team >= teams) return;
+  const float* __restrict__ Yc = a.Y + 4 * (int64_t)c4;
+  const int64_t ldy = a.ldy;
+  for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
+    const int64_t row = seg_row[s];
+    const int32_t* __restrict__ idx = a.col_idx + seg_beg[s];
+    const int len = seg_len[s];
+    Acc4 acc{0.0, 0.0, 0.0, 0.0};
+    int e = 0;
+    for (; e + 8 <= len; e += 8) {
+      int j[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) j[u] = __ldg(idx + e + u);
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ldg4(Yc + (int64_t)j[u] * ldy);
+      float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
+      acc_add(acc, f4add(f4add(s01, s23), f4add(s45, s67)));
+    }
+    if (e < len) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (; e < len; ++e) t = f4add(t, ldg4(Yc + (int64_t)__ldg(idx + e) * ldy));
+      acc_add(acc, t);
+    }
+    const int slot = seg_slot[s];
+    if (slot < 0) {
+      spmm_epilogue(a, row, c4, acc);
+    } else {
+      st4(partial + (int64_t)slot * a.wpad + 4 * (int64_t)c4,
+          make_float4((float)acc.x, (float)acc.y, (float)acc.z, (float)acc.w));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) spmm_fixup_kernel(SpmmArgs a, const int32_t* __restrict__ split_row,
+                                                          const int32_t* __restrict__ split_slot0,
+                                                          const int32_t* __restrict__ split_nslot, int64_t n_split,
+                                                          int teams, const float* __restrict__ partial) {
+  const int TS = (int)(a.wpad >> 2);
+  const int team = threadIdx.x / TS;
+  const int c4 = threadIdx.x - team * TS;
+  if (team >= teams) return;
+  for (int64_t r = (int64_t)blockIdx.x * teams + team; r < n_split; r += (int64_t)gridDim.x * teams) {
+    const int64_t row = split_row[r];
+    const int64_t s0 = split_slot0[r];
+    const int ns = split_nslot[r];
+    Acc4 acc{0.0, 0.0, 0.0, 0.0};
+    for (int t = 0; t < ns; ++t) acc_add(acc, ldg4(partial + (s0 + t) * a.wpad + 4 * (int64_t)c4));
+    spmm_epilogue(a, row, c4, acc);
+  }
+}
+
+void team_shape(int64_t wpad, int* teams, int* threads) {
+  int TS = (int)(wpad / 4);
+  int R = TS >= 512 ? 1 : 512 / TS;
+  if (R < 1) R = 1;
+  *teams = R;
+  *threads = TS * R;
+}
+
+}  // namespace
+
+int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad) { return plan.n_slots * wpad; }
+
+cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_partial, int num_sms, cudaStream_t st) {
+  if (plan.n_local == 0) return cudaSuccess;
+  // Column chunks of at most 4096 columns (team of <= 1024 threads).
+  for (int64_t c0 = 0; c0 < a0.wpad; c0 += 4096) {
+    SpmmArgs a = a0;
+    a.wpad = (a0.wpad - c0) < 4096 ? (a0.wpad - c0) : 4096;
+    a.Y += c0;
+    if (a.T) a.T += c0;
+    if (a.colsum) a.colsum += c0;
+    a.out += c0;
+    int teams, threads;
+    team_shape(a.wpad, &teams, &threads);
+    int64_t blocks = ceil_div(plan.n_seg, teams);
+    int per_sm = 2048 / threads;
+    if (per_sm < 1) per_sm = 1;
+    int64_t cap = (int64_t)num_sms * per_sm * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ++g_launches; spmm_kernel<<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,
+                                                 plan.n_seg, teams, ws_partial);
+    if (plan.n_split_rows > 0) {
+      int64_t fb = ceil_div(plan.n_split_rows, teams);
+      if (fb > cap) fb = cap;
+      ++g_launches; spmm_fixup_kernel<<<(int)fb, threads, 0, st>>>(a, plan.split_row, plan.split_slot0, plan.split_nslot,
+                                                     plan.n_split_rows, teams, ws_partial);
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace isvd

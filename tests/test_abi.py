@@ -1,0 +1,80 @@
+"""The C-ABI library builds, loads and exports every symbol include/isvd.h declares
+(no GPU: no compute calls).  Host-only entry points are exercised."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "isvd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(isvd_[a-z_T0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2111_06312_b200 import _build, _lib
+
+    _build.build()
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2111_06312_b200._lib import SIGNATURES
+
+    names = _declared()
+    assert len(names) >= 17
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in SIGNATURES, f"{n} has no ctypes signature in the binding"
+    assert set(SIGNATURES) == set(names)
+
+
+def test_abi_version_and_status_strings(lib):
+    assert lib.isvd_abi_version() == 1
+    assert lib.isvd_status_string(0) == b"ok"
+    assert lib.isvd_status_string(3) == b"rank out of range"
+    assert lib.isvd_last_error(None) == b""
+
+
+def test_partition_host_logic(lib):
+    """Row partition of the distributed layout: ceil(n / P) rows per rank,
+    contiguous, covering [0, n) exactly once, last block ragged."""
+    from paper_2111_06312_b200 import partition
+
+    for n in (1, 7, 2708, 2449029):
+        for P in (1, 2, 3, 4, 8):
+            covered = 0
+            for r in range(P):
+                rb, nl = partition(n, P, r)
+                assert rb == min(n, r * -(-n // P))
+                assert nl >= 0 and rb + nl <= n
+                assert rb == covered or nl == 0
+                covered += nl
+            assert covered == n
+    rb, nl = C.c_int64(), C.c_int64()
+    assert lib.isvd_partition(10, 2, 2, C.byref(rb), C.byref(nl)) == 1  # rank out of range
+
+
+def test_ctx_create_fails_cleanly_without_gpu(lib):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    st = lib.isvd_ctx_create(0, None, None, 0, 1, C.byref(h))
+    assert st != 0 and not h.value
+
+
+def test_product_path_has_no_oracle_import():
+    """The product package never imports the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2111_06312_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
