@@ -293,7 +293,8 @@ def main():
         graph2.close()
         if i > 0:  # first is a warm-up (allocator, pinned pages)
             e2e_times.append(t1 - t0)
-    te = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device="cuda")
+    te = torch.tensor([statistics.median(e2e_times) if e2e_times else float("nan")], dtype=torch.float64,
+                      device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
 

@@ -233,13 +233,14 @@ class _Operator:
         if profile:
             flags |= _lib.ISVD_SVD_PROFILE
         p = self._params(k, oversampling, power_iters, seed, flags, omega)
-        S = np.zeros(k, dtype=np.float64)
+        S = np.zeros(max(int(k), 1), dtype=np.float64)
         rep = _lib.SvdReport()
         check(self.ctx.lib.isvd_svd(self.h, C.byref(p), C.c_void_p(pu), ldu,
                                     S.ctypes.data_as(C.POINTER(C.c_double)), C.c_void_p(pv), ldv, C.byref(rep)),
               "isvd_svd", self.ctx.h)
         U = U[: self.graph.n_local, :k]
         V = V[: self.c_rows(), :k]
+        S = S[:k]
         return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
                          rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes)
 

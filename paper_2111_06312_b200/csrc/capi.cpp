@@ -937,8 +937,12 @@ extern "C" {
 
 isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu, double* S, float* V, int64_t ldv,
                      isvd_svd_report* rep) {
-  if (!op || !p || !U || !S || !V) return ISVD_ERR_INVALID_ARG;
+  if (!op) return ISVD_ERR_INVALID_ARG;
   isvd_ctx ctx = op->g->ctx;
+  if (!p || !U || !S || !V) {
+    set_err(ctx, "null argument");
+    return ISVD_ERR_INVALID_ARG;
+  }
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
     int64_t r, c;
