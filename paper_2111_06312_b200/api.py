@@ -211,7 +211,7 @@ class _Operator:
             out=None) -> SvdResult:
         """Rank-k implicit SVD (Alg. 1) -> U (n_local x k), S (k), V."""
         dev = self.ctx.device
-        kk = round_up(k)
+        kk = max(round_up(k), 4)
         flags = 0
         if host_output:
             flags |= _lib.ISVD_SVD_HOST_OUTPUT
