@@ -318,6 +318,14 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 // M G = sum_j A_hat^j X G_j  (Eq. 6), Horner from the deepest block, iterates stored
 // pre-scaled (Yt = s Y) so the gather needs no per-neighbour scale:
 //   Yt_L = s (X G_L);  Yt_j = s (X G_j) + s^2 ((A+I) Yt_{j+1});  out = X G_0 + s ((A+I) Yt_1).
+// Slab-major full buffers (L2-resident gather slabs) when the iterate is much larger than
+// L2; single-rank only (the all-gather of a row partition needs row-major blocks).
+bool use_slabs(isvd_ctx ctx, const isvd_op_s* op, int64_t wpad) {
+  const int64_t n_full = op->g->n_pad * ctx->world;
+  return op->kind == ISVD_OP_STACKED_PROPAGATION && ctx->world == 1 && wpad % kSlab == 0 &&
+         n_full * wpad * (int64_t)sizeof(float) > (64LL << 20);
+}
+
 void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad) {
   isvd_graph g = op->g;
   const int L = op->terms;
@@ -327,20 +335,22 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
                       ctx->stream));
     return;
   }
+  const int64_t sr = use_slabs(ctx, op, wpad) ? g->n_pad * ctx->world : 0;  // slab rows of the full buffers
+  auto local = [&](float* full) { return sr ? full : slice(g, full, wpad); };
   float* bufs[2] = {op->full_a, op->full_b};
   float* cur = bufs[L & 1];
-  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, slice(g, cur, wpad), wpad, g->n_local, wpad, d,
-                    g->s, 1.f, false, nullptr, ctx->stream));
+  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, local(cur), wpad, g->n_local, wpad, d, g->s, 1.f,
+                    false, nullptr, ctx->stream, sr));
   allgather_rows(ctx, g, cur, wpad);
   for (int j = L - 1; j >= 1; --j) {
     CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)j * d * ldgm, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr,
                       1.f, false, nullptr, ctx->stream));
     float* dst = bufs[j & 1];
     SpmmArgs a = spmm_base(g, wpad);
-    a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
+    a.Y = cur; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
     a.post_vec = g->s2;
     a.T = op->ptmp; a.ldt = wpad; a.term_vec = g->s;
-    a.out = slice(g, dst, wpad); a.ldo = wpad;
+    a.out = local(dst); a.ldo = wpad; a.osr = sr;
     spmm(ctx, op, a);
     allgather_rows(ctx, g, dst, wpad);
     cur = dst;
@@ -348,7 +358,7 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
   CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
                     ctx->stream));
   SpmmArgs a = spmm_base(g, wpad);
-  a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
+  a.Y = cur; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
   a.post_vec = g->s;
   a.T = out; a.ldt = ldo;  // in-place accumulate: each element is read then written by one thread
   a.out = out; a.ldo = ldo;
@@ -363,20 +373,22 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   CK(launch_atb(op->X, op->ldx, Q, ldq, g->n_local, d, wpad, nullptr, false, op->atb_ws, op->blk64, wpad, nullptr, 0,
                 ctx->num_sms, nullptr, ctx->stream));
   if (L > 0) {
+    const int64_t sr = use_slabs(ctx, op, wpad) ? g->n_pad * ctx->world : 0;
+    auto local = [&](float* full) { return sr ? full : slice(g, full, wpad); };
     float* bufs[2] = {op->full_a, op->full_b};
-    CK(launch_scale_rows(Q, ldq, slice(g, bufs[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream));
+    CK(launch_scale_rows(Q, ldq, local(bufs[0]), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream, 0, sr));
     allgather_rows(ctx, g, bufs[0], wpad);
     for (int j = 1; j <= L; ++j) {
       float* src = bufs[(j - 1) & 1];
       float* dst = bufs[j & 1];
       SpmmArgs a = spmm_base(g, wpad);
-      a.Y = src; a.ldy = wpad; a.self_coef = 1.f;
+      a.Y = src; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
       a.post_vec = g->s2;
-      a.out = slice(g, dst, wpad); a.ldo = wpad;
+      a.out = local(dst); a.ldo = wpad; a.osr = sr;
       spmm(ctx, op, a);
       if (j < L) allgather_rows(ctx, g, dst, wpad);
-      CK(launch_atb(op->X, op->ldx, slice(g, dst, wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
-                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream));
+      CK(launch_atb(op->X, op->ldx, local(dst), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
+                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, sr));
     }
   }
   const int64_t c = d * (L + 1);
@@ -632,6 +644,12 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     p.split_row = up32(split_row);
     p.split_slot0 = up32(split_slot0);
     p.split_nslot = up32(split_nslot);
+    {
+      std::vector<int32_t> order(seg_row.size());
+      for (size_t t = 0; t < order.size(); ++t) order[t] = (int32_t)t;
+      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return seg_len[a] > seg_len[b]; });
+      p.seg_order = up32(order);
+    }
     p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<size_t>(seg_beg.size(), 1), g->allocs);
     if (!seg_beg.empty())
       CK(cudaMemcpy(p.seg_beg, seg_beg.data(), sizeof(int64_t) * seg_beg.size(), cudaMemcpyHostToDevice));

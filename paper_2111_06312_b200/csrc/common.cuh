@@ -5,6 +5,11 @@
 #include <stdint.h>
 
 #define ISVD_DEVICE __device__ __forceinline__
+#if defined(__CUDACC__)
+#define ISVD_HOSTDEV __host__ __device__
+#else
+#define ISVD_HOSTDEV
+#endif
 
 namespace isvd {
 
@@ -32,6 +37,15 @@ ISVD_DEVICE float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y
 extern thread_local int64_t g_launches;
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Dense operands are either ROW-MAJOR (element (i, c) at p[i*ld + c]) or SLAB-MAJOR:
+// columns grouped in slabs of kSlab = 8 (32 bytes), each slab a contiguous sr x 8
+// block, element (i, c) at p[((c/8)*sr + i)*8 + c%8].  Slab-major gather sources
+// keep one slab (n x 32 B) resident in L2 while the SpMM streams the CSR over it.
+constexpr int kSlab = 8;
+ISVD_HOSTDEV inline int64_t mat_off(int64_t ld, int64_t sr, int64_t i, int64_t c) {
+  return sr ? ((c >> 3) * sr + i) * 8 + (c & 7) : i * ld + c;
+}
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 // ---------------------------------------------------------------- launchers
@@ -49,8 +63,10 @@ cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ld
                           cudaStream_t st);
 
 // out[i, :] = coef * (vec ? vec[i] : 1) * in[i, :]  for i < rows, columns < wpad.
+// isr / osr: slab rows of in / out (0 = row-major).
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows,
-                              int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st);
+                              int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st,
+                              int64_t isr = 0, int64_t osr = 0);
 
 // ------------------------------------------------------------------- SpMM
 // Fused CSR SpMM step (K1):  for each local row i (global id row_offset + i)
@@ -73,6 +89,7 @@ struct SpmmPlan {
   int32_t* split_row = nullptr;   // [n_split_rows] local row id
   int32_t* split_slot0 = nullptr; // [n_split_rows] first slot
   int32_t* split_nslot = nullptr; // [n_split_rows] number of slots
+  int32_t* seg_order = nullptr;   // [n_seg] segments sorted by length, longest first
 };
 constexpr int kSegEdges = 512;
 
@@ -85,18 +102,22 @@ struct SpmmArgs {
   const float* T; int64_t ldt; const float* term_vec; float term_coef;
   const double* colsum; double rank1_coef;
   float* out; int64_t ldo;
-  int64_t wpad;           // columns processed (multiple of 4)
+  int64_t wpad;           // columns processed (multiple of 4; of 8 with slab-major Y)
+  int64_t ysr = 0, tsr = 0, osr = 0;  // slab rows of Y / T / out (0 = row-major)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
+// With a slab-major Y the step runs one launch per group of slabs whose gather footprint
+// (rows x 32 B per slab) fits `l2_budget` bytes; segments are visited longest-first
+// (seg_order, a permutation of [0, n_seg)) so the 2-thread items of a warp have similar lengths.
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,
-                        cudaStream_t st);
+                        cudaStream_t st, int64_t l2_budget = 48LL << 20);
 
 // ------------------------------------------------------------------- dense
 // C[i, j] = row_scale(i) * sum_k A[i, k] B[k, j]  (+ C[i, j] if accumulate), i < M, j < N (N multiple of 4).
 // B is K x N row-major (ldb).  upper_tri_b: B[k, j] = 0 for k > j (skips those k).
 cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                            int64_t M, int64_t N, int64_t K, const float* row_scale, float alpha,
-                           bool upper_tri_b, const int* gate, cudaStream_t st);
+                           bool upper_tri_b, const int* gate, cudaStream_t st, int64_t csr = 0);
 
 // G = A^T diag(row_scale) B over `rows` rows, A: rows x Ka, B: rows x Kb -> fp64 Ka x ldg.
 // symmetric: A == B, only the upper triangle of tiles is computed and mirrored.
@@ -104,7 +125,8 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
 int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms);
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka,
                        int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,
-                       float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st);
+                       float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
+                       int64_t bsr = 0);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);

@@ -20,7 +20,8 @@ template <int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                    float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
-                   const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate) {
+                   const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate,
+                   int64_t csr) {
   if (gate && *((volatile const int*)gate) == 0) return;
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int TX = BN / TN;  // threads along N
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     for (int j = 0; j < TN; j += 4) {
       int64_t gn = n0 + tx * TN + j;
       if (gn < N)
-        *reinterpret_cast<float4*>(C + gm * ldc + gn) =
+        *reinterpret_cast<float4*>(C + mat_off(ldc, csr, gm, gn)) =
             make_float4(s * acc[i][j], s * acc[i][j + 1], s * acc[i][j + 2], s * acc[i][j + 3]);
     }
   }
@@ -152,13 +153,17 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 constexpr int ATB_T = 64;   // output tile edge
 constexpr int ATB_R = 16;   // rows per smem stage
 
-__global__ void __launch_bounds__(256)
+constexpr int ATB_THREADS = 64;  // 8 x 8 threads, each an 8 x 8 register tile of the 64 x 64 output tile
+
+__global__ void __launch_bounds__(ATB_THREADS)
     atb_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric, int tiles_a,
-               int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld, const int* gate) {
+               int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld, const int* gate,
+               int64_t bsr) {
   if (gate && *((volatile const int*)gate) == 0) return;
-  __shared__ double As[ATB_R][ATB_T];
-  __shared__ double Bs[ATB_R][ATB_T];
+  // operands promoted to fp64 once, when staged; 2 B of shared memory read per DFMA
+  __shared__ __align__(16) double As[2][ATB_R][ATB_T];
+  __shared__ __align__(16) double Bs[2][ATB_R][ATB_T];
   // output tile (ti, tj); symmetric: upper-triangular tiles only, enumerated row by row
   int ti = 0, tj = 0;
   {
@@ -177,50 +182,74 @@ __global__ void __launch_bounds__(256)
   int64_t r_end = r_begin + rows_per_chunk;
   if (r_end > rows) r_end = rows;
   const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
-  double acc[4][4];
+  const int tx = tid & 7, ty = tid >> 3;
+  // staging map: 16 rows x 64 cols = 256 float4 per operand, 4 per thread
+  float4 pa[4], pb[4];
+  auto load = [&](int64_t r0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += ATB_R) {
-    // stage: 16 rows x 64 cols of A and B: 256 float4 each = 1 per thread
-    {
-      int rr = tid / 16, cc = (tid % 16) * 4;
+    for (int u = 0; u < 4; ++u) {
+      int f = tid + u * ATB_THREADS;
+      int rr = f >> 4, cc = (f & 15) * 4;
       int64_t gr = r0 + rr;
       float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
       if (gr < r_end) {
-        if (a0 + cc < Ka) va = *reinterpret_cast<const float4*>(A + gr * lda + a0 + cc);
-        if (b0 + cc < Kb) vb = *reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc);
+        if (a0 + cc < Ka) va = __ldg(reinterpret_cast<const float4*>(A + gr * lda + a0 + cc));
+        if (b0 + cc < Kb) vb = __ldg(reinterpret_cast<const float4*>(B + mat_off(ldb, bsr, gr, b0 + cc)));
         if (row_scale) {
-          float s = row_scale[gr];
+          float s = __ldg(row_scale + gr);
           vb.x *= s; vb.y *= s; vb.z *= s; vb.w *= s;
         }
       }
-      As[rr][cc] = va.x; As[rr][cc + 1] = va.y; As[rr][cc + 2] = va.z; As[rr][cc + 3] = va.w;
-      Bs[rr][cc] = vb.x; Bs[rr][cc + 1] = vb.y; Bs[rr][cc + 2] = vb.z; Bs[rr][cc + 3] = vb.w;
+      pa[u] = va;
+      pb[u] = vb;
     }
-    __syncthreads();
+  };
+  auto store = [&](int buf) {
 #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int f = tid + u * ATB_THREADS;
+      int rr = f >> 4, cc = (f & 15) * 4;
+      double2* da = reinterpret_cast<double2*>(&As[buf][rr][cc]);
+      double2* db = reinterpret_cast<double2*>(&Bs[buf][rr][cc]);
+      da[0] = make_double2(pa[u].x, pa[u].y); da[1] = make_double2(pa[u].z, pa[u].w);
+      db[0] = make_double2(pb[u].x, pb[u].y); db[1] = make_double2(pb[u].z, pb[u].w);
+    }
+  };
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  const int64_t nst = (r_end - r_begin + ATB_R - 1) / ATB_R;
+  if (nst > 0) {
+    load(r_begin);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t st = 0; st < nst; ++st) {
+    const int buf = (int)(st & 1);
+    if (st + 1 < nst) load(r_begin + (st + 1) * ATB_R);
+#pragma unroll 4
     for (int r = 0; r < ATB_R; ++r) {
-      double a[4], b[4];
+      double a[8], b[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[r][ty + 16 * i];
+      for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[r][tx + 16 * j];
+      for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
+    if (st + 1 < nst) store(buf ^ 1);
     __syncthreads();
   }
   // partial tile -> ws[chunk][a][b]  (ws_ld = padded Kb)
   double* W = ws + chunk * (int64_t)((Ka + ATB_T - 1) / ATB_T * ATB_T) * ws_ld;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) W[(a0 + ty + 16 * i) * ws_ld + b0 + tx + 16 * j] = acc[i][j];
+    for (int j = 0; j < 8; ++j) W[(a0 + ty + 8 * i) * ws_ld + b0 + tx + 8 * j] = acc[i][j];
 }
 
 __global__ void atb_reduce_kernel(const double* __restrict__ ws, int64_t ws_ld, int64_t ka_pad, int nchunks,
@@ -276,14 +305,14 @@ constexpr int64_t kColsumRows = 2048;
 // ------------------------------------------------------------------ misc
 __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, float* __restrict__ out, int64_t ldo,
                                   int64_t rows, int64_t w4, const float* __restrict__ vec, float coef,
-                                  const int* gate) {
+                                  const int* gate, int64_t isr, int64_t osr) {
   if (gate && *((volatile const int*)gate) == 0) return;
   int64_t tot = rows * w4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / w4, c = (t - i * w4) * 4;
     float s = coef * (vec ? vec[i] : 1.f);
-    float4 v = *reinterpret_cast<const float4*>(in + i * ldi + c);
-    *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
+    float4 v = *reinterpret_cast<const float4*>(in + mat_off(ldi, isr, i, c));
+    *reinterpret_cast<float4*>(out + mat_off(ldo, osr, i, c)) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
   }
 }
 
@@ -318,22 +347,22 @@ int grid_for(int64_t work, int threads, int cap) {
 
 cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M,
                            int64_t N, int64_t K, const float* row_scale, float alpha, bool upper_tri_b,
-                           const int* gate, cudaStream_t st) {
+                           const int* gate, cudaStream_t st, int64_t csr) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (N > 64) {
     dim3 grid((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                           upper_tri_b ? 1 : 0, gate);
+                                                           upper_tri_b ? 1 : 0, gate, csr);
   } else {
     dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 64, 8, 8, 4><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                          upper_tri_b ? 1 : 0, gate);
+                                                          upper_tri_b ? 1 : 0, gate, csr);
   }
   return cudaGetLastError();
 }
 
 static int64_t atb_chunks(int64_t rows, int64_t ntiles, int num_sms) {
-  int64_t target = 2LL * num_sms;
+  int64_t target = 8LL * num_sms;  // 64-thread CTAs, several resident per SM
   int64_t ch = ceil_div(target, ntiles);
   int64_t max_ch = ceil_div(rows, 256);  // at least 256 rows per chunk
   if (ch > max_ch) ch = max_ch;
@@ -356,7 +385,7 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
 
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
                        const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg, float* out32,
-                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st) {
+                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st, int64_t bsr) {
   if (Ka <= 0 || Kb <= 0) return cudaSuccess;
   int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
   int64_t ntiles = atb_ntiles(Ka, Kb, symmetric);
@@ -366,8 +395,8 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
   int64_t ka_pad = round_up(Ka, ATB_T), ws_ld = round_up(Kb, ATB_T);
   if (rows > 0) {
     dim3 grid((unsigned)ntiles, (unsigned)ch);
-    ++g_launches; atb_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0, (int)ta,
-                                     (int)tb, rpc, ws, ws_ld, gate);
+    ++g_launches; atb_kernel<<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0, (int)ta,
+                                     (int)tb, rpc, ws, ws_ld, gate, bsr);
   } else {
     cudaMemsetAsync(ws, 0, sizeof(double) * ka_pad * ws_ld, st);
     ch = 1;
@@ -392,10 +421,11 @@ cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ld
 }
 
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
-                              const float* vec, float coef, const int* gate, cudaStream_t st) {
+                              const float* vec, float coef, const int* gate, cudaStream_t st,
+                              int64_t isr, int64_t osr) {
   if (rows <= 0) return cudaSuccess;
   ++g_launches; scale_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4, vec,
-                                                                               coef, gate);
+                                                                               coef, gate, isr, osr);
   return cudaGetLastError();
 }
 

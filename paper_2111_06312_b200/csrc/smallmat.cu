@@ -370,10 +370,235 @@ int grid_for(int64_t work, int threads, int cap) {
   return (int)b;
 }
 
+// ------------------------------------------------- cluster Cholesky + inverse (l > kCholSmemMax)
+// The l x l matrix is spread over a thread-block cluster (8 CTAs, 16 above l = 400) in
+// shared memory, block-cyclic by panels of kPanel rows.  Right-looking blocked Cholesky:
+// the owner of panel B factors its kPanel rows locally, the cluster syncs once, every CTA
+// copies the panel through DSMEM and applies the rank-kPanel update to its own rows.
+// The inverse of R is the blocked Gauss-Jordan back-substitution, in place, with the
+// same panel broadcast.  One cluster barrier per panel instead of one grid-wide barrier
+// per row.
+constexpr int kPanel = 8;
+
+struct ClusterLayout {
+  int CS, c, nblk, rows_max;
+  ISVD_DEVICE int owner(int i) const { return (i / kPanel) % CS; }
+  ISVD_DEVICE int local_row(int i) const { return ((i / kPanel) / CS) * kPanel + (i % kPanel); }
+  ISVD_DEVICE int global_row(int r) const { return ((r / kPanel) * CS + c) * kPanel + (r % kPanel); }
+};
+
+__global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __restrict__ G, int64_t ldg, int l,
+                                                               int64_t ld, float* __restrict__ Rinv32,
+                                                               double* __restrict__ R64, DevStatus* status,
+                                                               int force_fail, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;  // same value for every CTA of the cluster
+  cg::cluster_group cl = cg::this_cluster();
+  ClusterLayout L;
+  L.CS = (int)cl.num_blocks();
+  L.c = (int)cl.block_rank();
+  L.nblk = (l + kPanel - 1) / kPanel;
+  L.rows_max = ((L.nblk + L.CS - 1) / L.CS) * kPanel;
+  extern __shared__ double sm[];
+  double* A = sm;                                  // rows_max x l (own rows)
+  double* P = sm + (size_t)L.rows_max * l;         // kPanel x l (panel copy)
+  double* colk = P + (size_t)kPanel * l;           // rows_max x kPanel
+  __shared__ double s_misc[4];
+  __shared__ int s_bad, s_remote_bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int my_rows = ((L.nblk - L.c + L.CS - 1) / L.CS) * kPanel;
+
+  if (tid == 0) {
+    double tr = 0.0, mx = 0.0;
+    for (int i = 0; i < l; ++i) {
+      double d = G[(int64_t)i * ldg + i];
+      tr += d;
+      mx = d > mx ? d : mx;
+    }
+    s_misc[1] = tr;
+    s_misc[2] = mx;
+  }
+  __syncthreads();
+  const double trace = s_misc[1], tol = 1e-14 * s_misc[2];
+  double shift = 0.0;
+  int attempt, failed = 1;
+  for (attempt = 0; attempt < 4; ++attempt) {
+    cl.sync();  // nobody still reads our rows from a previous attempt
+    for (int t = tid; t < my_rows * l; t += nt) {
+      int r = t / l, j = t - r * l;
+      int gi = L.global_row(r);
+      double v = 0.0;
+      if (gi < l && j >= gi) v = G[(int64_t)gi * ldg + j] + (j == gi ? shift : 0.0);
+      A[t] = v;
+    }
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    int bad = 0;
+    for (int B = 0; B < L.nblk; ++B) {
+      const int own = B % L.CS, k0 = B * kPanel, kend = min(k0 + kPanel, l);
+      const int lb = (B / L.CS) * kPanel;
+      if (L.c == own) {
+        for (int kk = k0; kk < kend; ++kk) {
+          double* rk = A + (size_t)(lb + kk - k0) * l;
+          if (tid == 0) {
+            double piv = rk[kk];
+            int b = !(piv > tol) || !isfinite(piv);
+            if (b) s_bad = 1;
+            double rr = b ? 1.0 : sqrt(piv);
+            rk[kk] = rr;
+            s_misc[0] = 1.0 / rr;
+          }
+          __syncthreads();
+          const double inv = s_misc[0];
+          for (int j = kk + 1 + tid; j < l; j += nt) rk[j] *= inv;
+          __syncthreads();
+          const int nrem = kend - kk - 1;  // panel rows below kk
+          for (int t = tid; t < nrem * l; t += nt) {
+            int q = t / l, j = t - q * l;
+            int i2 = kk + 1 + q;
+            if (j >= i2) A[(size_t)(lb + i2 - k0) * l + j] -= rk[i2] * rk[j];
+          }
+          __syncthreads();
+        }
+      }
+      cl.sync();  // panel B final
+      const double* rem = cl.map_shared_rank(A, own) + (size_t)lb * l;
+      if (tid == 0) s_remote_bad = *cl.map_shared_rank(&s_bad, own);
+      const int nb = kend - k0;
+      for (int t = tid; t < nb * (l - k0); t += nt) {
+        int q = t / (l - k0), j = k0 + (t - q * (l - k0));
+        P[(size_t)q * l + j] = rem[(size_t)q * l + j];
+      }
+      __syncthreads();
+      if (s_remote_bad) { bad = 1; break; }
+      // rank-nb update of own rows i >= kend, columns j >= i
+      for (int t = tid; t < my_rows * (l - kend); t += nt) {
+        int r = t / (l - kend), j = kend + (t - r * (l - kend));
+        int gi = L.global_row(r);
+        if (gi < kend || gi >= l || j < gi) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kPanel; ++q)
+          if (q < nb) s += P[(size_t)q * l + gi] * P[(size_t)q * l + j];
+        A[(size_t)r * l + j] -= s;
+      }
+      __syncthreads();
+    }
+    if (force_fail && attempt == 0) bad = 1;
+    if (!bad) { failed = 0; break; }
+    shift = (attempt == 0) ? 1e-10 * trace : shift * 100.0;
+  }
+  if (L.c == 0 && tid == 0) {
+    if (attempt > 0) {
+      atomicAdd(&status->chol_breakdown, 1);
+      status->need_extra_pass = 1;
+    }
+    if (failed) status->chol_failed = 1;
+  }
+  if (R64) {
+    for (int t = tid; t < my_rows * l; t += nt) {
+      int r = t / l, j = t - r * l;
+      int gi = L.global_row(r);
+      if (gi < l) R64[(int64_t)gi * l + j] = A[t];
+    }
+  }
+  // ---- blocked Gauss-Jordan inverse, in place, panels from the bottom
+  for (int B = L.nblk - 1; B >= 0; --B) {
+    const int own = B % L.CS, k0 = B * kPanel, kend = min(k0 + kPanel, l);
+    const int lb = (B / L.CS) * kPanel;
+    const int nb = kend - k0;
+    // rows of a panel are final once its owner factored them; only the switch from the
+    // Cholesky (whose last panel is still being read) to the inverse needs a barrier
+    if (B == L.nblk - 1) cl.sync();
+    if (L.c == own) {
+      for (int kk = kend - 1; kk >= k0; --kk) {
+        double* rk = A + (size_t)(lb + kk - k0) * l;
+        const double d = rk[kk];
+        __syncthreads();
+        const double inv = 1.0 / d;
+        for (int j = kk + 1 + tid; j < l; j += nt) rk[j] *= inv;
+        if (tid == 0) rk[kk] = inv;
+        // rows of this panel above kk: save R[i][kk], then eliminate
+        for (int q = tid; q < kk - k0; q += nt) colk[q] = A[(size_t)(lb + q) * l + kk];
+        __syncthreads();
+        for (int t = tid; t < (kk - k0) * (l - kk); t += nt) {
+          int q = t / (l - kk), j = kk + (t - q * (l - kk));
+          double rik = colk[q];
+          double* ai = A + (size_t)(lb + q) * l;
+          ai[j] = (j == kk) ? -rik * inv : ai[j] - rik * rk[j];
+        }
+        __syncthreads();
+      }
+    }
+    cl.sync();  // panel rows of X final
+    const double* rem = cl.map_shared_rank(A, own) + (size_t)lb * l;
+    for (int t = tid; t < nb * (l - k0); t += nt) {
+      int q = t / (l - k0), j = k0 + (t - q * (l - k0));
+      P[(size_t)q * l + j] = rem[(size_t)q * l + j];
+    }
+    // save R[i][k0..kend) of own rows i < k0
+    for (int t = tid; t < my_rows * kPanel; t += nt) {
+      int r = t / kPanel, q = t - r * kPanel;
+      int gi = L.global_row(r);
+      colk[t] = (gi < k0 && q < nb) ? A[(size_t)r * l + k0 + q] : 0.0;
+    }
+    __syncthreads();
+    for (int t = tid; t < my_rows * (l - k0); t += nt) {
+      int r = t / (l - k0), j = k0 + (t - r * (l - k0));
+      int gi = L.global_row(r);
+      if (gi >= k0) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < kPanel; ++q)
+        if (q < nb && k0 + q <= j) s += colk[(size_t)r * kPanel + q] * P[(size_t)q * l + j];
+      double* a = A + (size_t)r * l + j;
+      *a = (j >= kend ? *a : 0.0) - s;
+    }
+    __syncthreads();
+  }
+  // ---- R^-1 -> fp32, upper, zero padded (ld x ld)
+  for (int t = tid; t < my_rows * ld; t += nt) {
+    int r = (int)(t / ld);
+    int64_t j = t - (int64_t)r * ld;
+    int gi = L.global_row(r);
+    if (gi >= l) continue;
+    Rinv32[(int64_t)gi * ld + j] = (j < l && j >= gi) ? (float)A[(size_t)r * l + j] : 0.f;
+  }
+  if (L.c == 0)
+    for (int64_t t = tid; t < (ld - l) * ld; t += nt) Rinv32[(int64_t)l * ld + t] = 0.f;
+  cl.sync();  // keep every CTA's shared memory alive until all remote reads are done
+}
+
 }  // namespace
 
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64, double* ws,
                             DevStatus* status, bool force_fail, const int* gate, cudaStream_t st) {
+  if (l > kCholSmemMax && l <= 512) {
+    const int CS = l <= 400 ? 8 : 16;
+    const int nblk = (l + kPanel - 1) / kPanel;
+    const int rows_max = ((nblk + CS - 1) / CS) * kPanel;
+    size_t smem = sizeof(double) * ((size_t)rows_max * l + (size_t)kPanel * l + (size_t)rows_max * kPanel);
+    static bool cattr = false;
+    if (!cattr) {
+      cudaFuncSetAttribute(chol_inv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(chol_inv_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cattr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ++g_launches;
+    return cudaLaunchKernelEx(&cfg, chol_inv_cluster_kernel, G, ldg, l, ld, Rinv32, R64, status,
+                              force_fail ? 1 : 0, gate);
+  }
   size_t smem = (l <= kCholSmemMax) ? sizeof(double) * (size_t)l * l : 0;
   static bool attr_set = false;
   if (!attr_set) {
