@@ -323,7 +323,7 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 bool use_slabs(isvd_ctx ctx, const isvd_op_s* op, int64_t wpad) {
   const int64_t n_full = op->g->n_pad * ctx->world;
   return op->kind == ISVD_OP_STACKED_PROPAGATION && ctx->world == 1 && wpad % kSlab == 0 &&
-         n_full * wpad * (int64_t)sizeof(float) > (64LL << 20);
+         n_full * wpad * (int64_t)sizeof(float) > (256LL << 20);
 }
 
 void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad) {

@@ -30,6 +30,30 @@ struct DevStatus {
 ISVD_DEVICE float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 ISVD_DEVICE void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 ISVD_DEVICE float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+// L2 eviction-priority policies (createpolicy, sm_80+): gather slabs are kept (evict_last)
+// while the once-per-pass CSR stream is marked evict_first so it does not push them out.
+ISVD_DEVICE uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+ISVD_DEVICE uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+ISVD_DEVICE float4 ldg4_hint(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+ISVD_DEVICE int ldg_hint(const int* ptr, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
 #endif
 
 // Kernels enqueued by this host thread (each launcher adds the number it launched);

@@ -80,6 +80,29 @@ ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, int len, const 
   return acc;
 }
 
+// Same, with L2 eviction priorities: gathered slab rows evict_last, CSR indices evict_first.
+ISVD_DEVICE Acc4 gather_segment_hint(const int32_t* __restrict__ idx, int len, const float* __restrict__ y,
+                                     int64_t stride, uint64_t keep, uint64_t stream) {
+  Acc4 acc{0.0, 0.0, 0.0, 0.0};
+  int e = 0;
+  for (; e + 8 <= len; e += 8) {
+    int j[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) j[u] = ldg_hint(idx + e + u, stream);
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ldg4_hint(y + (int64_t)j[u] * stride, keep);
+    float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
+    acc_add(acc, f4add(f4add(s01, s23), f4add(s45, s67)));
+  }
+  if (e < len) {
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; e < len; ++e) t = f4add(t, ldg4_hint(y + (int64_t)ldg_hint(idx + e, stream) * stride, keep));
+    acc_add(acc, t);
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
                                                     const int64_t* __restrict__ seg_beg,
                                                     const int32_t* __restrict__ seg_len,
@@ -111,6 +134,7 @@ __global__ void __launch_bounds__(256) spmm_slab_kernel(SpmmArgs a, const int32_
                                                         const int32_t* __restrict__ seg_slot, int64_t n_seg,
                                                         int slab0, int nslab, float* __restrict__ partial) {
   const int half = threadIdx.x & 1;
+  const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
   const int64_t n_items = n_seg * nslab;
   const int64_t stride_items = ((int64_t)gridDim.x * blockDim.x) >> 1;
   for (int64_t it = (((int64_t)blockIdx.x * blockDim.x) >> 1) + (threadIdx.x >> 1); it < n_items;
@@ -119,7 +143,7 @@ __global__ void __launch_bounds__(256) spmm_slab_kernel(SpmmArgs a, const int32_
     const int64_t s = __ldg(seg_order + (it - (it / n_seg) * n_seg));
     const int64_t row = __ldg(seg_row + s);
     const float* __restrict__ y = a.Y + (int64_t)sl * a.ysr * kSlab + 4 * half;
-    Acc4 acc = gather_segment(a.col_idx + __ldg(seg_beg + s), __ldg(seg_len + s), y, kSlab);
+    Acc4 acc = gather_segment_hint(a.col_idx + __ldg(seg_beg + s), __ldg(seg_len + s), y, kSlab, keep, stream);
     const int64_t col = (int64_t)sl * kSlab + 4 * half;
     const int slot = __ldg(seg_slot + s);
     if (slot < 0) {
