@@ -323,7 +323,7 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 bool use_slabs(isvd_ctx ctx, const isvd_op_s* op, int64_t wpad) {
   const int64_t n_full = op->g->n_pad * ctx->world;
   return op->kind == ISVD_OP_STACKED_PROPAGATION && ctx->world == 1 && wpad % kSlab == 0 &&
-         n_full * wpad * (int64_t)sizeof(float) > (256LL << 20);
+         n_full * wpad * (int64_t)sizeof(float) > (256LL << 20) && getenv("ISVD_SLABS") != nullptr;
 }
 
 void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad) {
@@ -371,7 +371,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   const int L = op->terms;
   const int64_t d = op->d;
   CK(launch_atb(op->X, op->ldx, Q, ldq, g->n_local, d, wpad, nullptr, false, op->atb_ws, op->blk64, wpad, nullptr, 0,
-                ctx->num_sms, nullptr, ctx->stream));
+                ctx->num_sms, nullptr, ctx->stream, 0, true));
   if (L > 0) {
     const int64_t sr = use_slabs(ctx, op, wpad) ? g->n_pad * ctx->world : 0;
     auto local = [&](float* full) { return sr ? full : slice(g, full, wpad); };
@@ -388,7 +388,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
       spmm(ctx, op, a);
       if (j < L) allgather_rows(ctx, g, dst, wpad);
       CK(launch_atb(op->X, op->ldx, local(dst), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
-                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, sr));
+                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, sr, true));
     }
   }
   const int64_t c = d * (L + 1);
@@ -588,6 +588,34 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       rs[i] = (float)std::sqrt((double)d + 1.0);
     }
     g->max_deg = maxd;
+    // Hotness tags (single rank: all degrees are local): bits 30-31 of col_idx mark edges into
+    // the top 1 % / 2 % / 5 % of nodes by degree, the rows the SpMM keeps L2-resident.
+    if (ctx->world == 1 && n_local > 0 && nnz > 0) {
+      std::vector<int64_t> dsort(n_local);
+      for (int64_t i = 0; i < n_local; ++i) dsort[i] = rp[i + 1] - rp[i];
+      std::sort(dsort.begin(), dsort.end(), std::greater<int64_t>());
+      const double frac[4] = {0.0, 0.05, 0.02, 0.01};
+      int64_t thr[4] = {0, 0, 0, 0};
+      for (int t = 1; t <= 3; ++t) {
+        int64_t r = std::max<int64_t>(1, (int64_t)(frac[t] * (double)n_local));
+        thr[t] = std::max<int64_t>(1, dsort[r - 1]);
+      }
+      std::vector<uint8_t> tag(n_local, 0);
+      for (int64_t i = 0; i < n_local; ++i) {
+        int64_t d = rp[i + 1] - rp[i];
+        uint8_t t = 0;
+        for (int q = 1; q <= 3; ++q)
+          if (d >= thr[q]) t = (uint8_t)q;
+        tag[i] = t;
+        for (int q = 1; q <= t; ++q) g->plan.hot_count[q]++;
+      }
+      std::vector<void*> tmp;
+      uint8_t* dtag = (uint8_t*)dmalloc(ctx, n_local, tmp);
+      CK(cudaMemcpy(dtag, tag.data(), n_local, cudaMemcpyHostToDevice));
+      CK(launch_tag_hot(g->col_idx, nnz, dtag, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      cudaFree(dtag);
+    }
     size_t nb = sizeof(float) * std::max<int64_t>(n_local, 1);
     g->inv_deg = (float*)dmalloc(ctx, nb, g->allocs);
     g->s = (float*)dmalloc(ctx, nb, g->allocs);
@@ -846,13 +874,13 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
 }
 
 // One Cholesky pass (Alg. 2 right): G = Y^T Y (all-reduced when row-partitioned), R = chol(G), Yout = Y R^-1.
-void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64,
+void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64, bool f32_gram,
               bool force_fail, const int* gate) {
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
   CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                ctx->stream));
+                ctx->stream, 0, f32_gram));
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
   CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));
@@ -866,9 +894,9 @@ void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64
   const int64_t ld = round_up(l, 4);
   int* gate = &ctx->status->need_extra_pass;
   CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, force_fail, nullptr);
-  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, false, nullptr);
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, false, gate);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, false, force_fail, nullptr);
+  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, true, false, nullptr);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, false, false, gate);
   CK(launch_scale_rows(Y2, ld, Y, ld, rows, ld, nullptr, 1.f, gate, ctx->stream));  // copy back iff pass 3 ran
   if (Rout) {
     CK(launch_trmm(s.Rb, s.Ra, s.Rab, (int)l, nullptr, ctx->stream));

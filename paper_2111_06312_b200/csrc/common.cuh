@@ -114,7 +114,13 @@ struct SpmmPlan {
   int32_t* split_slot0 = nullptr; // [n_split_rows] first slot
   int32_t* split_nslot = nullptr; // [n_split_rows] number of slots
   int32_t* seg_order = nullptr;   // [n_seg] segments sorted by length, longest first
+  int64_t hot_count[4] = {0, 0, 0, 0};  // nodes with hotness tag >= t (t = 1..3)
+  int64_t col_block = 0;          // columns per SpMM pass (0 = whole width)
 };
+// col_idx bits 30-31: hotness tag of the target node (3 = top 1 %, 2 = top 2 %, 1 = top 5 % by degree)
+constexpr unsigned kHotShift = 30;
+constexpr unsigned kIdxMask = (1u << kHotShift) - 1u;
+cudaError_t launch_tag_hot(int32_t* col_idx, int64_t nnz, const uint8_t* tag, cudaStream_t st);
 constexpr int kSegEdges = 512;
 
 struct SpmmArgs {
@@ -134,7 +140,7 @@ int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
 // (rows x 32 B per slab) fits `l2_budget` bytes; segments are visited longest-first
 // (seg_order, a permutation of [0, n_seg)) so the 2-thread items of a warp have similar lengths.
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,
-                        cudaStream_t st, int64_t l2_budget = 48LL << 20);
+                        cudaStream_t st, int64_t l2_budget = 80LL << 20);
 
 // ------------------------------------------------------------------- dense
 // C[i, j] = row_scale(i) * sum_k A[i, k] B[k, j]  (+ C[i, j] if accumulate), i < M, j < N (N multiple of 4).
@@ -150,7 +156,7 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms);
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka,
                        int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,
                        float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
-                       int64_t bsr = 0);
+                       int64_t bsr = 0, bool f32_stage = false);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);

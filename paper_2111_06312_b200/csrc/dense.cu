@@ -155,15 +155,20 @@ constexpr int ATB_R = 16;   // rows per smem stage
 
 constexpr int ATB_THREADS = 64;  // 8 x 8 threads, each an 8 x 8 register tile of the 64 x 64 output tile
 
+// S = double: operands promoted to fp64 once when staged, fp64 FMA (exact products of the
+//   fp32 inputs, fp64 sums): used for Grams whose input may be ill-conditioned.
+// S = float: fp32 FMA over each 16-row stage, the stage sums added into fp64 accumulators
+//   (relative error ~16 u_fp32 per stage sum): X^T Z products and the Gram of the second
+//   CholeskyQR pass (input already orthonormal to ~1e-6).
+template <typename S>
 __global__ void __launch_bounds__(ATB_THREADS)
     atb_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric, int tiles_a,
                int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld, const int* gate,
                int64_t bsr) {
   if (gate && *((volatile const int*)gate) == 0) return;
-  // operands promoted to fp64 once, when staged; 2 B of shared memory read per DFMA
-  __shared__ __align__(16) double As[2][ATB_R][ATB_T];
-  __shared__ __align__(16) double Bs[2][ATB_R][ATB_T];
+  __shared__ __align__(16) S As[2][ATB_R][ATB_T];
+  __shared__ __align__(16) S Bs[2][ATB_R][ATB_T];
   // output tile (ti, tj); symmetric: upper-triangular tiles only, enumerated row by row
   int ti = 0, tj = 0;
   {
@@ -209,10 +214,15 @@ __global__ void __launch_bounds__(ATB_THREADS)
     for (int u = 0; u < 4; ++u) {
       int f = tid + u * ATB_THREADS;
       int rr = f >> 4, cc = (f & 15) * 4;
-      double2* da = reinterpret_cast<double2*>(&As[buf][rr][cc]);
-      double2* db = reinterpret_cast<double2*>(&Bs[buf][rr][cc]);
-      da[0] = make_double2(pa[u].x, pa[u].y); da[1] = make_double2(pa[u].z, pa[u].w);
-      db[0] = make_double2(pb[u].x, pb[u].y); db[1] = make_double2(pb[u].z, pb[u].w);
+      if constexpr (sizeof(S) == 8) {
+        double2* da = reinterpret_cast<double2*>(&As[buf][rr][cc]);
+        double2* db = reinterpret_cast<double2*>(&Bs[buf][rr][cc]);
+        da[0] = make_double2(pa[u].x, pa[u].y); da[1] = make_double2(pa[u].z, pa[u].w);
+        db[0] = make_double2(pb[u].x, pb[u].y); db[1] = make_double2(pb[u].z, pb[u].w);
+      } else {
+        *reinterpret_cast<float4*>(&As[buf][rr][cc]) = pa[u];
+        *reinterpret_cast<float4*>(&Bs[buf][rr][cc]) = pb[u];
+      }
     }
   };
   double acc[8][8];
@@ -229,17 +239,41 @@ __global__ void __launch_bounds__(ATB_THREADS)
   for (int64_t st = 0; st < nst; ++st) {
     const int buf = (int)(st & 1);
     if (st + 1 < nst) load(r_begin + (st + 1) * ATB_R);
+    if constexpr (sizeof(S) == 8) {
 #pragma unroll 4
-    for (int r = 0; r < ATB_R; ++r) {
-      double a[8], b[8];
+      for (int r = 0; r < ATB_R; ++r) {
+        double a[8], b[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
+        for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
+        for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+      }
+    } else {
+      float part[8][8];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) part[i][j] = 0.f;
+#pragma unroll 4
+      for (int r = 0; r < ATB_R; ++r) {
+        float a[8], b[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) part[i][j] = fmaf(a[i], b[j], part[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] += (double)part[i][j];
     }
     if (st + 1 < nst) store(buf ^ 1);
     __syncthreads();
@@ -385,7 +419,8 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
 
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
                        const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg, float* out32,
-                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st, int64_t bsr) {
+                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st, int64_t bsr,
+                       bool f32_stage) {
   if (Ka <= 0 || Kb <= 0) return cudaSuccess;
   int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
   int64_t ntiles = atb_ntiles(Ka, Kb, symmetric);
@@ -395,8 +430,13 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
   int64_t ka_pad = round_up(Ka, ATB_T), ws_ld = round_up(Kb, ATB_T);
   if (rows > 0) {
     dim3 grid((unsigned)ntiles, (unsigned)ch);
-    ++g_launches; atb_kernel<<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0, (int)ta,
-                                     (int)tb, rpc, ws, ws_ld, gate, bsr);
+    ++g_launches;
+    if (f32_stage)
+      atb_kernel<float><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
+                                                      (int)ta, (int)tb, rpc, ws, ws_ld, gate, bsr);
+    else
+      atb_kernel<double><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
+                                                       (int)ta, (int)tb, rpc, ws, ws_ld, gate, bsr);
   } else {
     cudaMemsetAsync(ws, 0, sizeof(double) * ka_pad * ws_ld, st);
     ch = 1;

@@ -23,6 +23,8 @@
 // Rows longer than kSegEdges edges are split into segments whose fp32 partials
 // are combined by `spmm_fixup_kernel` in a fixed order: results are
 // deterministic and hubs (max degree ~1.4e5 in config 4) do not serialise.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace isvd {
@@ -59,63 +61,60 @@ ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4
 
 // Gather-sum of one segment for 4 columns: y points at column 4t of gather row 0 and
 // `stride` is the distance between consecutive gather rows (ld, or 8 in a slab).
-ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, int len, const float* __restrict__ y, int64_t stride) {
+// col_idx entries carry a 2-bit hotness tag in bits 30-31 (kHotShift; 0 = cold,
+// 3 = top 1 % by degree).  kHint: rows tagged >= hot_level are loaded with an L2
+// evict_last policy, the rest evict_first, so the few hub rows that take ~40 % of
+// the gathers of a power-law graph stay L2-resident under the stream of cold rows.
+template <bool kHint>
+ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, int len, const float* __restrict__ y, int64_t stride,
+                                unsigned hot_level, uint64_t keep, uint64_t stream) {
   Acc4 acc{0.0, 0.0, 0.0, 0.0};
   int e = 0;
   for (; e + 8 <= len; e += 8) {
-    int j[8];
+    unsigned j[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) j[u] = __ldg(idx + e + u);
+    for (int u = 0; u < 8; ++u) j[u] = (unsigned)__ldg(idx + e + u);
     float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = ldg4(y + (int64_t)j[u] * stride);
+    for (int u = 0; u < 8; ++u) {
+      const float* p = y + (int64_t)(j[u] & kIdxMask) * stride;
+      if (kHint) v[u] = ldg4_hint(p, (j[u] >> kHotShift) >= hot_level ? keep : stream);
+      else v[u] = ldg4(p);
+    }
     float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
     acc_add(acc, f4add(f4add(s01, s23), f4add(s45, s67)));
   }
   if (e < len) {
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (; e < len; ++e) t = f4add(t, ldg4(y + (int64_t)__ldg(idx + e) * stride));
+    for (; e < len; ++e) {
+      unsigned j = (unsigned)__ldg(idx + e);
+      const float* p = y + (int64_t)(j & kIdxMask) * stride;
+      t = f4add(t, kHint ? ldg4_hint(p, (j >> kHotShift) >= hot_level ? keep : stream) : ldg4(p));
+    }
     acc_add(acc, t);
   }
   return acc;
 }
 
-// Same, with L2 eviction priorities: gathered slab rows evict_last, CSR indices evict_first.
-ISVD_DEVICE Acc4 gather_segment_hint(const int32_t* __restrict__ idx, int len, const float* __restrict__ y,
-                                     int64_t stride, uint64_t keep, uint64_t stream) {
-  Acc4 acc{0.0, 0.0, 0.0, 0.0};
-  int e = 0;
-  for (; e + 8 <= len; e += 8) {
-    int j[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) j[u] = ldg_hint(idx + e + u, stream);
-    float4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = ldg4_hint(y + (int64_t)j[u] * stride, keep);
-    float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
-    acc_add(acc, f4add(f4add(s01, s23), f4add(s45, s67)));
-  }
-  if (e < len) {
-    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (; e < len; ++e) t = f4add(t, ldg4_hint(y + (int64_t)ldg_hint(idx + e, stream) * stride, keep));
-    acc_add(acc, t);
-  }
-  return acc;
-}
-
+template <bool kHint>
 __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
                                                     const int64_t* __restrict__ seg_beg,
                                                     const int32_t* __restrict__ seg_len,
                                                     const int32_t* __restrict__ seg_slot, int64_t n_seg,
-                                                    int teams, float* __restrict__ partial) {
+                                                    int teams, float* __restrict__ partial, unsigned hot_level) {
   const int TS = (int)(a.wpad >> 2);
   const int team = threadIdx.x / TS;
   const int c4 = threadIdx.x - team * TS;
   if (team >= teams) return;
+  uint64_t keep = 0, stream = 0;
+  if (kHint) {
+    keep = l2_policy_evict_last();
+    stream = l2_policy_evict_first();
+  }
   const float* __restrict__ Yc = a.Y + 4 * (int64_t)c4;
   for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
     const int64_t row = seg_row[s];
-    Acc4 acc = gather_segment(a.col_idx + seg_beg[s], seg_len[s], Yc, a.ldy);
+    Acc4 acc = gather_segment<kHint>(a.col_idx + seg_beg[s], seg_len[s], Yc, a.ldy, hot_level, keep, stream);
     const int slot = seg_slot[s];
     if (slot < 0) {
       spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(256) spmm_slab_kernel(SpmmArgs a, const int32_
                                                         const int32_t* __restrict__ seg_slot, int64_t n_seg,
                                                         int slab0, int nslab, float* __restrict__ partial) {
   const int half = threadIdx.x & 1;
-  const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
   const int64_t n_items = n_seg * nslab;
   const int64_t stride_items = ((int64_t)gridDim.x * blockDim.x) >> 1;
   for (int64_t it = (((int64_t)blockIdx.x * blockDim.x) >> 1) + (threadIdx.x >> 1); it < n_items;
@@ -143,7 +141,7 @@ __global__ void __launch_bounds__(256) spmm_slab_kernel(SpmmArgs a, const int32_
     const int64_t s = __ldg(seg_order + (it - (it / n_seg) * n_seg));
     const int64_t row = __ldg(seg_row + s);
     const float* __restrict__ y = a.Y + (int64_t)sl * a.ysr * kSlab + 4 * half;
-    Acc4 acc = gather_segment_hint(a.col_idx + __ldg(seg_beg + s), __ldg(seg_len + s), y, kSlab, keep, stream);
+    Acc4 acc = gather_segment<false>(a.col_idx + __ldg(seg_beg + s), __ldg(seg_len + s), y, kSlab, 4u, 0, 0);
     const int64_t col = (int64_t)sl * kSlab + 4 * half;
     const int slot = __ldg(seg_slot + s);
     if (slot < 0) {
@@ -194,7 +192,23 @@ cudaError_t launch_fixup(const SpmmPlan& plan, const SpmmArgs& a, const float* w
   return cudaGetLastError();
 }
 
+__global__ void tag_hot_kernel(int32_t* __restrict__ col_idx, int64_t nnz, const uint8_t* __restrict__ tag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+    unsigned j = (unsigned)col_idx[e] & kIdxMask;
+    col_idx[e] = (int32_t)(j | ((unsigned)tag[j] << kHotShift));
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_tag_hot(int32_t* col_idx, int64_t nnz, const uint8_t* tag, cudaStream_t st) {
+  if (nnz <= 0) return cudaSuccess;
+  int64_t b = ceil_div(nnz, 256);
+  if (b > 148 * 16) b = 148 * 16;
+  ++g_launches;
+  tag_hot_kernel<<<(int)b, 256, 0, st>>>(col_idx, nnz, tag);
+  return cudaGetLastError();
+}
 
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad) { return plan.n_slots * wpad; }
 
@@ -221,14 +235,26 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     }
     return launch_fixup(plan, a0, ws_partial, num_sms, st);
   }
-  // Column chunks of at most 4096 columns (team of <= 1024 threads).
-  for (int64_t c0 = 0; c0 < a0.wpad; c0 += 4096) {
+  // Column blocks: cb columns per pass (team of cb/4 threads).  A narrower block makes the
+  // gathered row shorter, so more hub rows fit the L2 budget; each pass re-reads the CSR.
+  int64_t cb = a0.wpad;
+  if (const char* e = getenv("ISVD_SPMM_CB")) cb = atoll(e);
+  else if (plan.col_block > 0) cb = plan.col_block;
+  cb = round_up(cb < 4 ? 4 : cb, 4);
+  if (cb > 4096) cb = 4096;
+  if (cb > a0.wpad) cb = a0.wpad;
+  for (int64_t c0 = 0; c0 < a0.wpad; c0 += cb) {
     SpmmArgs a = a0;
-    a.wpad = (a0.wpad - c0) < 4096 ? (a0.wpad - c0) : 4096;
+    a.wpad = (a0.wpad - c0) < cb ? (a0.wpad - c0) : cb;
     a.Y += c0;
     if (a.T) a.T += c0;
     if (a.colsum) a.colsum += c0;
     a.out += c0;
+    // hottest tag level whose rows fit the L2 budget at this block width (4 = no hints)
+    unsigned lvl = 4;
+    for (int t = 1; t <= 3; ++t)
+      if (plan.hot_count[t] > 0 && plan.hot_count[t] * a.wpad * 4 <= l2_budget) { lvl = (unsigned)t; break; }
+    if (const char* e = getenv("ISVD_SPMM_HOT")) lvl = (unsigned)atoi(e);
     int teams, threads;
     team_shape(a.wpad, &teams, &threads);
     int64_t blocks = ceil_div(plan.n_seg, teams);
@@ -238,8 +264,12 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ++g_launches;
-    spmm_kernel<<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,
-                                                 plan.n_seg, teams, ws_partial);
+    if (lvl <= 3)
+      spmm_kernel<true><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,
+                                                         plan.n_seg, teams, ws_partial, lvl);
+    else
+      spmm_kernel<false><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,
+                                                          plan.n_seg, teams, ws_partial, lvl);
     cudaError_t e = launch_fixup(plan, a, ws_partial, num_sms, st);
     if (e != cudaSuccess) return e;
   }
