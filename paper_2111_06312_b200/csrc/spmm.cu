@@ -251,10 +251,17 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     if (a.colsum) a.colsum += c0;
     a.out += c0;
     // hottest tag level whose rows fit the L2 budget at this block width (4 = no hints)
+    // Measured on B200 (profiles/r01_spmm_sweep.md): the hints did not beat the default
+    // replacement policy at config 4, so they are opt-in (ISVD_SPMM_HOT=auto|1..3).
     unsigned lvl = 4;
-    for (int t = 1; t <= 3; ++t)
-      if (plan.hot_count[t] > 0 && plan.hot_count[t] * a.wpad * 4 <= l2_budget) { lvl = (unsigned)t; break; }
-    if (const char* e = getenv("ISVD_SPMM_HOT")) lvl = (unsigned)atoi(e);
+    if (const char* e = getenv("ISVD_SPMM_HOT")) {
+      if (e[0] == 'a') {
+        for (int t = 1; t <= 3; ++t)
+          if (plan.hot_count[t] > 0 && plan.hot_count[t] * a.wpad * 4 <= l2_budget) { lvl = (unsigned)t; break; }
+      } else {
+        lvl = (unsigned)atoi(e);
+      }
+    }
     int teams, threads;
     team_shape(a.wpad, &teams, &threads);
     int64_t blocks = ceil_div(plan.n_seg, teams);
