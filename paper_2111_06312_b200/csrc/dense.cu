@@ -16,8 +16,12 @@ namespace isvd {
 namespace {
 
 // ------------------------------------------------------------------ GEMM
+// Thread (tx, ty) owns rows {g*4*TY + ty*4 + 0..3} and columns {g*4*TX + tx*4 + 0..3}: every
+// shared-memory float4 read of a quarter-warp covers 128 contiguous bytes (no bank conflicts).
+// A is stored transposed with 4 floats of padding per k-row so the transposing stores do
+// not conflict either.  __launch_bounds__(., 2): <= 128 registers, two CTAs per SM.
 template <int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
     gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                    float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                    const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate,
@@ -25,7 +29,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   if (gate && *((volatile const int*)gate) == 0) return;
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int TX = BN / TN;  // threads along N
-  __shared__ __align__(16) float As[2][BK][BM];
+  constexpr int TY = BM / TM;  // threads along M
+  __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN];
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -115,12 +120,12 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       float a[TM], b[TN];
 #pragma unroll
       for (int i = 0; i < TM; i += 4) {
-        float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
+        float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][(i / 4) * 4 * TY + ty * 4]);
         a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
       }
 #pragma unroll
       for (int j = 0; j < TN; j += 4) {
-        float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * TN + j]);
+        float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][(j / 4) * 4 * TX + tx * 4]);
         b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
       }
 #pragma unroll
@@ -135,13 +140,13 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    int64_t gm = m0 + ty * TM + i;
+    int64_t gm = m0 + (i / 4) * 4 * TY + ty * 4 + (i & 3);
     if (gm >= M) continue;
     float s = alpha;
     if (row_scale) s *= row_scale[gm];
 #pragma unroll
     for (int j = 0; j < TN; j += 4) {
-      int64_t gn = n0 + tx * TN + j;
+      int64_t gn = n0 + (j / 4) * 4 * TX + tx * 4;
       if (gn < N)
         *reinterpret_cast<float4*>(C + mat_off(ldc, csr, gm, gn)) =
             make_float4(s * acc[i][j], s * acc[i][j + 1], s * acc[i][j + 2], s * acc[i][j + 3]);
@@ -225,11 +230,21 @@ __global__ void __launch_bounds__(ATB_THREADS)
       }
     }
   };
-  double acc[8][8];
+  // fp64 accumulators: registers for S = double; shared memory for S = float (frees the
+  // registers for the fp32 stage sums; element q of thread t at accs[q][t], conflict-free)
+  constexpr int kAccRegs = sizeof(S) == 8 ? 8 : 1;
+  double acc[kAccRegs][kAccRegs == 8 ? 8 : 1];
+  __shared__ double accs[sizeof(S) == 8 ? 1 : 64][ATB_THREADS];
+  if constexpr (sizeof(S) == 8) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 64; ++q) accs[q][tid] = 0.0;
+    acc[0][0] = 0.0;
+  }
   const int64_t nst = (r_end - r_begin + ATB_R - 1) / ATB_R;
   if (nst > 0) {
     load(r_begin);
@@ -243,14 +258,19 @@ __global__ void __launch_bounds__(ATB_THREADS)
 #pragma unroll 4
       for (int r = 0; r < ATB_R; ++r) {
         double a[8], b[8];
+        // 4 x LDS.128 per operand; 8 lanes of a phase read 128 contiguous bytes (no conflicts)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
+        for (int q = 0; q < 4; ++q) {
+          double2 va = *reinterpret_cast<const double2*>(&As[buf][r][q * 16 + ty * 2]);
+          double2 vb = *reinterpret_cast<const double2*>(&Bs[buf][r][q * 16 + tx * 2]);
+          a[2 * q] = va.x; a[2 * q + 1] = va.y;
+          b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          for (int j = 0; j < 8; ++j) acc[i % kAccRegs][j % (kAccRegs == 8 ? 8 : 1)] =
+              fma(a[i], b[j], acc[i % kAccRegs][j % (kAccRegs == 8 ? 8 : 1)]);
       }
     } else {
       float part[8][8];
@@ -262,9 +282,12 @@ __global__ void __launch_bounds__(ATB_THREADS)
       for (int r = 0; r < ATB_R; ++r) {
         float a[8], b[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a[i] = As[buf][r][ty + 8 * i];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] = Bs[buf][r][tx + 8 * j];
+        for (int q = 0; q < 2; ++q) {
+          float4 va = *reinterpret_cast<const float4*>(&As[buf][r][q * 32 + ty * 4]);
+          float4 vb = *reinterpret_cast<const float4*>(&Bs[buf][r][q * 32 + tx * 4]);
+          a[4 * q] = va.x; a[4 * q + 1] = va.y; a[4 * q + 2] = va.z; a[4 * q + 3] = va.w;
+          b[4 * q] = vb.x; b[4 * q + 1] = vb.y; b[4 * q + 2] = vb.z; b[4 * q + 3] = vb.w;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -273,17 +296,24 @@ __global__ void __launch_bounds__(ATB_THREADS)
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] += (double)part[i][j];
+        for (int j = 0; j < 8; ++j) accs[i * 8 + j][tid] += (double)part[i][j];
     }
     if (st + 1 < nst) store(buf ^ 1);
     __syncthreads();
   }
-  // partial tile -> ws[chunk][a][b]  (ws_ld = padded Kb)
+  // partial tile -> ws[chunk][a][b]  (ws_ld = padded Kb).  Register element (i, j) of thread
+  // (tx, ty) is tile row rowmap(ty, i), column rowmap(tx, j).
+  auto tmap = [](int t, int q) { return sizeof(S) == 8 ? (q >> 1) * 16 + t * 2 + (q & 1) : (q >> 2) * 32 + t * 4 + (q & 3); };
   double* W = ws + chunk * (int64_t)((Ka + ATB_T - 1) / ATB_T * ATB_T) * ws_ld;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) W[(a0 + ty + 8 * i) * ws_ld + b0 + tx + 8 * j] = acc[i][j];
+    for (int j = 0; j < 8; ++j) {
+      double v;
+      if constexpr (sizeof(S) == 8) v = acc[i][j];
+      else v = accs[i * 8 + j][tid];
+      W[(a0 + tmap(ty, i)) * ws_ld + b0 + tmap(tx, j)] = v;
+    }
 }
 
 __global__ void atb_reduce_kernel(const double* __restrict__ ws, int64_t ws_ld, int64_t ka_pad, int nchunks,
