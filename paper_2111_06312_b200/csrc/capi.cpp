@@ -40,7 +40,8 @@ struct isvd_ctx_s {
   int num_sms = 148;
   std::string last_error;
   DevStatus* status = nullptr;  // device
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
+  cudaStream_t work = nullptr;  // private non-blocking stream the solver runs (and is captured) on
   std::atomic<int> live_graphs{0};
   // SpMM accounting of the current isvd_svd call
   bool profiling = false;
@@ -77,9 +78,11 @@ struct SolverWs {
   double *gram = nullptr, *Ra = nullptr, *Rb = nullptr, *Rc = nullptr, *Rab = nullptr, *Rfin = nullptr,
          *chol_ws = nullptr, *jac_ws = nullptr, *sigma = nullptr, *cand = nullptr, *cand_all = nullptr,
          *absmax_ws = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;  // the captured isvd for the argument set graph_key
   uint64_t graph_key = 0;
   bool graph_broken = false;
+  int64_t graph_launches = 0, graph_spmm_steps = 0;
+  double graph_alg_bytes = 0.0;
 };
 
 struct isvd_op_s {
@@ -187,6 +190,10 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   CK(cudaStreamSynchronize(ctx->stream));
   for (void* p : op->ws_allocs) cudaFree(p);
   op->ws_allocs.clear();
+  if (op->sws.graph_exec) {  // the captured solver referenced the freed buffers
+    cudaGraphExecDestroy(op->sws.graph_exec);
+    op->sws.graph_exec = nullptr;
+  }
   int64_t n_full = g->n_pad * ctx->world;
   size_t full_bytes = sizeof(float) * (size_t)n_full * wpad;
   op->full_a = (float*)dmalloc(ctx, full_bytes, op->ws_allocs);
@@ -500,6 +507,8 @@ isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id
     CK(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
     CK(cudaEventCreate(&ctx->ev0));
     CK(cudaEventCreate(&ctx->ev1));
+    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking));
     if (world > 1) {
       ncclUniqueId id;
       memcpy(&id, nccl_unique_id, sizeof(id));
@@ -525,6 +534,12 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->work) {
+    cudaStreamSynchronize(ctx->work);
+    cudaStreamDestroy(ctx->work);
+  }
+  for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   delete ctx;
   return ISVD_OK;
 }
@@ -834,6 +849,21 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
 // ==================================================================== solver
 namespace {
 
+// Everything a captured solver graph bakes in (FNV-1a over the argument values).
+uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t ldu, const float* V, int64_t ldv) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xFF;
+      h *= 0x100000001B3ULL;
+    }
+  };
+  mix((uint64_t)p->k); mix((uint64_t)(uint32_t)p->oversampling); mix((uint64_t)p->power_iters); mix(p->seed);
+  mix(p->flags); mix((uint64_t)(uintptr_t)p->omega); mix((uint64_t)l); mix((uint64_t)(uintptr_t)U);
+  mix((uint64_t)ldu); mix((uint64_t)(uintptr_t)V); mix((uint64_t)ldv);
+  return h;
+}
+
 int64_t working_l(const isvd_op_s* op, const isvd_svd_params* p) {
   int64_t r, c;
   op_shape(op, &r, &c);
@@ -1012,19 +1042,68 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     float* Ud = host_out ? s.Utmp : U;
     float* Vd = host_out ? s.Vtmp : V;
     const int64_t lduu = host_out ? ldk : ldu, ldvv = host_out ? ldk : ldv;
-    int64_t launches0 = g_launches;
+    // The solver runs on the context's private stream, joined to the caller's stream by
+    // events; without ISVD_SVD_NO_GRAPH / ISVD_SVD_PROFILE the whole enqueue sequence is
+    // captured once per argument set into a CUDA graph and replayed (one launch per isvd).
+    cudaStream_t user = ctx->stream;
+    CK(cudaEventRecord(ctx->ev_join, user));
+    CK(cudaStreamWaitEvent(ctx->work, ctx->ev_join, 0));
+    struct StreamSwap {
+      isvd_ctx c;
+      cudaStream_t u;
+      ~StreamSwap() { c->stream = u; c->profiling = false; }
+    } swap_back{ctx, user};
+    ctx->stream = ctx->work;
     ctx->profiling = p->flags & ISVD_SVD_PROFILE;
-    ctx->spmm_steps = 0;
-    ctx->spmm_alg_bytes = 0.0;
+    const uint64_t key = graph_key(p, l, Ud, lduu, Vd, ldvv);
+    const bool use_graph = !(p->flags & (ISVD_SVD_NO_GRAPH | ISVD_SVD_PROFILE)) && !s.graph_broken;
+    int64_t launches = 0;
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
-    try {
+    if (use_graph && (s.graph_exec == nullptr || s.graph_key != key)) {
+      if (s.graph_exec) cudaGraphExecDestroy(s.graph_exec);
+      s.graph_exec = nullptr;
+      ctx->spmm_steps = 0;
+      ctx->spmm_alg_bytes = 0.0;
+      const int64_t l0 = g_launches;
+      bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        try {
+          solver_body(op, p, l, Ud, lduu, Vd, ldvv);
+        } catch (const Fail&) {
+          ok = false;
+        }
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        ok = ok && e == cudaSuccess && graph != nullptr &&
+             cudaGraphInstantiate(&s.graph_exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+      }
+      if (!ok) {  // some launch could not be captured: fall back to eager enqueue for this op
+        (void)cudaGetLastError();
+        if (s.graph_exec) cudaGraphExecDestroy(s.graph_exec);
+        s.graph_exec = nullptr;
+        s.graph_broken = true;
+        ctx->last_error.clear();
+      } else {
+        s.graph_key = key;
+        s.graph_launches = g_launches - l0;
+        s.graph_spmm_steps = ctx->spmm_steps;
+        s.graph_alg_bytes = ctx->spmm_alg_bytes;
+      }
+    }
+    if (use_graph && s.graph_exec) {
+      CK(cudaGraphLaunch(s.graph_exec, ctx->stream));
+      launches = s.graph_launches;
+      ctx->spmm_steps = s.graph_spmm_steps;
+      ctx->spmm_alg_bytes = s.graph_alg_bytes;
+    } else {
+      ctx->spmm_steps = 0;
+      ctx->spmm_alg_bytes = 0.0;
+      const int64_t l0 = g_launches;
       solver_body(op, p, l, Ud, lduu, Vd, ldvv);
-    } catch (...) {
-      ctx->profiling = false;
-      throw;
+      launches = g_launches - l0;
     }
     CK(cudaEventRecord(ctx->ev1, ctx->stream));
-    ctx->profiling = false;
     DevStatus st;
     std::vector<double> sig(k);
     CK(cudaMemcpyAsync(sig.data(), s.sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1038,6 +1117,8 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
                            cudaMemcpyDeviceToHost, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaEventRecord(ctx->ev_join, ctx->stream));
+    CK(cudaStreamWaitEvent(user, ctx->ev_join, 0));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     if (rep) {
@@ -1046,7 +1127,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
       rep->chol_fallbacks = st.chol_breakdown;
       rep->jacobi_sweeps = st.jacobi_sweeps;
       rep->world = ctx->world;
-      rep->kernel_launches = (int32_t)(g_launches - launches0);
+      rep->kernel_launches = (int32_t)launches;
       rep->ms_total = ms;
       rep->spmm_steps = ctx->spmm_steps;
       rep->spmm_alg_bytes = ctx->spmm_alg_bytes;
