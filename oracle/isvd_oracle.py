@@ -266,3 +266,40 @@ def exact_svd(M, k: int):
     U, s, Vt = np.linalg.svd(np.asarray(M, dtype=np.float64), full_matrices=False)
     Uk, Vk = sign_fix(U[:, :k], Vt[:k].T)
     return Uk, s[:k].copy(), Vk, s.copy()
+
+
+def nc_blocks(op: "NCOperator"):
+    """The column blocks [X, A_hat X, ..., A_hat^L X] of Eq. 6, each by j repeated
+    sparse products, as a list (never concatenated: config 4 is 2.45M x 400)."""
+    blocks = [op.X]
+    P = op.X
+    for _ in range(op.L):
+        P = op.Ahat @ P
+        blocks.append(P)
+    return blocks
+
+
+def exact_svd_tall(blocks, k: int):
+    """Exact SVD_k of a tall M = [B_0 | B_1 | ...] through its c x c Gram:
+    M^T M = V S^2 V^T (LAPACK symmetric eigensolver), U = M V S^-1.  Used where M has far more
+    rows than columns and l = c makes Alg. 1 exact (config 4, reading O6).  Returns
+    (s[:k], V[:, :k], s_all, Ufun) with Ufun(rows) -> U[rows, :k] (sign rule of S:141 is not
+    applied: callers compare subspaces)."""
+    c = sum(b.shape[1] for b in blocks)
+    G = np.empty((c, c))
+    offs = np.cumsum([0] + [b.shape[1] for b in blocks])
+    for i, bi in enumerate(blocks):
+        for j in range(i, len(blocks)):
+            gij = bi.T @ blocks[j]
+            G[offs[i] : offs[i + 1], offs[j] : offs[j + 1]] = gij
+            G[offs[j] : offs[j + 1], offs[i] : offs[i + 1]] = gij.T
+    lam, V = np.linalg.eigh(G)
+    order = np.argsort(lam)[::-1]
+    lam, V = lam[order], V[:, order]
+    s_all = np.sqrt(np.maximum(lam, 0.0))
+
+    def Ufun(rows):
+        Mr = np.hstack([b[rows] for b in blocks])
+        return Mr @ V[:, :k] / s_all[:k]
+
+    return s_all[:k].copy(), V[:, :k].copy(), s_all, Ufun

@@ -270,6 +270,24 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     int64_t cap = (int64_t)num_sms * per_sm * 4;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    // Experiment hook (profiles/spmm_sweep.py): persisting-L2 window over the first
+    // ISVD_L2_WINDOW_MB of the gather source (hub rows first after a degree relabel).
+    static const char* win_env = getenv("ISVD_L2_WINDOW_MB");
+    if (win_env) {
+      static bool limit_set = false;
+      size_t want = (size_t)atoll(win_env) << 20;
+      if (!limit_set) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        limit_set = true;
+      }
+      cudaStreamAttrValue v = {};
+      v.accessPolicyWindow.base_ptr = (void*)a.Y;
+      v.accessPolicyWindow.num_bytes = want;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     ++g_launches;
     if (lvl <= 3)
       spmm_kernel<true><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,

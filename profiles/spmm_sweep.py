@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--cb", default="0,200,100,48")
     ap.add_argument("--hot", default="auto,4")
+    ap.add_argument("--relabel", action="store_true", help="relabel nodes by degree (hubs first)")
+    ap.add_argument("--window", default="", help="comma list of persisting-L2 window sizes (MB)")
     args = ap.parse_args()
     import torch
 
@@ -28,15 +30,26 @@ def main():
     cfg = get_config(args.config)
     sp = solver_params(cfg)
     g = make_graph(cfg)
+    import numpy as np
+
+    X = make_features(cfg["n"], cfg["d"], cfg["seed"]) if cfg["op"] == "NC" else None
+    if args.relabel:
+        order = np.argsort(-g.degrees(), kind="stable")  # new id t -> old node order[t]
+        perm = np.empty(g.n, dtype=np.int64)
+        perm[order] = np.arange(g.n)
+        g = g.permuted(perm)
+        if X is not None:
+            X = np.ascontiguousarray(X[order])
     ctx = isvd.Context(0)
     graph = isvd.Graph(ctx, g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
     if cfg["op"] == "NC":
-        X = make_features(cfg["n"], cfg["d"], cfg["seed"])
         op = isvd.NC(graph, torch.from_numpy(X).cuda(), sp["L"])
     else:
         op = isvd.NE(graph, sp["weights"], sp["lambda_ones"])
     p = -1 if cfg["p"] is None else cfg["p"]
     ref = None
+    if args.window:
+        os.environ["ISVD_L2_WINDOW_MB"] = args.window
     for cb in args.cb.split(","):
         for hot in args.hot.split(","):
             os.environ.pop("ISVD_SPMM_CB", None)

@@ -411,3 +411,20 @@ def test_isvd_rejects_bad_rank():
     """k > min(r, c) is an error."""
     with pytest.raises(ValueError):
         isvd(DenseOperator(np.eye(3)), 4, philox_omega(0, 0, 3, 4), iterations=1)
+
+
+def test_exact_svd_tall_matches_lapack_svd():
+    """exact_svd_tall (Gram route, used for config 4 where l = c) equals the LAPACK SVD of the
+    explicit stacked matrix on an NC design matrix of a random graph."""
+    from oracle.isvd_oracle import exact_svd_tall, nc_blocks
+
+    rng = np.random.default_rng(21)
+    A = _random_connected(300, 500, rng)
+    op = NCOperator(A, rng.standard_normal((300, 5)), 3)
+    s, V, s_all, Ufun = exact_svd_tall(nc_blocks(op), 8)
+    Ue, se, Ve, se_all = exact_svd(op.dense(), 8)
+    assert np.allclose(s_all, se_all, rtol=1e-10)
+    assert np.allclose(np.abs(V.T @ Ve), np.eye(8), atol=1e-8)
+    rows = np.arange(0, 300, 7)
+    Ur = Ufun(rows)
+    assert np.allclose(np.abs(np.sum(Ur * Ue[rows], axis=0)) / np.linalg.norm(Ur, axis=0) / np.linalg.norm(Ue[rows], axis=0), 1.0, atol=1e-8)

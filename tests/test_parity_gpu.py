@@ -269,3 +269,24 @@ def test_permutation_invariance_through_library(ctx):
     Ua = _to_np(a.U)
     Ub = _to_np(b.U)[perm]
     assert sin_theta(Ub[:, :16], Ua[:, :16]) <= 1e-3
+
+
+@pytest.mark.slow
+def test_isvd_config4_exact(ctx):
+    """Config 4: l = c = 400 makes Alg. 1 exact (reading O6), so the oracle is the exact SVD of
+    M = [X | AX | A^2X | A^3X], taken through its 400 x 400 Gram in fp64.
+    Checked: top-k singular values, V subspace, and U on 20,000 sampled rows."""
+    from oracle.isvd_oracle import exact_svd_tall, nc_blocks
+
+    op, ref, cfg, sp = _op(ctx, 4)
+    res = op.svd(sp["k"], -1, sp["q"], sp["seed"])
+    s, V, s_all, Ufun = exact_svd_tall(nc_blocks(ref), sp["k"])
+    assert sigma_rel(res.S, s) <= SIG_TOL
+    Vg = _to_np(res.V)
+    assert sin_theta(Vg, V) <= ANGLE_TOL
+    rows = np.sort(np.random.default_rng(0).choice(op.graph.n_local, 20000, replace=False))
+    Ug = _to_np(res.U)[rows]
+    Ur = Ufun(rows)
+    # same column space on the sampled rows: U_gpu[rows] = U_ref[rows] (V_ref^T V_gpu) up to rounding
+    Rot = V.T @ Vg
+    assert np.linalg.norm(Ug - Ur @ Rot) <= 1e-3 * np.linalg.norm(Ur)
