@@ -23,6 +23,9 @@
 
 using namespace isvd;
 
+// graphs with at least this many rows (single rank) are relabelled by degree
+constexpr int64_t kRelabelMinRows = 100000;
+
 namespace isvd {
 thread_local int64_t g_launches = 0;
 }
@@ -42,6 +45,7 @@ struct isvd_ctx_s {
   DevStatus* status = nullptr;  // device
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
   cudaStream_t work = nullptr;  // private non-blocking stream the solver runs (and is captured) on
+  size_t max_persist_l2 = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   std::atomic<int> live_graphs{0};
   // SpMM accounting of the current isvd_svd call
   bool profiling = false;
@@ -59,6 +63,8 @@ struct isvd_graph_s {
   float* s = nullptr;          // (d+1)^-1/2
   float* s2 = nullptr;         // (d+1)^-1
   float* rs = nullptr;         // (d+1)^1/2
+  int32_t* new2old = nullptr;  // relabelled graphs: caller row of internal row i (device); else null
+  std::vector<int32_t> h_new2old;
   SpmmPlan plan;
   std::vector<void*> allocs;
   std::atomic<int> refs{0};
@@ -236,7 +242,10 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
     e1 = ctx->prof_events[i + 1];
     CK(cudaEventRecord(e0, ctx->stream));
   }
-  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream));
+  // relabelled graphs: the leading (hub) rows of the gather source stay L2-persisting
+  size_t persist = 0;
+  if (g->new2old) persist = std::min(ctx->max_persist_l2, (size_t)(g->n_pad * ctx->world) * a.wpad * sizeof(float));
+  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist));
   if (e1) CK(cudaEventRecord(e1, ctx->stream));
   // algorithmic bytes of the step: CSR, scale vectors, the gather source read
   // once (all n rows), the epilogue operand T, the output
@@ -255,15 +264,25 @@ float* slice(const isvd_graph_s* g, float* full, int64_t ld) { return full + (si
 // ----------------------------------------------------------------- NE products
 // M Q = sum_c w_c T^c Q - lambda 1 (1^T Q), T = D^-1 A   (Eq. 3)
 // Horner: H_C = w_C Q; H_c = w_c Q + D^-1 A H_{c+1}; M Q = D^-1 A H_1 - lambda 1 cs^T.
-void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+// user_order: Q and out are in the caller's row order (relabelled graphs map at the boundary).
+void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
+               bool user_order) {
   isvd_graph g = op->g;
   const int C = op->terms;
-  CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));
+  const int32_t* omap = nullptr;
+  CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));  // order-free
   allreduce_f64(ctx, op->colsum, wpad);
+  if (user_order && g->new2old) {
+    CK(launch_scale_rows(Q, ldq, op->ptmp, wpad, g->n_local, wpad, nullptr, 1.f, nullptr, ctx->stream, g->new2old));
+    Q = op->ptmp;
+    ldq = wpad;
+    omap = g->new2old;
+  }
   const float* src = Q;
   int64_t lds = ldq;
   if (ctx->world > 1) {
-    CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr, ctx->stream));
+    CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr,
+                         ctx->stream));
     allgather_rows(ctx, g, op->full_a, wpad);
     src = op->full_a;
     lds = wpad;
@@ -287,17 +306,25 @@ void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out
   a.post_vec = g->inv_deg;
   a.post_coef = (C == 1) ? (float)op->w[0] : 1.f;
   a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
-  a.out = out; a.ldo = ldo;
+  a.out = out; a.ldo = ldo; a.out_map = omap;
   spmm(ctx, op, a);
 }
 
 // M^T Q = sum_c w_c (A D^-1)^c Q - lambda 1 (1^T Q)   (T^T = A D^-1 for symmetric A)
 // Horner: Ht_C = D^-1 w_C Q; Ht_c = D^-1 (w_c Q + A Ht_{c+1}); M^T Q = A Ht_1 - lambda 1 cs^T.
-void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
+                 bool user_order) {
   isvd_graph g = op->g;
   const int C = op->terms;
+  const int32_t* omap = nullptr;
   CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));
   allreduce_f64(ctx, op->colsum, wpad);
+  if (user_order && g->new2old) {
+    CK(launch_scale_rows(Q, ldq, op->ptmp, wpad, g->n_local, wpad, nullptr, 1.f, nullptr, ctx->stream, g->new2old));
+    Q = op->ptmp;
+    ldq = wpad;
+    omap = g->new2old;
+  }
   CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, g->inv_deg, (float)op->w[C - 1],
                        nullptr, ctx->stream));
   allgather_rows(ctx, g, op->full_a, wpad);
@@ -317,7 +344,7 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   SpmmArgs a = spmm_base(g, wpad);
   a.Y = src; a.ldy = wpad;
   a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
-  a.out = out; a.ldo = ldo;
+  a.out = out; a.ldo = ldo; a.out_map = omap;
   spmm(ctx, op, a);
 }
 
@@ -325,96 +352,94 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 // M G = sum_j A_hat^j X G_j  (Eq. 6), Horner from the deepest block, iterates stored
 // pre-scaled (Yt = s Y) so the gather needs no per-neighbour scale:
 //   Yt_L = s (X G_L);  Yt_j = s (X G_j) + s^2 ((A+I) Yt_{j+1});  out = X G_0 + s ((A+I) Yt_1).
-// Slab-major full buffers (L2-resident gather slabs) when the iterate is much larger than
-// L2; single-rank only (the all-gather of a row partition needs row-major blocks).
-bool use_slabs(isvd_ctx ctx, const isvd_op_s* op, int64_t wpad) {
-  const int64_t n_full = op->g->n_pad * ctx->world;
-  return op->kind == ISVD_OP_STACKED_PROPAGATION && ctx->world == 1 && wpad % kSlab == 0 &&
-         n_full * wpad * (int64_t)sizeof(float) > (256LL << 20) && getenv("ISVD_SLABS") != nullptr;
-}
-
-void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad) {
+// G (c rows) is never permuted; out rows are in the caller's order when user_order.
+void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* out, int64_t ldo, int64_t wpad,
+               bool user_order) {
   isvd_graph g = op->g;
   const int L = op->terms;
   const int64_t d = op->d;
+  const int32_t* omap = (user_order && g->new2old) ? g->new2old : nullptr;
   if (L == 0) {
     CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
-                      ctx->stream));
+                      ctx->stream, omap));
     return;
   }
-  const int64_t sr = use_slabs(ctx, op, wpad) ? g->n_pad * ctx->world : 0;  // slab rows of the full buffers
-  auto local = [&](float* full) { return sr ? full : slice(g, full, wpad); };
   float* bufs[2] = {op->full_a, op->full_b};
   float* cur = bufs[L & 1];
-  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, local(cur), wpad, g->n_local, wpad, d, g->s, 1.f,
-                    false, nullptr, ctx->stream, sr));
+  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, slice(g, cur, wpad), wpad, g->n_local, wpad, d,
+                    g->s, 1.f, false, nullptr, ctx->stream));
   allgather_rows(ctx, g, cur, wpad);
   for (int j = L - 1; j >= 1; --j) {
     CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)j * d * ldgm, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr,
                       1.f, false, nullptr, ctx->stream));
     float* dst = bufs[j & 1];
     SpmmArgs a = spmm_base(g, wpad);
-    a.Y = cur; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
+    a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
     a.post_vec = g->s2;
     a.T = op->ptmp; a.ldt = wpad; a.term_vec = g->s;
-    a.out = local(dst); a.ldo = wpad; a.osr = sr;
+    a.out = slice(g, dst, wpad); a.ldo = wpad;
     spmm(ctx, op, a);
     allgather_rows(ctx, g, dst, wpad);
     cur = dst;
   }
-  CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
+  // X G_0 in internal row order; with a row map it goes through ptmp (the in-place
+  // accumulation into `out` needs identical read and write rows)
+  float* t0 = omap ? op->ptmp : out;
+  const int64_t ldt0 = omap ? wpad : ldo;
+  CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, t0, ldt0, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
                     ctx->stream));
   SpmmArgs a = spmm_base(g, wpad);
-  a.Y = cur; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
+  a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
   a.post_vec = g->s;
-  a.T = out; a.ldt = ldo;  // in-place accumulate: each element is read then written by one thread
-  a.out = out; a.ldo = ldo;
+  a.T = t0; a.ldt = ldt0;  // may alias out: each element is read then written by one thread
+  a.out = out; a.ldo = ldo; a.out_map = omap;
   spmm(ctx, op, a);
 }
 
 // M^T Q: block j = X^T A_hat^j Q.  Zt_0 = s Q; Zt_{j+1} = s^2 ((A+I) Zt_j); block j = X^T diag(1/s) Zt_j.
-void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+// Q rows are in the caller's order when user_order (mapped by the first scaling pass).
+void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
+                 bool user_order) {
   isvd_graph g = op->g;
   const int L = op->terms;
   const int64_t d = op->d;
-  CK(launch_atb(op->X, op->ldx, Q, ldq, g->n_local, d, wpad, nullptr, false, op->atb_ws, op->blk64, wpad, nullptr, 0,
-                ctx->num_sms, nullptr, ctx->stream, 0, true));
-  if (L > 0) {
-    const int64_t sr = use_slabs(ctx, op, wpad) ? g->n_pad * ctx->world : 0;
-    auto local = [&](float* full) { return sr ? full : slice(g, full, wpad); };
-    float* bufs[2] = {op->full_a, op->full_b};
-    CK(launch_scale_rows(Q, ldq, local(bufs[0]), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream, 0, sr));
-    allgather_rows(ctx, g, bufs[0], wpad);
-    for (int j = 1; j <= L; ++j) {
-      float* src = bufs[(j - 1) & 1];
-      float* dst = bufs[j & 1];
-      SpmmArgs a = spmm_base(g, wpad);
-      a.Y = src; a.ldy = wpad; a.ysr = sr; a.self_coef = 1.f;
-      a.post_vec = g->s2;
-      a.out = local(dst); a.ldo = wpad; a.osr = sr;
-      spmm(ctx, op, a);
-      if (j < L) allgather_rows(ctx, g, dst, wpad);
-      CK(launch_atb(op->X, op->ldx, local(dst), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
-                    op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, sr, true));
-    }
+  const int32_t* imap = (user_order && g->new2old) ? g->new2old : nullptr;
+  float* bufs[2] = {op->full_a, op->full_b};
+  // Zt_0 = s Q (internal row order), block 0 = X^T diag(1/s) Zt_0
+  CK(launch_scale_rows(Q, ldq, slice(g, bufs[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream,
+                       imap));
+  CK(launch_atb(op->X, op->ldx, slice(g, bufs[0], wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
+                op->blk64, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, true));
+  if (L > 0) allgather_rows(ctx, g, bufs[0], wpad);
+  for (int j = 1; j <= L; ++j) {
+    float* src = bufs[(j - 1) & 1];
+    float* dst = bufs[j & 1];
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = src; a.ldy = wpad; a.self_coef = 1.f;
+    a.post_vec = g->s2;
+    a.out = slice(g, dst, wpad); a.ldo = wpad;
+    spmm(ctx, op, a);
+    if (j < L) allgather_rows(ctx, g, dst, wpad);
+    CK(launch_atb(op->X, op->ldx, slice(g, dst, wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
+                  op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, true));
   }
   const int64_t c = d * (L + 1);
   allreduce_f64(ctx, op->blk64, (size_t)c * wpad);
   CK(launch_f64_to_f32(op->blk64, wpad, out, ldo, c, wpad, ctx->stream));
 }
 
-void op_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+void op_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool user_order) {
   isvd_ctx ctx = op->g->ctx;
   ensure_op_ws(op, wpad);
-  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad);
-  else nc_matmul(ctx, op, Q, ldq, out, ldo, wpad);
+  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  else nc_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
 }
 
-void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad) {
+void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool user_order) {
   isvd_ctx ctx = op->g->ctx;
   ensure_op_ws(op, wpad);
-  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad);
-  else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad);
+  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
 }
 
 void op_shape(const isvd_op_s* op, int64_t* r, int64_t* c) {
@@ -509,6 +534,9 @@ isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id
     CK(cudaEventCreate(&ctx->ev1));
     CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking));
+    int persist = 0;
+    CK(cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+    ctx->max_persist_l2 = (size_t)persist;
     if (world > 1) {
       ncclUniqueId id;
       memcpy(&id, nccl_unique_id, sizeof(id));
@@ -579,18 +607,50 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->n_local = n_local;
     g->n_pad = (n_global + ctx->world - 1) / ctx->world;
     g->nnz = nnz;
+    std::vector<int32_t> ci(nnz);
+    if (nnz > 0) {
+      if (dev) CK(cudaMemcpy(ci.data(), col_idx + base, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+      else memcpy(ci.data(), col_idx + base, sizeof(int32_t) * nnz);
+    }
+    if (flags & ISVD_GRAPH_VALIDATE)
+      for (int64_t e = 0; e < nnz; ++e)
+        REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
+    // Degree relabelling (single rank, large graphs; SURVEY 8(d2) "allowed optimisation"):
+    // internal row t is caller row order[t], in decreasing degree, so the hub rows that take
+    // most gathers form one contiguous prefix of every iterate, which the SpMM marks
+    // L2-persisting.  A symmetric permutation of A: singular values are unchanged and every
+    // caller-ordered input/output is mapped at the boundary (X, Omega, U, V, matmul I/O).
+    if (ctx->world == 1 && n_local >= kRelabelMinRows) {
+      std::vector<int32_t> order(n_local), new_of_old(n_local);
+      for (int64_t i = 0; i < n_local; ++i) order[i] = (int32_t)i;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+      for (int64_t t = 0; t < n_local; ++t) new_of_old[order[t]] = (int32_t)t;
+      std::vector<int64_t> rp2(n_local + 1);
+      std::vector<int32_t> ci2(nnz);
+      rp2[0] = 0;
+      for (int64_t t = 0; t < n_local; ++t) {
+        const int64_t o = order[t], b = rp[o], d = rp[o + 1] - rp[o];
+        for (int64_t e = 0; e < d; ++e) ci2[rp2[t] + e] = new_of_old[ci[b + e]];
+        rp2[t + 1] = rp2[t] + d;
+      }
+      rp.swap(rp2);
+      ci.swap(ci2);
+      g->new2old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, g->allocs);
+      CK(cudaMemcpy(g->new2old, order.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice));
+      g->h_new2old.swap(order);
+      if (ctx->max_persist_l2 > 0) {
+        static bool limit_set = false;  // process-wide L2 set-aside for persisting accesses
+        if (!limit_set) {
+          CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ctx->max_persist_l2));
+          limit_set = true;
+        }
+      }
+    }
     g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
     CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
     g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), g->allocs);
-    if (nnz > 0)
-      CK(cudaMemcpy(g->col_idx, col_idx + base, sizeof(int32_t) * nnz,
-                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-    if (flags & ISVD_GRAPH_VALIDATE) {
-      std::vector<int32_t> ci(nnz);
-      if (nnz) CK(cudaMemcpy(ci.data(), g->col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
-      for (int64_t e = 0; e < nnz; ++e)
-        REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
-    }
+    if (nnz > 0) CK(cudaMemcpy(g->col_idx, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
     // degrees (integers) -> scale vectors computed once in fp64, stored fp32 (reading O3)
     std::vector<float> inv(n_local), s(n_local), s2(n_local), rs(n_local);
     int64_t maxd = 0;
@@ -603,34 +663,6 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       rs[i] = (float)std::sqrt((double)d + 1.0);
     }
     g->max_deg = maxd;
-    // Hotness tags (single rank: all degrees are local): bits 30-31 of col_idx mark edges into
-    // the top 1 % / 2 % / 5 % of nodes by degree, the rows the SpMM keeps L2-resident.
-    if (ctx->world == 1 && n_local > 0 && nnz > 0) {
-      std::vector<int64_t> dsort(n_local);
-      for (int64_t i = 0; i < n_local; ++i) dsort[i] = rp[i + 1] - rp[i];
-      std::sort(dsort.begin(), dsort.end(), std::greater<int64_t>());
-      const double frac[4] = {0.0, 0.05, 0.02, 0.01};
-      int64_t thr[4] = {0, 0, 0, 0};
-      for (int t = 1; t <= 3; ++t) {
-        int64_t r = std::max<int64_t>(1, (int64_t)(frac[t] * (double)n_local));
-        thr[t] = std::max<int64_t>(1, dsort[r - 1]);
-      }
-      std::vector<uint8_t> tag(n_local, 0);
-      for (int64_t i = 0; i < n_local; ++i) {
-        int64_t d = rp[i + 1] - rp[i];
-        uint8_t t = 0;
-        for (int q = 1; q <= 3; ++q)
-          if (d >= thr[q]) t = (uint8_t)q;
-        tag[i] = t;
-        for (int q = 1; q <= t; ++q) g->plan.hot_count[q]++;
-      }
-      std::vector<void*> tmp;
-      uint8_t* dtag = (uint8_t*)dmalloc(ctx, n_local, tmp);
-      CK(cudaMemcpy(dtag, tag.data(), n_local, cudaMemcpyHostToDevice));
-      CK(launch_tag_hot(g->col_idx, nnz, dtag, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      cudaFree(dtag);
-    }
     size_t nb = sizeof(float) * std::max<int64_t>(n_local, 1);
     g->inv_deg = (float*)dmalloc(ctx, nb, g->allocs);
     g->s = (float*)dmalloc(ctx, nb, g->allocs);
@@ -687,12 +719,6 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     p.split_row = up32(split_row);
     p.split_slot0 = up32(split_slot0);
     p.split_nslot = up32(split_nslot);
-    {
-      std::vector<int32_t> order(seg_row.size());
-      for (size_t t = 0; t < order.size(); ++t) order[t] = (int32_t)t;
-      std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return seg_len[a] > seg_len[b]; });
-      p.seg_order = up32(order);
-    }
     p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<size_t>(seg_beg.size(), 1), g->allocs);
     if (!seg_beg.empty())
       CK(cudaMemcpy(p.seg_beg, seg_beg.data(), sizeof(int64_t) * seg_beg.size(), cudaMemcpyHostToDevice));
@@ -757,16 +783,31 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
       op->d = desc->d;
       op->ldx = desc->ldx;
       const bool dev = desc->x_flags & ISVD_PTR_DEVICE;
-      if (dev && (desc->x_flags & ISVD_BORROW)) {
+      if (dev && (desc->x_flags & ISVD_BORROW) && !g->new2old) {
         REQ(aligned16(desc->X), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
         op->X = desc->X;
       } else {
-        // copy with padding columns zeroed (ldx kept)
+        // own copy (ldx kept); a relabelled graph stores X's rows in its internal order
         std::vector<void*> tmp;
-        float* x = (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * desc->ldx, tmp);
-        if (g->n_local > 0)
-          CK(cudaMemcpy(x, desc->X, sizeof(float) * (size_t)g->n_local * desc->ldx,
-                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        const size_t row_bytes = sizeof(float) * (size_t)desc->ldx;
+        float* x = (float*)dmalloc(ctx, row_bytes * (size_t)std::max<int64_t>(g->n_local, 1), tmp);
+        if (g->n_local > 0) {
+          if (!g->new2old) {
+            CK(cudaMemcpy(x, desc->X, row_bytes * (size_t)g->n_local,
+                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+          } else if (dev) {
+            REQ(aligned16(desc->X), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
+            CK(launch_scale_rows(desc->X, desc->ldx, x, desc->ldx, g->n_local, desc->ldx, nullptr, 1.f, nullptr,
+                                 ctx->stream, g->new2old));
+            CK(cudaStreamSynchronize(ctx->stream));
+          } else {
+            std::vector<float> h((size_t)g->n_local * desc->ldx);
+            const float* src = desc->X;
+            for (int64_t i = 0; i < g->n_local; ++i)
+              memcpy(h.data() + (size_t)i * desc->ldx, src + (size_t)g->h_new2old[i] * desc->ldx, row_bytes);
+            CK(cudaMemcpy(x, h.data(), row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
+          }
+        }
         op->X = x;
         op->own_x = true;
       }
@@ -829,7 +870,7 @@ isvd_status isvd_matmul(isvd_op op, const float* Q, int64_t w, int64_t ldq, floa
   if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    op_matmul(op, Q, ldq, out, ldo, round_up(w, 4));
+    op_matmul(op, Q, ldq, out, ldo, round_up(w, 4), true);
   });
 }
 
@@ -842,7 +883,7 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
   if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    op_matmul_T(op, Q, ldq, out, ldo, round_up(w, 4));
+    op_matmul_T(op, Q, ldq, out, ldo, round_up(w, 4), true);
   });
 }
 
@@ -910,7 +951,7 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
   CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                ctx->stream, 0, f32_gram));
+                ctx->stream, f32_gram));
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
   CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));
@@ -951,7 +992,7 @@ isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* 
     int64_t l = working_l(op, params);
     REQ(ldo >= round_up(l, 4) && ldo % 4 == 0 && aligned16(omega), ISVD_ERR_INVALID_ARG, "bad omega ld");
     int64_t row0 = op->kind == ISVD_OP_POWER_SUM ? op->g->row_begin : 0;
-    CK(launch_omega(params->seed, row0, c_rows_local(op), (int)l, ldo, omega, ctx->stream));
+    CK(launch_omega(params->seed, row0, c_rows_local(op), (int)l, ldo, omega, nullptr, ctx->stream));
   });
 }
 
@@ -971,31 +1012,34 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   const bool force = p->flags & ISVD_SVD_FORCE_CHOL_FAIL;
   CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
   // Alg. 1 line 4: Q ~ N(0,1)^{c x l}
+  // (NE on a relabelled graph: Omega's rows are node ids, mapped to the internal order)
+  const int32_t* omap = ne ? g->new2old : nullptr;
   if (p->flags & ISVD_SVD_OMEGA_PROVIDED) {
-    CK(cudaMemcpy2DAsync(s.Qc, ld * sizeof(float), p->omega, ld * sizeof(float), ld * sizeof(float), cr,
-                         cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(launch_scale_rows(p->omega, ld, s.Qc, ld, cr, ld, nullptr, 1.f, nullptr, ctx->stream, omap));
   } else {
-    CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, ctx->stream));
+    CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, omap, ctx->stream));
   }
   // Alg. 1 lines 5-8
   for (int it = 0; it < p->power_iters; ++it) {
-    op_matmul(op, s.Qc, ld, s.Yr, ld, ld);                       // M Q       (r x l)
+    op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);                // M Q       (r x l)
     cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);          // orthonorm
-    op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld);                     // M^T Q     (c x l)
+    op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);              // M^T Q     (c x l)
     cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr);            // orthonorm
   }
   // Alg. 1 line 9: Q <- orthonorm(M Q)
-  op_matmul(op, s.Qc, ld, s.Yr, ld, ld);
+  op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);
   cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);
   // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
-  op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld);
+  op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);
   cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin);
   // Alg. 1 line 11: svd(B) with B = R^T Q_W^T -> one-sided Jacobi on R^T
   CK(launch_jacobi_svd(s.Rfin, (int)l, (int)k, ldk, s.sigma, s.Ub, s.Vb, s.jac_ws, ctx->status, ctx->num_sms,
                        ctx->stream));
   // Alg. 1 line 12: U = Q U_B;  V = Q_W V_B;  truncate to k
-  CK(launch_gemm_tn(s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream));
-  CK(launch_gemm_tn(s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream));
+  // (relabelled graphs: rows go back to the caller's order here)
+  CK(launch_gemm_tn(s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream, g->new2old));
+  CK(launch_gemm_tn(s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream,
+                    ne ? g->new2old : nullptr));
   // sign rule (reading O9)
   CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
   const double* cand = s.cand;

@@ -5,15 +5,8 @@
 #include <stdint.h>
 
 #define ISVD_DEVICE __device__ __forceinline__
-#if defined(__CUDACC__)
-#define ISVD_HOSTDEV __host__ __device__
-#else
-#define ISVD_HOSTDEV
-#endif
 
 namespace isvd {
-
-constexpr int kNumSMs = 148;  // B200; the runtime value is queried, this is only a default
 
 // Device-side status word shared by every kernel of one solver call.
 // Kernels set bits; the host reads the word once at the end of isvd_svd.
@@ -30,30 +23,6 @@ struct DevStatus {
 ISVD_DEVICE float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 ISVD_DEVICE void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 ISVD_DEVICE float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-// L2 eviction-priority policies (createpolicy, sm_80+): gather slabs are kept (evict_last)
-// while the once-per-pass CSR stream is marked evict_first so it does not push them out.
-ISVD_DEVICE uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-ISVD_DEVICE uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-ISVD_DEVICE float4 ldg4_hint(const float* ptr, uint64_t pol) {
-  float4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(ptr), "l"(pol));
-  return v;
-}
-ISVD_DEVICE int ldg_hint(const int* ptr, uint64_t pol) {
-  int v;
-  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
-  return v;
-}
 #endif
 
 // Kernels enqueued by this host thread (each launcher adds the number it launched);
@@ -61,24 +30,20 @@ ISVD_DEVICE int ldg_hint(const int* ptr, uint64_t pol) {
 extern thread_local int64_t g_launches;
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
-
-// Dense operands are either ROW-MAJOR (element (i, c) at p[i*ld + c]) or SLAB-MAJOR:
-// columns grouped in slabs of kSlab = 8 (32 bytes), each slab a contiguous sr x 8
-// block, element (i, c) at p[((c/8)*sr + i)*8 + c%8].  Slab-major gather sources
-// keep one slab (n x 32 B) resident in L2 while the SpMM streams the CSR over it.
-constexpr int kSlab = 8;
-ISVD_HOSTDEV inline int64_t mat_off(int64_t ld, int64_t sr, int64_t i, int64_t c) {
-  return sr ? ((c >> 3) * sr + i) * 8 + (c & 7) : i * ld + c;
-}
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// Row maps.  A graph may be relabelled internally (degree-descending, so hub rows are
+// contiguous and L2-persistable); `new2old[i]` is the caller's row of internal row i.
+// Kernels that read a caller-ordered operand take an `in_map`, kernels that write a
+// caller-ordered result take an `out_map` (nullptr = identity).
 
 // ---------------------------------------------------------------- launchers
 // All launchers enqueue on `st` and return cudaGetLastError().
 
-// Omega (Alg. 1 line 4): rows [row0, row0+rows) of the c x l matrix, ld >= l;
-// padding columns [l, ld) are written as 0.
+// Omega (Alg. 1 line 4): `rows` rows of the c x l matrix, ld >= l; row i is global
+// row (row_map ? row_map[i] : row0 + i).  Padding columns [l, ld) are written as 0.
 cudaError_t launch_omega(uint64_t seed, int64_t row0, int64_t rows, int l, int64_t ld, float* out,
-                         cudaStream_t st);
+                         const int32_t* row_map, cudaStream_t st);
 
 // Column sums (fp64) of a rows x w fp32 matrix: out[j] = sum_i Q[i, j], j < wpad (wpad = round_up(w,4)).
 // Deterministic two-stage reduction; `ws` needs colsum_ws_doubles(rows, wpad) doubles.
@@ -86,11 +51,10 @@ int64_t colsum_ws_doubles(int64_t rows, int64_t wpad);
 cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ldq, double* ws, double* out,
                           cudaStream_t st);
 
-// out[i, :] = coef * (vec ? vec[i] : 1) * in[i, :]  for i < rows, columns < wpad.
-// isr / osr: slab rows of in / out (0 = row-major).
+// out[i, :] = coef * (vec ? vec[i] : 1) * in[in_map ? in_map[i] : i, :]  for i < rows, columns < wpad.
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows,
                               int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st,
-                              int64_t isr = 0, int64_t osr = 0);
+                              const int32_t* in_map = nullptr);
 
 // ------------------------------------------------------------------- SpMM
 // Fused CSR SpMM step (K1):  for each local row i (global id row_offset + i)
@@ -98,6 +62,7 @@ cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t 
 //   out_i = post_coef * post_vec[i] * acc_i
 //         + term_coef * term_vec[i] * T[i]
 //         - rank1_coef * colsum                                          (all in fp64, one rounding)
+// written to out row (out_map ? out_map[i] : i).
 // Rows are processed as segments of <= kSegEdges edges; long rows are split and
 // their fp32 partial sums combined in a fixed order by a fixup pass.
 struct SpmmPlan {
@@ -113,14 +78,7 @@ struct SpmmPlan {
   int32_t* split_row = nullptr;   // [n_split_rows] local row id
   int32_t* split_slot0 = nullptr; // [n_split_rows] first slot
   int32_t* split_nslot = nullptr; // [n_split_rows] number of slots
-  int32_t* seg_order = nullptr;   // [n_seg] segments sorted by length, longest first
-  int64_t hot_count[4] = {0, 0, 0, 0};  // nodes with hotness tag >= t (t = 1..3)
-  int64_t col_block = 0;          // columns per SpMM pass (0 = whole width)
 };
-// col_idx bits 30-31: hotness tag of the target node (3 = top 1 %, 2 = top 2 %, 1 = top 5 % by degree)
-constexpr unsigned kHotShift = 30;
-constexpr unsigned kIdxMask = (1u << kHotShift) - 1u;
-cudaError_t launch_tag_hot(int32_t* col_idx, int64_t nnz, const uint8_t* tag, cudaStream_t st);
 constexpr int kSegEdges = 512;
 
 struct SpmmArgs {
@@ -132,31 +90,31 @@ struct SpmmArgs {
   const float* T; int64_t ldt; const float* term_vec; float term_coef;
   const double* colsum; double rank1_coef;
   float* out; int64_t ldo;
-  int64_t wpad;           // columns processed (multiple of 4; of 8 with slab-major Y)
-  int64_t ysr = 0, tsr = 0, osr = 0;  // slab rows of Y / T / out (0 = row-major)
+  const int32_t* out_map;  // nullable
+  int64_t wpad;            // columns processed (multiple of 4)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
-// With a slab-major Y the step runs one launch per group of slabs whose gather footprint
-// (rows x 32 B per slab) fits `l2_budget` bytes; segments are visited longest-first
-// (seg_order, a permutation of [0, n_seg)) so the 2-thread items of a warp have similar lengths.
+// `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled
+// graph) are marked L2-persisting for this launch (cudaAccessPolicyWindow on `st`).
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,
-                        cudaStream_t st, int64_t l2_budget = 80LL << 20);
+                        cudaStream_t st, size_t persist_bytes = 0);
 
 // ------------------------------------------------------------------- dense
-// C[i, j] = row_scale(i) * sum_k A[i, k] B[k, j]  (+ C[i, j] if accumulate), i < M, j < N (N multiple of 4).
+// C[out_map ? out_map[i] : i, j] = alpha * row_scale(i) * sum_k A[i, k] B[k, j],  i < M, j < N (N multiple of 4).
 // B is K x N row-major (ldb).  upper_tri_b: B[k, j] = 0 for k > j (skips those k).
 cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                            int64_t M, int64_t N, int64_t K, const float* row_scale, float alpha,
-                           bool upper_tri_b, const int* gate, cudaStream_t st, int64_t csr = 0);
+                           bool upper_tri_b, const int* gate, cudaStream_t st, const int32_t* out_map = nullptr);
 
 // G = A^T diag(row_scale) B over `rows` rows, A: rows x Ka, B: rows x Kb -> fp64 Ka x ldg.
 // symmetric: A == B, only the upper triangle of tiles is computed and mirrored.
 // If out32 != null the result is also written as fp32 (ld32).
+// f32_stage: fp32 sums over 16-row stages added into fp64 (else fp64 FMA throughout).
 int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms);
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka,
                        int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,
                        float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
-                       int64_t bsr = 0, bool f32_stage = false);
+                       bool f32_stage = false);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);
@@ -171,7 +129,7 @@ cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t 
 // Breakdown (pivot <= 1e-14 * max diag, or non-finite) -> shift the diagonal by
 // 1e-10 * trace (x100 per retry, 3 retries); status->chol_breakdown++ and
 // status->need_extra_pass = 1.  force_fail treats the first attempt as broken.
-// `ws` needs l*l doubles when l > kCholSmemMax (global-memory path).
+// `ws` needs l*l doubles when l > 512 (global-memory path).
 constexpr int kCholSmemMax = 160;
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64,
                             double* ws, DevStatus* status, bool force_fail, const int* gate, cudaStream_t st);

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
     gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                    float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                    const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate,
-                   int64_t csr) {
+                   const int32_t* __restrict__ out_map) {
   if (gate && *((volatile const int*)gate) == 0) return;
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int TX = BN / TN;  // threads along N
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
     for (int j = 0; j < TN; j += 4) {
       int64_t gn = n0 + (j / 4) * 4 * TX + tx * 4;
       if (gn < N)
-        *reinterpret_cast<float4*>(C + mat_off(ldc, csr, gm, gn)) =
+        *reinterpret_cast<float4*>(C + (out_map ? (int64_t)out_map[gm] : gm) * ldc + gn) =
             make_float4(s * acc[i][j], s * acc[i][j + 1], s * acc[i][j + 2], s * acc[i][j + 3]);
     }
   }
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(ATB_THREADS)
     atb_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric, int tiles_a,
                int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld, const int* gate,
-               int64_t bsr) {
+               int /*unused*/) {
   if (gate && *((volatile const int*)gate) == 0) return;
   __shared__ __align__(16) S As[2][ATB_R][ATB_T];
   __shared__ __align__(16) S Bs[2][ATB_R][ATB_T];
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(ATB_THREADS)
       float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
       if (gr < r_end) {
         if (a0 + cc < Ka) va = __ldg(reinterpret_cast<const float4*>(A + gr * lda + a0 + cc));
-        if (b0 + cc < Kb) vb = __ldg(reinterpret_cast<const float4*>(B + mat_off(ldb, bsr, gr, b0 + cc)));
+        if (b0 + cc < Kb) vb = __ldg(reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc));
         if (row_scale) {
           float s = __ldg(row_scale + gr);
           vb.x *= s; vb.y *= s; vb.z *= s; vb.w *= s;
@@ -369,14 +369,15 @@ constexpr int64_t kColsumRows = 2048;
 // ------------------------------------------------------------------ misc
 __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, float* __restrict__ out, int64_t ldo,
                                   int64_t rows, int64_t w4, const float* __restrict__ vec, float coef,
-                                  const int* gate, int64_t isr, int64_t osr) {
+                                  const int* gate, const int32_t* __restrict__ in_map) {
   if (gate && *((volatile const int*)gate) == 0) return;
   int64_t tot = rows * w4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / w4, c = (t - i * w4) * 4;
     float s = coef * (vec ? vec[i] : 1.f);
-    float4 v = *reinterpret_cast<const float4*>(in + mat_off(ldi, isr, i, c));
-    *reinterpret_cast<float4*>(out + mat_off(ldo, osr, i, c)) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
+    const int64_t src = in_map ? (int64_t)in_map[i] : i;
+    float4 v = *reinterpret_cast<const float4*>(in + src * ldi + c);
+    *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
   }
 }
 
@@ -411,16 +412,16 @@ int grid_for(int64_t work, int threads, int cap) {
 
 cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M,
                            int64_t N, int64_t K, const float* row_scale, float alpha, bool upper_tri_b,
-                           const int* gate, cudaStream_t st, int64_t csr) {
+                           const int* gate, cudaStream_t st, const int32_t* out_map) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (N > 64) {
     dim3 grid((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                           upper_tri_b ? 1 : 0, gate, csr);
+                                                           upper_tri_b ? 1 : 0, gate, out_map);
   } else {
     dim3 grid((unsigned)ceil_div(N, 64), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 64, 8, 8, 4><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                          upper_tri_b ? 1 : 0, gate, csr);
+                                                          upper_tri_b ? 1 : 0, gate, out_map);
   }
   return cudaGetLastError();
 }
@@ -449,7 +450,7 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
 
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
                        const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg, float* out32,
-                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st, int64_t bsr,
+                       int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
                        bool f32_stage) {
   if (Ka <= 0 || Kb <= 0) return cudaSuccess;
   int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
@@ -463,10 +464,10 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     ++g_launches;
     if (f32_stage)
       atb_kernel<float><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
-                                                      (int)ta, (int)tb, rpc, ws, ws_ld, gate, bsr);
+                                                      (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
     else
       atb_kernel<double><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
-                                                       (int)ta, (int)tb, rpc, ws, ws_ld, gate, bsr);
+                                                       (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
   } else {
     cudaMemsetAsync(ws, 0, sizeof(double) * ka_pad * ws_ld, st);
     ch = 1;
@@ -492,10 +493,11 @@ cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ld
 
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
                               const float* vec, float coef, const int* gate, cudaStream_t st,
-                              int64_t isr, int64_t osr) {
+                              const int32_t* in_map) {
   if (rows <= 0) return cudaSuccess;
-  ++g_launches; scale_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4, vec,
-                                                                               coef, gate, isr, osr);
+  ++g_launches;
+  scale_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4,
+                                                                               vec, coef, gate, in_map);
   return cudaGetLastError();
 }
 

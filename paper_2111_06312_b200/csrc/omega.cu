@@ -34,25 +34,35 @@ ISVD_DEVICE U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Box-Muller output t of Philox block b (the pair (u0,u1) feeds words 0,1; (u2,u3) words 2,3).
+ISVD_DEVICE void gauss4(int64_t b, uint32_t k0, uint32_t k1, double z[4]) {
+  const double two_pi = 6.283185307179586;  // nearest double to 2 pi
+  const double two_m32 = 2.3283064365386963e-10;  // 2^-32
+  U4 c{(uint32_t)(b & 0xFFFFFFFFu), (uint32_t)((uint64_t)b >> 32), 0x4F4D4547u, 0u};
+  U4 x = philox4x32_10(c, k0, k1);
+  double u0 = ((double)x.x + 0.5) * two_m32;
+  double u1 = ((double)x.y + 0.5) * two_m32;
+  double u2 = ((double)x.z + 0.5) * two_m32;
+  double u3 = ((double)x.w + 0.5) * two_m32;
+  double r01 = sqrt(-2.0 * log(u0));
+  double r23 = sqrt(-2.0 * log(u2));
+  double t1 = two_pi * u1, t3 = two_pi * u3;
+  z[0] = r01 * cos(t1);
+  z[1] = r01 * sin(t1);
+  z[2] = r23 * cos(t3);
+  z[3] = r23 * sin(t3);
+}
+
+// Contiguous global rows [row0, row0 + rows): one thread per Philox block.
 __global__ void omega_kernel(uint32_t k0, uint32_t k1, int64_t row0, int64_t rows, int l, int64_t ld,
                              float* __restrict__ out) {
   const int64_t e0 = row0 * (int64_t)l;
   const int64_t e1 = (row0 + rows) * (int64_t)l;
   const int64_t b0 = e0 >> 2, b1 = (e1 + 3) >> 2;
-  const double two_pi = 6.283185307179586;  // nearest double to 2 pi
-  const double two_m32 = 2.3283064365386963e-10;  // 2^-32
   for (int64_t b = b0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < b1;
        b += (int64_t)gridDim.x * blockDim.x) {
-    U4 c{(uint32_t)(b & 0xFFFFFFFFu), (uint32_t)((uint64_t)b >> 32), 0x4F4D4547u, 0u};
-    U4 x = philox4x32_10(c, k0, k1);
-    double u0 = ((double)x.x + 0.5) * two_m32;
-    double u1 = ((double)x.y + 0.5) * two_m32;
-    double u2 = ((double)x.z + 0.5) * two_m32;
-    double u3 = ((double)x.w + 0.5) * two_m32;
-    double r01 = sqrt(-2.0 * log(u0));
-    double r23 = sqrt(-2.0 * log(u2));
-    double t1 = two_pi * u1, t3 = two_pi * u3;
-    double z[4] = {r01 * cos(t1), r01 * sin(t1), r23 * cos(t3), r23 * sin(t3)};
+    double z[4];
+    gauss4(b, k0, k1, z);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       int64_t e = 4 * b + t;
@@ -61,6 +71,18 @@ __global__ void omega_kernel(uint32_t k0, uint32_t k1, int64_t row0, int64_t row
       int64_t j = e - (e / l) * l;
       out[i * ld + j] = (float)z[t];
     }
+  }
+}
+
+// Relabelled rows: internal row i is global row row_map[i]; one thread per element.
+__global__ void omega_mapped_kernel(uint32_t k0, uint32_t k1, const int32_t* __restrict__ row_map, int64_t rows,
+                                    int l, int64_t ld, float* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * l; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / l, j = t - i * l;
+    int64_t e = (int64_t)row_map[i] * l + j;
+    double z[4];
+    gauss4(e >> 2, k0, k1, z);
+    out[i * ld + j] = (float)z[e & 3];
   }
 }
 
@@ -74,14 +96,23 @@ __global__ void zero_pad_kernel(float* out, int64_t rows, int l, int64_t ld) {
 
 }  // namespace
 
-cudaError_t launch_omega(uint64_t seed, int64_t row0, int64_t rows, int l, int64_t ld, float* out, cudaStream_t st) {
+cudaError_t launch_omega(uint64_t seed, int64_t row0, int64_t rows, int l, int64_t ld, float* out,
+                         const int32_t* row_map, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
-  int64_t nb = ((row0 + rows) * l + 3) / 4 - (row0 * l) / 4;
-  int threads = 256;
-  int64_t blocks = (nb + threads - 1) / threads;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  ++g_launches; omega_kernel<<<(int)blocks, threads, 0, st>>>((uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32), row0, rows,
-                                                l, ld, out);
+  const uint32_t k0 = (uint32_t)(seed & 0xFFFFFFFFu), k1 = (uint32_t)(seed >> 32);
+  const int threads = 256;
+  if (row_map) {
+    int64_t blocks = (rows * l + threads - 1) / threads;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
+    omega_mapped_kernel<<<(int)blocks, threads, 0, st>>>(k0, k1, row_map, rows, l, ld, out);
+  } else {
+    int64_t nb = ((row0 + rows) * l + 3) / 4 - (row0 * l) / 4;
+    int64_t blocks = (nb + threads - 1) / threads;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
+    omega_kernel<<<(int)blocks, threads, 0, st>>>(k0, k1, row0, rows, l, ld, out);
+  }
   if (ld > l) {
     int64_t tot = rows * (ld - l);
     int64_t zb = (tot + 255) / 256;
