@@ -16,6 +16,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/isvd.h"
@@ -629,11 +630,21 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       std::vector<int64_t> rp2(n_local + 1);
       std::vector<int32_t> ci2(nnz);
       rp2[0] = 0;
-      for (int64_t t = 0; t < n_local; ++t) {
-        const int64_t o = order[t], b = rp[o], d = rp[o + 1] - rp[o];
-        for (int64_t e = 0; e < d; ++e) ci2[rp2[t] + e] = new_of_old[ci[b + e]];
-        rp2[t + 1] = rp2[t] + d;
-      }
+      for (int64_t t = 0; t < n_local; ++t) rp2[t + 1] = rp2[t] + (rp[order[t] + 1] - rp[order[t]]);
+      // remap and sort each row's neighbours by internal id (hub rows first within every
+      // segment: neighbouring gathers of a team land close together), in parallel over rows
+      const int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+      std::vector<std::thread> pool;
+      for (int w = 0; w < nth; ++w)
+        pool.emplace_back([&, w] {
+          for (int64_t t = w; t < n_local; t += nth) {
+            const int64_t o = order[t], b = rp[o], d = rp[o + 1] - rp[o];
+            int32_t* dst = ci2.data() + rp2[t];
+            for (int64_t e = 0; e < d; ++e) dst[e] = new_of_old[ci[b + e]];
+            std::sort(dst, dst + d);
+          }
+        });
+      for (auto& th : pool) th.join();
       rp.swap(rp2);
       ci.swap(ci2);
       g->new2old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, g->allocs);

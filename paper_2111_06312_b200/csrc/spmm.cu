@@ -133,7 +133,7 @@ void set_window(cudaStream_t st, const void* base, size_t bytes) {
   v.accessPolicyWindow.num_bytes = bytes;
   v.accessPolicyWindow.hitRatio = bytes ? 1.0f : 0.0f;
   v.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
-  v.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+  v.accessPolicyWindow.missProp = bytes ? cudaAccessPropertyStreaming : cudaAccessPropertyNormal;
   cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
 }
 
