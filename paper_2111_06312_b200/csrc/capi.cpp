@@ -246,6 +246,8 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
   // relabelled graphs: the leading (hub) rows of the gather source stay L2-persisting
   size_t persist = 0;
   if (g->new2old) persist = std::min(ctx->max_persist_l2, (size_t)(g->n_pad * ctx->world) * a.wpad * sizeof(float));
+  static const char* persist_env = getenv("ISVD_L2_PERSIST_MB");  // tuning override (MB; 0 = off)
+  if (persist_env && g->new2old) persist = std::min(persist, (size_t)atoll(persist_env) << 20);
   CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist));
   if (e1) CK(cudaEventRecord(e1, ctx->stream));
   // algorithmic bytes of the step: CSR, scale vectors, the gather source read
