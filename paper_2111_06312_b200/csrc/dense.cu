@@ -426,6 +426,157 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------ A^T B, fp32 chunks (f32_stage)
+// Register-tiled SIMT contraction over a chunk of <= kF32ChunkRows rows, fp32 FMA
+// accumulation inside the chunk (relative error ~ sqrt(chunk) u_fp32 ~ 2e-6), fp32
+// partial tiles reduced in fp64 across chunks in a fixed order.  Thread (tx, ty) owns
+// rows ty*4 + 0..3 and columns {tx*4 + 0..3, BN/2 + tx*4 + 0..3} of a BM x BN tile, so
+// every shared-memory float4 read of a quarter-warp is conflict-free.  Tile shapes are
+// picked per call to avoid padding (d = 100, l = 400: 100 x 80 tiles, no waste).
+constexpr int kF32ChunkRows = 1024;
+constexpr int kF32Stage = 16;
+
+template <int BM, int BN>
+__global__ void __launch_bounds__((BM / 4) * (BN / 8))
+    atb_f32_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
+                   int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int tiles_b, int64_t rows_per_chunk,
+                   float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  constexpr int TY = BM / 4, TX = BN / 8, NT = TX * TY;
+  constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
+  __shared__ __align__(16) float As[2][kF32Stage][BM];
+  __shared__ __align__(16) float Bs[2][kF32Stage][BN];
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int ti = blockIdx.x / tiles_b, tj = blockIdx.x - ti * tiles_b;
+  const int64_t a0 = (int64_t)ti * BM, b0 = (int64_t)tj * BN;
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t r_end = r_begin + rows_per_chunk < rows ? r_begin + rows_per_chunk : rows;
+  float4 pa[(A4 + NT - 1) / NT], pb[(B4 + NT - 1) / NT];
+  auto load = [&](int64_t r0) {
+#pragma unroll
+    for (int u = 0; u < (A4 + NT - 1) / NT; ++u) {
+      int f = tid + u * NT;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < A4) {
+        int rr = f / (BM / 4), cc = (f % (BM / 4)) * 4;
+        int64_t gr = r0 + rr;
+        if (gr < r_end && a0 + cc < Ka) v = __ldg(reinterpret_cast<const float4*>(A + gr * lda + a0 + cc));
+      }
+      pa[u] = v;
+    }
+#pragma unroll
+    for (int u = 0; u < (B4 + NT - 1) / NT; ++u) {
+      int f = tid + u * NT;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < B4) {
+        int rr = f / (BN / 4), cc = (f % (BN / 4)) * 4;
+        int64_t gr = r0 + rr;
+        if (gr < r_end && b0 + cc < Kb) {
+          v = __ldg(reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc));
+          if (row_scale) {
+            float s = __ldg(row_scale + gr);
+            v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+          }
+        }
+      }
+      pb[u] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < (A4 + NT - 1) / NT; ++u) {
+      int f = tid + u * NT;
+      if (f < A4) *reinterpret_cast<float4*>(&As[buf][f / (BM / 4)][(f % (BM / 4)) * 4]) = pa[u];
+    }
+#pragma unroll
+    for (int u = 0; u < (B4 + NT - 1) / NT; ++u) {
+      int f = tid + u * NT;
+      if (f < B4) *reinterpret_cast<float4*>(&Bs[buf][f / (BN / 4)][(f % (BN / 4)) * 4]) = pb[u];
+    }
+  };
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
+  if (nst > 0) {
+    load(r_begin);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t s = 0; s < nst; ++s) {
+    const int buf = (int)(s & 1);
+    if (s + 1 < nst) load(r_begin + (s + 1) * kF32Stage);
+#pragma unroll
+    for (int kk = 0; kk < kF32Stage; ++kk) {
+      const float4 va = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 v0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 v1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][BN / 2 + tx * 4]);
+      const float a[4] = {va.x, va.y, va.z, va.w};
+      const float b[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (s + 1 < nst) store(buf ^ 1);
+    __syncthreads();
+  }
+  float* W = ws + (int64_t)blockIdx.y * ws_lda * ws_ld;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float* w = W + (a0 + ty * 4 + i) * ws_ld + b0;
+    *reinterpret_cast<float4*>(w + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    *reinterpret_cast<float4*>(w + BN / 2 + tx * 4) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+  }
+}
+
+__global__ void atb_f32_reduce_kernel(const float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, int nchunks,
+                                      int64_t Ka, int64_t Kb, int symmetric, double* __restrict__ G, int64_t ldg,
+                                      float* __restrict__ out32, int64_t ld32, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  int64_t tot = Ka * Kb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / Kb, j = t - (t / Kb) * Kb;
+    int64_t si = i, sj = j;
+    if (symmetric && i > j) { si = j; sj = i; }
+    double s = 0.0;
+    for (int c = 0; c < nchunks; ++c) s += (double)ws[((int64_t)c * ws_lda + si) * ws_ld + sj];
+    if (G) G[i * ldg + j] = s;
+    if (out32) out32[i * ld32 + j] = (float)s;
+  }
+}
+
+struct F32Tiling {
+  int bm, bn;
+  int64_t ta, tb, chunk_rows, chunks;
+};
+
+F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
+  const int cand[3][2] = {{64, 64}, {100, 80}, {128, 128}};
+  F32Tiling t{64, 64, 0, 0, 0, 0};
+  int64_t best = -1;
+  for (auto& c : cand) {
+    int64_t area = round_up(Ka, c[0]) * round_up(Kb, c[1]);
+    if (best < 0 || area < best || (area == best && c[0] * c[1] > t.bm * t.bn)) {
+      best = area;
+      t.bm = c[0];
+      t.bn = c[1];
+    }
+  }
+  t.ta = ceil_div(Ka, t.bm);
+  t.tb = ceil_div(Kb, t.bn);
+  // enough CTAs to fill the GPU several times over, chunks of 64 .. kF32ChunkRows rows
+  int64_t want = ceil_div(4LL * num_sms, t.ta * t.tb);
+  int64_t cr = round_up(ceil_div(rows > 0 ? rows : 1, want), kF32Stage);
+  if (cr > kF32ChunkRows) cr = kF32ChunkRows;
+  if (cr < 64) cr = 64;
+  t.chunk_rows = cr;
+  t.chunks = rows > 0 ? ceil_div(rows, cr) : 1;
+  return t;
+}
+
 static int64_t atb_chunks(int64_t rows, int64_t ntiles, int num_sms) {
   int64_t target = 8LL * num_sms;  // 64-thread CTAs, several resident per SM
   int64_t ch = ceil_div(target, ntiles);
@@ -445,7 +596,10 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   int64_t ch = atb_chunks(rows, atb_ntiles(Ka, Kb, Ka == Kb), num_sms);
   int64_t ch2 = atb_chunks(rows, atb_ntiles(Ka, Kb, false), num_sms);
   if (ch2 > ch) ch = ch2;
-  return ch * round_up(Ka, ATB_T) * round_up(Kb, ATB_T);
+  const int64_t f64_path = ch * round_up(Ka, ATB_T) * round_up(Kb, ATB_T);
+  F32Tiling t = f32_tiling(rows, Ka, Kb, num_sms);
+  const int64_t f32_path = (t.chunks * t.ta * t.bm * t.tb * t.bn + 1) / 2;  // floats -> doubles
+  return f64_path > f32_path ? f64_path : f32_path;
 }
 
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
@@ -453,6 +607,30 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
                        int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
                        bool f32_stage) {
   if (Ka <= 0 || Kb <= 0) return cudaSuccess;
+  if (f32_stage) {
+    F32Tiling t = f32_tiling(rows, Ka, Kb, num_sms);
+    float* ws32 = reinterpret_cast<float*>(ws);
+    const int64_t ws_lda = t.ta * t.bm, ws_ld = t.tb * t.bn;
+    if (rows > 0) {
+      dim3 grid((unsigned)(t.ta * t.tb), (unsigned)t.chunks);
+      ++g_launches;
+      if (t.bm == 64)
+        atb_f32_kernel<64, 64><<<grid, 128, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows,
+                                                     ws32, ws_lda, ws_ld, gate);
+      else if (t.bm == 100)
+        atb_f32_kernel<100, 80><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
+                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+      else
+        atb_f32_kernel<128, 128><<<grid, 512, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
+                                                       t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+    } else {
+      cudaMemsetAsync(ws32, 0, sizeof(float) * ws_lda * ws_ld, st);
+    }
+    ++g_launches;
+    atb_f32_reduce_kernel<<<grid_for(Ka * Kb, 256, num_sms * 8), 256, 0, st>>>(
+        ws32, ws_lda, ws_ld, rows > 0 ? (int)t.chunks : 1, Ka, Kb, symmetric ? 1 : 0, G, ldg, out32, ld32, gate);
+    return cudaGetLastError();
+  }
   int64_t ta = ceil_div(Ka, ATB_T), tb = ceil_div(Kb, ATB_T);
   int64_t ntiles = atb_ntiles(Ka, Kb, symmetric);
   int64_t ch = atb_chunks(rows, ntiles, num_sms);
