@@ -972,13 +972,16 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
 
 // CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
 // If Rout != null it receives R = R_3 R_2 R_1 (so that Y_in = Y_out R).
-void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64_t l, bool force_fail, double* Rout) {
+// exact_gram: pass 1 takes the fp64 Gram (input possibly ill-conditioned: Y = M Omega);
+// otherwise pass 1 uses the fp32-chunk Gram too (Y = M Q with Q orthonormal, cond(Y) <= cond(M)).
+void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64_t l, bool force_fail, double* Rout,
+          bool exact_gram) {
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
   int* gate = &ctx->status->need_extra_pass;
   CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, false, force_fail, nullptr);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, !exact_gram, force_fail, nullptr);
   cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, true, false, nullptr);
   cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, false, false, gate);
   CK(launch_scale_rows(Y2, ld, Y, ld, rows, ld, nullptr, 1.f, gate, ctx->stream));  // copy back iff pass 3 ran
@@ -1035,16 +1038,16 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   // Alg. 1 lines 5-8
   for (int it = 0; it < p->power_iters; ++it) {
     op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);                // M Q       (r x l)
-    cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);          // orthonorm
+    cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr, it == 0);  // orthonorm
     op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);              // M^T Q     (c x l)
-    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr);            // orthonorm
+    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr, true);      // orthonorm
   }
   // Alg. 1 line 9: Q <- orthonorm(M Q)
   op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);
-  cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr);
+  cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr, p->power_iters == 0);
   // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
   op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);
-  cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin);
+  cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin, true);
   // Alg. 1 line 11: svd(B) with B = R^T Q_W^T -> one-sided Jacobi on R^T
   CK(launch_jacobi_svd(s.Rfin, (int)l, (int)k, ldk, s.sigma, s.Ub, s.Vb, s.jac_ws, ctx->status, ctx->num_sms,
                        ctx->stream));
