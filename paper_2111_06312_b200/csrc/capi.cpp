@@ -662,7 +662,8 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     }
     g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
     CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
-    g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), g->allocs);
+    // + kIdxPad zero entries: the gather prefetches indices one batch past a segment's end
+    g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nnz + kIdxPad), g->allocs);
     if (nnz > 0) CK(cudaMemcpy(g->col_idx, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
     // degrees (integers) -> scale vectors computed once in fp64, stored fp32 (reading O3)
     std::vector<float> inv(n_local), s(n_local), s2(n_local), rs(n_local);

@@ -80,6 +80,7 @@ struct SpmmPlan {
   int32_t* split_nslot = nullptr; // [n_split_rows] number of slots
 };
 constexpr int kSegEdges = 512;
+constexpr int kIdxPad = 16;  // readable zero entries after col_idx[nnz - 1] (index prefetch)
 
 struct SpmmArgs {
   const int32_t* col_idx;
