@@ -16,7 +16,6 @@
 #include <cstring>
 #include <new>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "../../include/isvd.h"
@@ -65,7 +64,6 @@ struct isvd_graph_s {
   float* s2 = nullptr;         // (d+1)^-1
   float* rs = nullptr;         // (d+1)^1/2
   int32_t* new2old = nullptr;  // relabelled graphs: caller row of internal row i (device); else null
-  std::vector<int32_t> h_new2old;
   SpmmPlan plan;
   std::vector<void*> allocs;
   std::atomic<int> refs{0};
@@ -610,48 +608,52 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->n_local = n_local;
     g->n_pad = (n_global + ctx->world - 1) / ctx->world;
     g->nnz = nnz;
-    std::vector<int32_t> ci(nnz);
-    if (nnz > 0) {
-      if (dev) CK(cudaMemcpy(ci.data(), col_idx + base, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
-      else memcpy(ci.data(), col_idx + base, sizeof(int32_t) * nnz);
-    }
-    if (flags & ISVD_GRAPH_VALIDATE)
+    // CSR on the device (copied: the caller may free its arrays on return), with kIdxPad
+    // readable zero entries after the last index (the gather prefetches one batch ahead)
+    const bool relabel = ctx->world == 1 && n_local >= kRelabelMinRows;
+    std::vector<void*> tmp;
+    struct TmpFree {
+      std::vector<void*>& v;
+      ~TmpFree() { for (void* q : v) cudaFree(q); }
+    } tmp_free{tmp};
+    g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
+    g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nnz + kIdxPad), g->allocs);
+    int32_t* ci_in = relabel ? (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), tmp) : g->col_idx;
+    if (nnz > 0)
+      CK(cudaMemcpy(ci_in, col_idx + base, sizeof(int32_t) * nnz,
+                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    if (flags & ISVD_GRAPH_VALIDATE) {
+      std::vector<int32_t> ci(nnz);
+      if (nnz) CK(cudaMemcpy(ci.data(), ci_in, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
       for (int64_t e = 0; e < nnz; ++e)
         REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
+    }
     // Degree relabelling (single rank, large graphs; SURVEY 8(d2) "allowed optimisation"):
     // internal row t is caller row order[t], in decreasing degree, so the hub rows that take
     // most gathers form one contiguous prefix of every iterate, which the SpMM marks
     // L2-persisting.  A symmetric permutation of A: singular values are unchanged and every
     // caller-ordered input/output is mapped at the boundary (X, Omega, U, V, matmul I/O).
-    if (ctx->world == 1 && n_local >= kRelabelMinRows) {
+    // The order is computed on the host from the degrees; the index renaming runs on the GPU.
+    if (relabel) {
       std::vector<int32_t> order(n_local), new_of_old(n_local);
       for (int64_t i = 0; i < n_local; ++i) order[i] = (int32_t)i;
       std::stable_sort(order.begin(), order.end(),
                        [&](int32_t a, int32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
       for (int64_t t = 0; t < n_local; ++t) new_of_old[order[t]] = (int32_t)t;
       std::vector<int64_t> rp2(n_local + 1);
-      std::vector<int32_t> ci2(nnz);
       rp2[0] = 0;
       for (int64_t t = 0; t < n_local; ++t) rp2[t + 1] = rp2[t] + (rp[order[t] + 1] - rp[order[t]]);
-      // remap and sort each row's neighbours by internal id (hub rows first within every
-      // segment: neighbouring gathers of a team land close together), in parallel over rows
-      const int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-      std::vector<std::thread> pool;
-      for (int w = 0; w < nth; ++w)
-        pool.emplace_back([&, w] {
-          for (int64_t t = w; t < n_local; t += nth) {
-            const int64_t o = order[t], b = rp[o], d = rp[o + 1] - rp[o];
-            int32_t* dst = ci2.data() + rp2[t];
-            for (int64_t e = 0; e < d; ++e) dst[e] = new_of_old[ci[b + e]];
-            std::sort(dst, dst + d);
-          }
-        });
-      for (auto& th : pool) th.join();
-      rp.swap(rp2);
-      ci.swap(ci2);
+      int64_t* d_rp_old = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+      int32_t* d_new_of_old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, tmp);
       g->new2old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, g->allocs);
+      CK(cudaMemcpy(d_rp_old, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_new_of_old, new_of_old.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(g->new2old, order.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice));
-      g->h_new2old.swap(order);
+      CK(cudaMemcpy(g->row_ptr, rp2.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
+      CK(launch_relabel_csr(d_rp_old, ci_in, g->new2old, d_new_of_old, g->row_ptr, g->col_idx, n_local,
+                            ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      rp.swap(rp2);
       if (ctx->max_persist_l2 > 0) {
         static bool limit_set = false;  // process-wide L2 set-aside for persisting accesses
         if (!limit_set) {
@@ -659,12 +661,9 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
           limit_set = true;
         }
       }
+    } else {
+      CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
     }
-    g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
-    CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
-    // + kIdxPad zero entries: the gather prefetches indices one batch past a segment's end
-    g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nnz + kIdxPad), g->allocs);
-    if (nnz > 0) CK(cudaMemcpy(g->col_idx, ci.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
     // degrees (integers) -> scale vectors computed once in fp64, stored fp32 (reading O3)
     std::vector<float> inv(n_local), s(n_local), s2(n_local), rs(n_local);
     int64_t maxd = 0;
@@ -809,17 +808,20 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
           if (!g->new2old) {
             CK(cudaMemcpy(x, desc->X, row_bytes * (size_t)g->n_local,
                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-          } else if (dev) {
-            REQ(aligned16(desc->X), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
-            CK(launch_scale_rows(desc->X, desc->ldx, x, desc->ldx, g->n_local, desc->ldx, nullptr, 1.f, nullptr,
+          } else {
+            // caller-ordered X on the device (uploaded if needed), rows gathered to the internal order
+            const float* src = desc->X;
+            std::vector<void*> stage;
+            if (!dev) {
+              float* d = (float*)dmalloc(ctx, row_bytes * (size_t)g->n_local, stage);
+              CK(cudaMemcpy(d, desc->X, row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
+              src = d;
+            }
+            REQ(aligned16(src), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
+            CK(launch_scale_rows(src, desc->ldx, x, desc->ldx, g->n_local, desc->ldx, nullptr, 1.f, nullptr,
                                  ctx->stream, g->new2old));
             CK(cudaStreamSynchronize(ctx->stream));
-          } else {
-            std::vector<float> h((size_t)g->n_local * desc->ldx);
-            const float* src = desc->X;
-            for (int64_t i = 0; i < g->n_local; ++i)
-              memcpy(h.data() + (size_t)i * desc->ldx, src + (size_t)g->h_new2old[i] * desc->ldx, row_bytes);
-            CK(cudaMemcpy(x, h.data(), row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
+            for (void* q : stage) cudaFree(q);
           }
         }
         op->X = x;

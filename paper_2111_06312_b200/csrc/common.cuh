@@ -95,6 +95,10 @@ struct SpmmArgs {
   int64_t wpad;            // columns processed (multiple of 4)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
+// Graph relabelling on the device: new row t = old row order[t], neighbour ids renamed by new_of_old.
+cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const int32_t* order,
+                               const int32_t* new_of_old, const int64_t* rp_new, int32_t* ci_new, int64_t n,
+                               cudaStream_t st);
 // `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled
 // graph) are marked L2-persisting for this launch (cudaAccessPolicyWindow on `st`).
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,

@@ -158,6 +158,32 @@ void set_window(cudaStream_t st, const void* base, size_t bytes) {
 
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad) { return plan.n_slots * wpad; }
 
+namespace {
+// One warp per new row t: copy old row order[t]'s neighbours, renamed through new_of_old.
+__global__ void relabel_csr_kernel(const int64_t* __restrict__ rp_old, const int32_t* __restrict__ ci_old,
+                                   const int32_t* __restrict__ order, const int32_t* __restrict__ new_of_old,
+                                   const int64_t* __restrict__ rp_new, int32_t* __restrict__ ci_new, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t o = order[t];
+    const int64_t b = rp_old[o], d = rp_old[o + 1] - b, dst = rp_new[t];
+    for (int64_t e = lane; e < d; e += 32) ci_new[dst + e] = new_of_old[ci_old[b + e]];
+  }
+}
+}  // namespace
+
+cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const int32_t* order,
+                               const int32_t* new_of_old, const int64_t* rp_new, int32_t* ci_new, int64_t n,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = ceil_div(n * 32, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  ++g_launches;
+  relabel_csr_kernel<<<(int)blocks, 256, 0, st>>>(rp_old, ci_old, order, new_of_old, rp_new, ci_new, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_partial, int num_sms, cudaStream_t st,
                         size_t persist_bytes) {
   if (plan.n_local == 0) return cudaSuccess;
