@@ -338,6 +338,8 @@ def main():
             "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,
+            "solver": {"jacobi_sweeps": results[-1].jacobi_sweeps, "chol_fallbacks": results[-1].chol_fallbacks,
+                       "launches_per_isvd": results[-1].kernel_launches},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

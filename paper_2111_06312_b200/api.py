@@ -215,8 +215,9 @@ class _Operator:
         flags = 0
         if host_output:
             flags |= _lib.ISVD_SVD_HOST_OUTPUT
-            U = np.zeros((max(self.graph.n_local, 1), kk), dtype=np.float32)
-            V = np.zeros((max(self.c_rows(), 1), kk), dtype=np.float32)
+            # page-locked host buffers: the library's device-to-host copies run at full DMA speed
+            U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, pin_memory=True).numpy()
+            V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, pin_memory=True).numpy()
             pu, pv, ldu, ldv = U.ctypes.data, V.ctypes.data, kk, kk
         else:
             if out is not None:

@@ -364,7 +364,11 @@ __global__ void colsum_final_kernel(const double* __restrict__ ws, int nblocks, 
   }
 }
 
-constexpr int64_t kColsumRows = 2048;
+// rows per colsum block: >= 64, and at most ~8 blocks per SM worth of blocks
+int64_t colsum_rows_per_block(int64_t rows) {
+  int64_t r = round_up(ceil_div(rows > 0 ? rows : 1, 148 * 8), 64);
+  return r < 64 ? 64 : r;
+}
 
 // ------------------------------------------------------------------ misc
 __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, float* __restrict__ out, int64_t ldo,
@@ -660,16 +664,19 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
   return cudaGetLastError();
 }
 
-int64_t colsum_ws_doubles(int64_t rows, int64_t wpad) { return (ceil_div(rows, kColsumRows) + 1) * wpad; }
+int64_t colsum_ws_doubles(int64_t rows, int64_t wpad) {
+  return (ceil_div(rows, colsum_rows_per_block(rows)) + 1) * wpad;
+}
 
 cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ldq, double* ws, double* out,
                           cudaStream_t st) {
-  int64_t nb = ceil_div(rows, kColsumRows);
+  const int64_t rpb = colsum_rows_per_block(rows);
+  int64_t nb = ceil_div(rows, rpb);
   if (nb < 1) {
     cudaMemsetAsync(out, 0, sizeof(double) * wpad, st);
     return cudaGetLastError();
   }
-  ++g_launches; colsum_partial_kernel<<<(unsigned)nb, dim3(32, 8), 0, st>>>(Q, rows, wpad, ldq, kColsumRows, ws);
+  ++g_launches; colsum_partial_kernel<<<(unsigned)nb, dim3(32, 8), 0, st>>>(Q, rows, wpad, ldq, rpb, ws);
   ++g_launches; colsum_final_kernel<<<grid_for(wpad, 128, 64), 128, 0, st>>>(ws, (int)nb, wpad, out);
   return cudaGetLastError();
 }

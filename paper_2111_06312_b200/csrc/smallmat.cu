@@ -13,6 +13,8 @@
 //  K17 sort/sign    descending order (reading O9) and the sign rule.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -173,11 +175,17 @@ ISVD_DEVICE void jsync() {
 }
 
 // A: l x l, column j of R^T (= row j of R) contiguous at A + j*l; J: accumulated rotations.
+// Column norms are carried across rotations (Rutishauser: ||a_i'||^2 = ||a_i||^2 - t g,
+// ||a_j'||^2 = ||a_j||^2 + t g) and recomputed exactly at every sweep, so a pair costs one
+// dot-product reduction instead of three.
 template <bool kOneBlock>
 __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ R, int l, double* Ag, double* Jg,
                                                       int* counters, DevStatus* status, int max_sweeps,
-                                                      double* __restrict__ Aout, double* __restrict__ Jout) {
+                                                      double* __restrict__ Aout, double* __restrict__ Jout,
+                                                      double* nrm_g) {
   extern __shared__ double smem[];
+  __shared__ double nrm_s[kOneBlock ? 1024 : 1];
+  double* nrm = kOneBlock ? nrm_s : nrm_g;
   const bool in_smem = kOneBlock && (2 * l * l * (int)sizeof(double) <= 200 * 1024);
   double* A = in_smem ? smem : Ag;
   double* J = in_smem ? smem + (int64_t)l * l : Jg;
@@ -197,6 +205,14 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
   int sweep = 0;
   for (sweep = 0; sweep < max_sweeps; ++sweep) {
     int* cnt = counters + (sweep & 1);
+    for (int64_t c = gwarp; c < l; c += nwarps) {
+      const double* ac = A + c * l;
+      double q = 0.0;
+      for (int r = lane; r < l; r += 32) q += ac[r] * ac[r];
+      q = warp_sum(q);
+      if (lane == 0) nrm[c] = q;
+    }
+    jsync<kOneBlock>();
     for (int round = 0; round < m - 1; ++round) {
       for (int64_t p = gwarp; p < m / 2; p += nwarps) {
         int i = rr_index((int)p, round, m), j = rr_index(m - 1 - (int)p, round, m);
@@ -204,12 +220,10 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
         if (i > j) { int t = i; i = j; j = t; }
         double* ai = A + (int64_t)i * l;
         double* aj = A + (int64_t)j * l;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int r = lane; r < l; r += 32) {
-          double x = ai[r], y = aj[r];
-          al += x * x; be += y * y; ga += x * y;
-        }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+        double ga = 0.0;
+        for (int r = lane; r < l; r += 32) ga += ai[r] * aj[r];
+        ga = warp_sum(ga);
+        const double al = nrm[i], be = nrm[j];
         if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           double zeta = (be - al) / (2.0 * ga);
           double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
@@ -226,7 +240,11 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
             ji[r] = c * x - s * y;
             jj[r] = s * x + c * y;
           }
-          if (lane == 0) atomicAdd(cnt, 1);
+          if (lane == 0) {
+            atomicAdd(cnt, 1);
+            nrm[i] = al - t * ga;
+            nrm[j] = be + t * ga;
+          }
         }
         __syncwarp();
       }
@@ -572,8 +590,10 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
 
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64, double* ws,
                             DevStatus* status, bool force_fail, const int* gate, cudaStream_t st) {
-  if (l > kCholSmemMax && l <= 512) {
-    const int CS = l <= 400 ? 8 : 16;
+  // Blocked (panel) algorithm: one CTA for l <= kCholSmemMax (whole matrix in its shared
+  // memory), a cluster of 8 / 16 CTAs sharing it through DSMEM above that.
+  if (l <= 512 && !getenv("ISVD_CHOL_UNBLOCKED")) {
+    const int CS = l <= kCholSmemMax ? 1 : (l <= 400 ? 8 : 16);
     const int nblk = (l + kPanel - 1) / kPanel;
     const int rows_max = ((nblk + CS - 1) / CS) * kPanel;
     size_t smem = sizeof(double) * ((size_t)rows_max * l + (size_t)kPanel * l + (size_t)rows_max * kPanel);
@@ -624,6 +644,7 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
   double* Aout = ws + 2LL * l * l;  // smem path copies results here
   double* Jout = ws + 3LL * l * l;
   double* sig = ws + 4LL * l * l;
+  double* nrm = ws + 4LL * l * l + l;  // column norms of the cooperative variant
   int* counters = reinterpret_cast<int*>(ws + 4LL * l * l + 2LL * l);
   const int max_sweeps = 60;
   const bool one_block = l <= 128;
@@ -634,7 +655,8 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
       cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_set = true;
     }
-    ++g_launches; jacobi_kernel<true><<<1, 1024, smem, st>>>(R, l, A, J, counters, status, max_sweeps, Aout, Jout);
+    ++g_launches;
+    jacobi_kernel<true><<<1, 1024, smem, st>>>(R, l, A, J, counters, status, max_sweeps, Aout, Jout, nrm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (smem == 0) { Aout = A; Jout = J; }
@@ -645,7 +667,7 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
     int blocks = (warps_needed * 32 + threads - 1) / threads;
     if (blocks > num_sms) blocks = num_sms;
     void* args[] = {(void*)&R, (void*)&l, (void*)&A, (void*)&J, (void*)&counters, (void*)&status,
-                    (void*)&max_sweeps, (void*)&Aout, (void*)&Jout};
+                    (void*)&max_sweeps, (void*)&Aout, (void*)&Jout, (void*)&nrm};
     ++g_launches;
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel<false>, dim3(blocks), dim3(threads), args,
                                                 0, st);
