@@ -168,58 +168,84 @@ ISVD_DEVICE int rr_index(int pos, int round, int m) {
   return pos == 0 ? 0 : 1 + (pos - 1 + round) % (m - 1);
 }
 
-template <bool kOneBlock>
-ISVD_DEVICE void jsync() {
-  if (kOneBlock) __syncthreads();
-  else cg::this_grid().sync();
-}
-
-// A: l x l, column j of R^T (= row j of R) contiguous at A + j*l; J: accumulated rotations.
+// A: l x l, column j of R^T (= row j of R); J: accumulated rotations (column j = v_j).
+// kMode 0: one CTA (columns in its shared memory when they fit, else global memory);
+// kMode 1: cooperative grid, columns in (L2-resident) global memory, grid barrier per round;
+// kMode 2: thread-block cluster, column c in the shared memory of CTA c % CS (slot c / CS),
+//          read and rotated through DSMEM, one cluster barrier per round.
 // Column norms are carried across rotations (Rutishauser: ||a_i'||^2 = ||a_i||^2 - t g,
 // ||a_j'||^2 = ||a_j||^2 + t g) and recomputed exactly at every sweep, so a pair costs one
 // dot-product reduction instead of three.
-template <bool kOneBlock>
+template <int kMode>
 __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ R, int l, double* Ag, double* Jg,
                                                       int* counters, DevStatus* status, int max_sweeps,
                                                       double* __restrict__ Aout, double* __restrict__ Jout,
                                                       double* nrm_g) {
   extern __shared__ double smem[];
-  __shared__ double nrm_s[kOneBlock ? 1024 : 1];
-  double* nrm = kOneBlock ? nrm_s : nrm_g;
-  const bool in_smem = kOneBlock && (2 * l * l * (int)sizeof(double) <= 200 * 1024);
+  __shared__ double nrm_s[kMode == 0 ? 1024 : 1];
+  double* nrm = kMode == 0 ? nrm_s : nrm_g;
+  int CS = 1, crank = 0;
+  if constexpr (kMode == 2) {
+    CS = (int)cg::this_cluster().num_blocks();
+    crank = (int)cg::this_cluster().block_rank();
+  }
+  const int cols_per = (l + CS - 1) / CS;
+  const bool in_smem = (kMode == 0 && 2 * l * l * (int)sizeof(double) <= 200 * 1024) || kMode == 2;
   double* A = in_smem ? smem : Ag;
-  double* J = in_smem ? smem + (int64_t)l * l : Jg;
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  double* J = in_smem ? smem + (int64_t)(kMode == 2 ? cols_per : l) * l : Jg;
+  auto colA = [&](int c) -> double* {
+    if constexpr (kMode == 2) return cg::this_cluster().map_shared_rank(A, c % CS) + (int64_t)(c / CS) * l;
+    return A + (int64_t)c * l;
+  };
+  auto colJ = [&](int c) -> double* {
+    if constexpr (kMode == 2) return cg::this_cluster().map_shared_rank(J, c % CS) + (int64_t)(c / CS) * l;
+    return J + (int64_t)c * l;
+  };
+  auto jsync = [&]() {
+    if constexpr (kMode == 0) __syncthreads();
+    else if constexpr (kMode == 1) cg::this_grid().sync();
+    else cg::this_cluster().sync();
+  };
+  const int64_t gtid = (kMode == 1 ? (int64_t)blockIdx.x : (int64_t)crank) * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (kMode == 1 ? (int64_t)gridDim.x : (int64_t)CS) * blockDim.x;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = gtid >> 5, nwarps = gthreads >> 5;
-  for (int64_t t = gtid; t < (int64_t)l * l; t += gthreads) {
-    A[t] = R[t];
-    int64_t j = t / l, i = t - j * l;
-    J[t] = (i == j) ? 1.0 : 0.0;
+  if constexpr (kMode == 2) {  // own columns c = q*CS + crank
+    for (int64_t t = threadIdx.x; t < (int64_t)cols_per * l; t += blockDim.x) {
+      const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+      const int c = q * CS + crank;
+      A[t] = c < l ? R[(int64_t)c * l + r] : 0.0;
+      J[t] = (c < l && r == c) ? 1.0 : 0.0;
+    }
+  } else {
+    for (int64_t t = gtid; t < (int64_t)l * l; t += gthreads) {
+      A[t] = R[t];
+      int64_t j = t / l, i = t - j * l;
+      J[t] = (i == j) ? 1.0 : 0.0;
+    }
   }
   if (gtid == 0) { counters[0] = 0; counters[1] = 0; }
-  jsync<kOneBlock>();
+  jsync();
   const int m = (l & 1) ? l + 1 : l;
   const double tol = (double)l * 1.1102230246251565e-16;
   int sweep = 0;
   for (sweep = 0; sweep < max_sweeps; ++sweep) {
     int* cnt = counters + (sweep & 1);
     for (int64_t c = gwarp; c < l; c += nwarps) {
-      const double* ac = A + c * l;
+      const double* ac = colA((int)c);
       double q = 0.0;
       for (int r = lane; r < l; r += 32) q += ac[r] * ac[r];
       q = warp_sum(q);
       if (lane == 0) nrm[c] = q;
     }
-    jsync<kOneBlock>();
+    jsync();
     for (int round = 0; round < m - 1; ++round) {
       for (int64_t p = gwarp; p < m / 2; p += nwarps) {
         int i = rr_index((int)p, round, m), j = rr_index(m - 1 - (int)p, round, m);
         if (i >= l || j >= l) continue;
         if (i > j) { int t = i; i = j; j = t; }
-        double* ai = A + (int64_t)i * l;
-        double* aj = A + (int64_t)j * l;
+        double* ai = colA(i);
+        double* aj = colA(j);
         double ga = 0.0;
         for (int r = lane; r < l; r += 32) ga += ai[r] * aj[r];
         ga = warp_sum(ga);
@@ -233,8 +259,8 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
             ai[r] = c * x - s * y;
             aj[r] = s * x + c * y;
           }
-          double* ji = J + (int64_t)i * l;
-          double* jj = J + (int64_t)j * l;
+          double* ji = colJ(i);
+          double* jj = colJ(j);
           for (int r = lane; r < l; r += 32) {
             double x = ji[r], y = jj[r];
             ji[r] = c * x - s * y;
@@ -248,16 +274,26 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
         }
         __syncwarp();
       }
-      jsync<kOneBlock>();
+      jsync();
     }
     int rotations = *((volatile int*)cnt);
-    jsync<kOneBlock>();
+    jsync();
     if (gtid == 0) counters[(sweep + 1) & 1] = 0;
-    jsync<kOneBlock>();
+    jsync();
     if (rotations == 0) { ++sweep; break; }
   }
   if (gtid == 0) status->jacobi_sweeps = sweep;
-  if (in_smem) {
+  if constexpr (kMode == 2) {
+    for (int64_t t = threadIdx.x; t < (int64_t)cols_per * l; t += blockDim.x) {
+      const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+      const int c = q * CS + crank;
+      if (c < l) {
+        Aout[(int64_t)c * l + r] = A[t];
+        Jout[(int64_t)c * l + r] = J[t];
+      }
+    }
+    jsync();  // keep shared memory alive until every remote access is done
+  } else if (in_smem) {
     for (int64_t t = threadIdx.x; t < (int64_t)l * l; t += blockDim.x) {
       Aout[t] = A[t];
       Jout[t] = J[t];
@@ -647,29 +683,60 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
   double* nrm = ws + 4LL * l * l + l;  // column norms of the cooperative variant
   int* counters = reinterpret_cast<int*>(ws + 4LL * l * l + 2LL * l);
   const int max_sweeps = 60;
-  const bool one_block = l <= 128;
-  if (one_block) {
-    size_t smem = (2 * (size_t)l * l * sizeof(double) <= 200 * 1024) ? 2 * (size_t)l * l * sizeof(double) : 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr_set = true;
-    }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(jacobi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(jacobi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(jacobi_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  bool done = false;
+  if (l <= 112) {
+    size_t smem = 2 * (size_t)l * l * sizeof(double);
     ++g_launches;
-    jacobi_kernel<true><<<1, 1024, smem, st>>>(R, l, A, J, counters, status, max_sweeps, Aout, Jout, nrm);
+    jacobi_kernel<0><<<1, 1024, smem, st>>>(R, l, A, J, counters, status, max_sweeps, Aout, Jout, nrm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (smem == 0) { Aout = A; Jout = J; }
-  } else {
+    done = true;
+  } else if (l <= 448) {
+    // cluster: the smallest cluster (8, else 16 CTAs) whose shared memory holds A and J
+    for (int CS : {8, 16}) {
+      const int cols_per = (l + CS - 1) / CS;
+      const size_t smem = 2 * (size_t)cols_per * l * sizeof(double);
+      if (smem > 200 * 1024) continue;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      ++g_launches;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, jacobi_kernel<2>, R, l, A, J, counters, status, max_sweeps, Aout,
+                                         Jout, nrm);
+      if (e == cudaSuccess) {
+        done = true;
+        break;
+      }
+      --g_launches;
+      (void)cudaGetLastError();
+    }
+  }
+  if (!done) {
     int m = (l & 1) ? l + 1 : l;
     int warps_needed = m / 2;
     int threads = 256;
     int blocks = (warps_needed * 32 + threads - 1) / threads;
     if (blocks > num_sms) blocks = num_sms;
     void* args[] = {(void*)&R, (void*)&l, (void*)&A, (void*)&J, (void*)&counters, (void*)&status,
-                    (void*)&max_sweeps, (void*)&Aout, (void*)&Jout, (void*)&nrm};
+                    (void*)&max_sweeps, (void*)&A, (void*)&J, (void*)&nrm};
     ++g_launches;
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel<false>, dim3(blocks), dim3(threads), args,
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_kernel<1>, dim3(blocks), dim3(threads), args,
                                                 0, st);
     if (e != cudaSuccess) return e;
     Aout = A;
