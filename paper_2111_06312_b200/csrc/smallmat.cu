@@ -698,7 +698,9 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     done = true;
-  } else if (l <= 448) {
+  } else if (l <= 448 && getenv("ISVD_JACOBI_CLUSTER")) {
+    // measured slower than the cooperative-grid variant at l = 160 / 256 / 400 (DSMEM
+    // column reads per pair); kept behind a switch for experiments
     // cluster: the smallest cluster (8, else 16 CTAs) whose shared memory holds A and J
     for (int CS : {8, 16}) {
       const int cols_per = (l + CS - 1) / CS;
