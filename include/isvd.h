@@ -67,11 +67,16 @@ typedef struct isvd_op_s* isvd_op;
 
 /* Create a context on CUDA device `device`, enqueuing on `stream`
  * (a cudaStream_t passed as void*; NULL = the legacy default stream).
- * world == 1: single GPU, nccl_unique_id must be NULL.
- * world  > 1: nccl_unique_id points to the 128-byte ncclUniqueId that rank 0
- *             created (isvd_nccl_unique_id) and every rank received out of
- *             band; the call is collective over the `world` ranks.
- * Device workspace comes from cudaMallocAsync on the ctx stream. */
+ * nccl_unique_id == NULL: single GPU (world must be 1).  Large graphs are then
+ *             relabelled internally by degree (hub rows contiguous and kept
+ *             L2-persisting; every caller-ordered input and output is mapped at
+ *             this boundary, and cudaLimitPersistingL2CacheSize is raised once).
+ * nccl_unique_id != NULL: distributed mode over `world` >= 1 ranks; it points to
+ *             the 128-byte ncclUniqueId that rank 0 created (isvd_nccl_unique_id)
+ *             and every rank received out of band; the call is collective.  The
+ *             row-partitioned schedule (all-gather of every SpMM gather source,
+ *             fp64 all-reduce of Gram / column sums / X^T Z) runs even for world 1.
+ * Device workspace is allocated with cudaMalloc when an op first needs it. */
 isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world,
                             isvd_ctx* out);
 isvd_status isvd_ctx_destroy(isvd_ctx ctx);

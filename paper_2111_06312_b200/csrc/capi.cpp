@@ -39,6 +39,7 @@ struct isvd_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
+  bool dist = false;  // NCCL collectives on (nccl id given); the row partition follows `world`
   ncclComm_t comm = nullptr;
   int num_sms = 148;
   std::string last_error;
@@ -177,13 +178,13 @@ void partition(int64_t n, int world, int rank, int64_t* rb, int64_t* nl) {
 
 // --------------------------------------------------------------- collectives
 void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld) {
-  if (ctx->world == 1) return;
+  if (!ctx->dist) return;
   size_t count = (size_t)g->n_pad * ld;
   NK(ncclAllGather(full + (size_t)ctx->rank * count, full, count, ncclFloat, ctx->comm, ctx->stream));
 }
 
 void allreduce_f64(isvd_ctx ctx, double* buf, size_t count) {
-  if (ctx->world == 1) return;
+  if (!ctx->dist) return;
   NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
 }
 
@@ -281,7 +282,7 @@ void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out
   }
   const float* src = Q;
   int64_t lds = ldq;
-  if (ctx->world > 1) {
+  if (ctx->dist) {
     CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr,
                          ctx->stream));
     allgather_rows(ctx, g, op->full_a, wpad);
@@ -512,7 +513,7 @@ isvd_status isvd_nccl_unique_id(void* id_out, size_t id_bytes) {
 
 isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world, isvd_ctx* out) {
   if (!out || world < 1 || rank < 0 || rank >= world) return ISVD_ERR_INVALID_ARG;
-  if ((world > 1) != (nccl_unique_id != nullptr)) return ISVD_ERR_INVALID_ARG;
+  if (world > 1 && nccl_unique_id == nullptr) return ISVD_ERR_INVALID_ARG;
   *out = nullptr;
   isvd_ctx ctx = new (std::nothrow) isvd_ctx_s();
   if (!ctx) return ISVD_ERR_OOM;
@@ -538,7 +539,8 @@ isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id
     int persist = 0;
     CK(cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device));
     ctx->max_persist_l2 = (size_t)persist;
-    if (world > 1) {
+    if (nccl_unique_id) {  // distributed mode (also world == 1: NCCL path with a 1-rank communicator)
+      ctx->dist = true;
       ncclUniqueId id;
       memcpy(&id, nccl_unique_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, world, id, rank));
@@ -610,7 +612,7 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->nnz = nnz;
     // CSR on the device (copied: the caller may free its arrays on return), with kIdxPad
     // readable zero entries after the last index (the gather prefetches one batch ahead)
-    const bool relabel = ctx->world == 1 && n_local >= kRelabelMinRows;
+    const bool relabel = !ctx->dist && n_local >= kRelabelMinRows;
     std::vector<void*> tmp;
     struct TmpFree {
       std::vector<void*>& v;
@@ -1062,7 +1064,7 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   // sign rule (reading O9)
   CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
   const double* cand = s.cand;
-  if (ctx->world > 1) {
+  if (ctx->dist) {
     NK(ncclAllGather(s.cand, s.cand_all, 3 * k, ncclDouble, ctx->comm, ctx->stream));
     cand = s.cand_all;
   }

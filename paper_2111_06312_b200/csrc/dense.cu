@@ -115,23 +115,28 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
   for (int64_t t = 0; t < ntiles; ++t) {
     int buf = (int)(t & 1);
     if (t + 1 < ntiles) load_tiles((t + 1) * BK);
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float a[TM], b[TN];
+    // fragments of step kk + 1 are read from shared memory while step kk's FMAs issue
+    float a[2][TM], b[2][TN];
+    auto frag = [&](int kk, int s) {
 #pragma unroll
       for (int i = 0; i < TM; i += 4) {
         float4 v = *reinterpret_cast<const float4*>(&As[buf][kk][(i / 4) * 4 * TY + ty * 4]);
-        a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+        a[s][i] = v.x; a[s][i + 1] = v.y; a[s][i + 2] = v.z; a[s][i + 3] = v.w;
       }
 #pragma unroll
       for (int j = 0; j < TN; j += 4) {
         float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][(j / 4) * 4 * TX + tx * 4]);
-        b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+        b[s][j] = v.x; b[s][j + 1] = v.y; b[s][j + 2] = v.z; b[s][j + 3] = v.w;
       }
+    };
+    frag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      if (kk + 1 < BK) frag(kk + 1, (kk + 1) & 1);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[kk & 1][i], b[kk & 1][j], acc[i][j]);
     }
     if (t + 1 < ntiles) {
       store_tiles(buf ^ 1);

@@ -290,3 +290,24 @@ def test_isvd_config4_exact(ctx):
     # same column space on the sampled rows: U_gpu[rows] = U_ref[rows] (V_ref^T V_gpu) up to rounding
     Rot = V.T @ Vg
     assert np.linalg.norm(Ug - Ur @ Rot) <= 1e-3 * np.linalg.norm(Ur)
+
+
+@pytest.mark.parametrize("i", [0, 2])
+def test_distributed_schedule_world1_nccl(i):
+    """The NCCL row-partitioned schedule (all-gathers, fp64 all-reduces, candidate all-gather of
+    the sign rule) through a 1-rank communicator: same parity bar as the single-GPU path."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2111_06312_b200 as isvd
+
+    cfg, g, X, sp = config_inputs(i)
+    c = isvd.Context(0, rank=0, world=1, nccl_id=isvd.nccl_unique_id())
+    op = gpu_op(c, cfg, g, X, sp)
+    p = -1 if cfg["p"] is None else cfg["p"]
+    res = op.svd(sp["k"], p, sp["q"], sp["seed"])
+    _check_isvd(res, _oracle_result(i), sp["k"], f"cfg{i}/nccl")
+    ref = oracle_op(cfg, g, X, sp)
+    from oracle import philox_omega
+
+    Qc = philox_omega(7, 0, op.c_rows(), sp["l"])
+    assert rel_fro(_to_np(op.matmul(torch.from_numpy(Qc).cuda())), ref.matmul(Qc.astype(np.float64))) <= PROD_TOL
