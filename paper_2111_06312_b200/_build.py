@@ -25,6 +25,7 @@ SOURCES = [
     ("omega.cu", ["--fmad=false"]),
     ("spmm.cu", []),
     ("dense.cu", []),
+    ("gram_tc.cu", []),
     ("smallmat.cu", []),
     ("capi.cpp", []),
 ]

@@ -212,6 +212,8 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   int64_t ka = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : wpad;
   int64_t atb = std::max(atb_ws_doubles(g->n_local, ka, wpad, ctx->num_sms),
                          atb_ws_doubles(g->n_local, wpad, wpad, ctx->num_sms));
+  if (gram_tc_supported(g->n_local, wpad))
+    atb = std::max(atb, (gram_tc_ws_floats(g->n_local, wpad, nullptr, nullptr) + 1) / 2);
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
   int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
   op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
@@ -908,6 +910,13 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
 // ==================================================================== solver
 namespace {
 
+// Tensor-core Gram (3xTF32 tcgen05) for the fp32-class Grams of tall iterates; ISVD_TC_GRAM=0 disables.
+bool use_tensor_core_gram(int64_t rows, int64_t l) {
+  static const char* env = getenv("ISVD_TC_GRAM");
+  if (env && env[0] == '0') return false;
+  return gram_tc_supported(rows, l);
+}
+
 // Everything a captured solver graph bakes in (FNV-1a over the argument values).
 uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t ldu, const float* V, int64_t ldv) {
   uint64_t h = 0xCBF29CE484222325ULL;
@@ -968,8 +977,17 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
-  CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                ctx->stream, f32_gram));
+  if (f32_gram && use_tensor_core_gram(rows, l)) {
+    // tcgen05 3xTF32 partials per row chunk, fixed-order fp64 reduction (gram_tc.cu)
+    int64_t lda_ws = 0, ld_ws = 0, chunks = 0;
+    float* ws32 = reinterpret_cast<float*>(op->atb_ws);
+    CK(launch_gram_tc(Y, ld, rows, l, ws32, &lda_ws, &ld_ws, &chunks, gate, ctx->stream));
+    CK(launch_atb_f32_reduce(ws32, lda_ws, ld_ws, chunks, l, l, true, s.gram, l, nullptr, 0, ctx->num_sms, gate,
+                             ctx->stream));
+  } else {
+    CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
+                  ctx->stream, f32_gram));
+  }
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
   CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));

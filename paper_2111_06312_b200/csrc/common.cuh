@@ -120,6 +120,16 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
                        int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,
                        float* out32, int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
                        bool f32_stage = false);
+// fp64 fixed-order sum of `chunks` fp32 partial tiles ws32[c][Ka_pad = ws_lda][ws_ld] -> G / out32.
+cudaError_t launch_atb_f32_reduce(const float* ws32, int64_t ws_lda, int64_t ws_ld, int64_t chunks, int64_t Ka,
+                                  int64_t Kb, bool symmetric, double* G, int64_t ldg, float* out32, int64_t ld32,
+                                  int num_sms, const int* gate, cudaStream_t st);
+// Tensor-core (tcgen05, 3xTF32) Gram partials of Y (rows x l, ld): fp32 tiles per row chunk
+// into ws32 (gram_tc_ws_floats floats); reduce with launch_atb_f32_reduce (symmetric).
+bool gram_tc_supported(int64_t rows, int64_t l);
+int64_t gram_tc_ws_floats(int64_t rows, int64_t l, int64_t* chunks, int64_t* chunk_rows);
+cudaError_t launch_gram_tc(const float* Y, int64_t ld, int64_t rows, int64_t l, float* ws32, int64_t* ws_lda,
+                           int64_t* ws_ld, int64_t* chunks, const int* gate, cudaStream_t st);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);

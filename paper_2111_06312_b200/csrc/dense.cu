@@ -605,6 +605,15 @@ static int64_t atb_ntiles(int64_t Ka, int64_t Kb, bool symmetric) {
   return symmetric ? ta * (ta + 1) / 2 : ta * tb;
 }
 
+cudaError_t launch_atb_f32_reduce(const float* ws32, int64_t ws_lda, int64_t ws_ld, int64_t chunks, int64_t Ka,
+                                  int64_t Kb, bool symmetric, double* G, int64_t ldg, float* out32, int64_t ld32,
+                                  int num_sms, const int* gate, cudaStream_t st) {
+  ++g_launches;
+  atb_f32_reduce_kernel<<<grid_for(Ka * Kb, 256, num_sms * 8), 256, 0, st>>>(
+      ws32, ws_lda, ws_ld, (int)chunks, Ka, Kb, symmetric ? 1 : 0, G, ldg, out32, ld32, gate);
+  return cudaGetLastError();
+}
+
 int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   // the non-symmetric tile count is the smaller one, so its chunk count bounds both cases
   int64_t ch = atb_chunks(rows, atb_ntiles(Ka, Kb, Ka == Kb), num_sms);
