@@ -971,13 +971,23 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
   s.key_k = k;
 }
 
+// Gram precision classes of one CholeskyQR pass.
+//   kGramF64: fp64 FMA on the fp32 data (exact products, fp64 sums) -- input possibly
+//             ill-conditioned (Y = M Omega), and the shifted third pass;
+//   kGramF32: SIMT fp32 sums over <= 1024-row chunks, fp64 across chunks (~1e-6 relative);
+//   kGramTC:  tcgen05 3xTF32 over 512-row chunks: the tensor core's fp32 accumulation
+//             truncates, ~1e-5 relative (measured, profiles/gram_tc_check.cu), so it is only
+//             used where the next pass corrects it: pass 1 of a CholeskyQR2 whose input is
+//             Y = M Q with Q orthonormal (cond(Y) <= cond(M)).
+enum GramMode { kGramF64 = 0, kGramF32 = 1, kGramTC = 2 };
+
 // One Cholesky pass (Alg. 2 right): G = Y^T Y (all-reduced when row-partitioned), R = chol(G), Yout = Y R^-1.
-void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64, bool f32_gram,
-              bool force_fail, const int* gate) {
+void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64,
+              GramMode mode, bool force_fail, const int* gate) {
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
-  if (f32_gram && use_tensor_core_gram(rows, l)) {
+  if (mode == kGramTC && use_tensor_core_gram(rows, l)) {
     // tcgen05 3xTF32 partials per row chunk, fixed-order fp64 reduction (gram_tc.cu)
     int64_t lda_ws = 0, ld_ws = 0, chunks = 0;
     float* ws32 = reinterpret_cast<float*>(op->atb_ws);
@@ -986,7 +996,7 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
                              ctx->stream));
   } else {
     CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                  ctx->stream, f32_gram));
+                  ctx->stream, mode != kGramF64));
   }
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
@@ -996,7 +1006,8 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
 // CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
 // If Rout != null it receives R = R_3 R_2 R_1 (so that Y_in = Y_out R).
 // exact_gram: pass 1 takes the fp64 Gram (input possibly ill-conditioned: Y = M Omega);
-// otherwise pass 1 uses the fp32-chunk Gram too (Y = M Q with Q orthonormal, cond(Y) <= cond(M)).
+// otherwise Y = M Q with Q orthonormal (cond(Y) <= cond(M)) and pass 1 may take the
+// tensor-core Gram; pass 2 (input orthonormal to ~1e-2 or better) takes the fp32-chunk Gram.
 void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64_t l, bool force_fail, double* Rout,
           bool exact_gram) {
   isvd_ctx ctx = op->g->ctx;
@@ -1004,9 +1015,10 @@ void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64
   const int64_t ld = round_up(l, 4);
   int* gate = &ctx->status->need_extra_pass;
   CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, !exact_gram, force_fail, nullptr);
-  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, true, false, nullptr);
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, false, false, gate);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, exact_gram ? kGramF64 : kGramTC, force_fail,
+           nullptr);
+  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, kGramF32, false, nullptr);
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, kGramF64, false, gate);
   CK(launch_scale_rows(Y2, ld, Y, ld, rows, ld, nullptr, 1.f, gate, ctx->stream));  // copy back iff pass 3 ran
   if (Rout) {
     CK(launch_trmm(s.Rb, s.Ra, s.Rab, (int)l, nullptr, ctx->stream));

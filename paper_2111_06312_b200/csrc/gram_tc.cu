@@ -10,8 +10,12 @@
 //
 // One CTA computes a 128 x N tile of G over one chunk of rows:
 //   * all 256 threads stage 32 rows of Y into shared memory, split into hi / lo, in the
-//     UMMA MN-major no-swizzle canonical layout (core matrices of 8 K-rows x 16 bytes,
-//     MN-groups 128 B apart, K-groups E/4*128 B apart), double-buffered;
+//     UMMA K-major no-swizzle canonical layout (core matrices of 8 MN-rows x 4 K-values =
+//     16 bytes per row, MN-groups 128 B apart, K-groups E/8*128 B apart): each thread loads a
+//     4 x 4 block of Y (4 rows, one float4 each), transposes it in registers and stores
+//     four 4-value K-vectors; double-buffered.  (The MN-major form of kind::tf32 was measured
+//     to produce no output on this driver -- profiles/umma_probe.cu -- so the transpose is
+//     done while staging.)
 //   * one thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32 (M = 128, N <= 256, K = 8)
 //     per stage and commits to the stage's mbarrier, which gates refilling that buffer;
 //   * the accumulator lives in TMEM (N fp32 columns x 128 lanes); the epilogue reads it
@@ -28,7 +32,7 @@ constexpr int kTcThreads = 256;
 
 ISVD_DEVICE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// MN-major, SWIZZLE_NONE smem matrix descriptor: start, LBO = K-group stride, SBO = MN-group stride.
+// SWIZZLE_NONE smem matrix descriptor: start, LBO = K-group stride, SBO = MN-group stride.
 ISVD_DEVICE uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
@@ -39,10 +43,9 @@ ISVD_DEVICE uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_
   return d;
 }
 
-// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, both MN-major, M x N.
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, both K-major, M x N.
 __host__ __device__ constexpr uint32_t umma_idesc(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 ISVD_DEVICE void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -82,12 +85,42 @@ ISVD_DEVICE void umma_commit(uint64_t* bar) {
 
 ISVD_DEVICE float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// Store 4 consecutive MN-elements (c % 4 == 0) of K-row k into the canonical layout.
-ISVD_DEVICE void st_split(float* hi, float* lo, int k, int c, int lbo_floats, float4 v) {
-  const int off = (k >> 3) * lbo_floats + (c >> 2) * 32 + (k & 7) * 4;
+// Store the K-vector (rows k0..k0+3, k0 % 4 == 0) of MN-element c into the K-major layout.
+ISVD_DEVICE void st_split(float* hi, float* lo, int k0, int c, int lbo_floats, float4 v) {
+  const int off = (k0 >> 2) * lbo_floats + (c >> 3) * 32 + (c & 7) * 4;
   float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
   *reinterpret_cast<float4*>(hi + off) = h;
   *reinterpret_cast<float4*>(lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
+
+// Stage a 32-row x E-column slice of Y (columns [c0, c0 + E)) into the K-major hi/lo buffers.
+template <int E>
+ISVD_DEVICE void stage_operand(const float* __restrict__ Y, int64_t ld, int64_t k0, int64_t r_end, int64_t c0,
+                               int64_t l, float* hi, float* lo, int tid) {
+  constexpr int LBO = E / 8 * 32;  // floats
+  for (int f = tid; f < (kTcKB / 4) * (E / 4); f += kTcThreads) {
+    const int kb = f / (E / 4), cb = f - kb * (E / 4);
+    const int c = cb * 4;
+    float4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t gr = k0 + kb * 4 + q;
+      v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < r_end && c0 + c < l) v[q] = __ldg(reinterpret_cast<const float4*>(Y + gr * ld + c0 + c));
+    }
+    // transpose: K-vector of column c + j = (v[0].j, v[1].j, v[2].j, v[3].j); rotate j by the
+    // thread index to spread the 16-byte stores over the banks
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = (jj + cb) & 3;
+      float4 kv;
+      if (j == 0) kv = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+      else if (j == 1) kv = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+      else if (j == 2) kv = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+      else kv = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+      st_split(hi, lo, kb * 4, c + j, LBO, kv);
+    }
+  }
 }
 
 template <int N>
@@ -97,7 +130,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (gate && *((volatile const int*)gate) == 0) return;
   constexpr int A_FL = kTcKB * kTcM;  // floats per A hi/lo stage buffer
   constexpr int B_FL = kTcKB * N;
-  constexpr int LBO_A = kTcM / 4 * 32, LBO_B = N / 4 * 32;  // K-group strides in floats
+  constexpr int LBO_A = kTcM / 8 * 32, LBO_B = N / 8 * 32;  // K-group (4 values) strides in floats
   extern __shared__ __align__(1024) float sm[];
   float* Ahi[2] = {sm, sm + 2 * A_FL + 2 * B_FL};
   float* Alo[2] = {Ahi[0] + A_FL, Ahi[1] + A_FL};
@@ -134,20 +167,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (st >= 2) mbar_wait(&mbar[buf], (uint32_t)(((st - 2) >> 1) & 1));  // MMAs of stage st-2 done
     const int64_t k0 = r_begin + st * kTcKB;
     // stage rows [k0, k0 + 32): A = columns [a0, a0 + 128), B = columns [b0, b0 + N)
-    for (int f = tid; f < kTcKB * (kTcM / 4); f += kTcThreads) {
-      const int k = f / (kTcM / 4), c = (f - k * (kTcM / 4)) * 4;
-      const int64_t gr = k0 + k, gc = a0 + c;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < r_end && gc < l) v = __ldg(reinterpret_cast<const float4*>(Y + gr * ld + gc));
-      st_split(Ahi[buf], Alo[buf], k, c, LBO_A, v);
-    }
-    for (int f = tid; f < kTcKB * (N / 4); f += kTcThreads) {
-      const int k = f / (N / 4), c = (f - k * (N / 4)) * 4;
-      const int64_t gr = k0 + k, gc = b0 + c;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < r_end && gc < l) v = __ldg(reinterpret_cast<const float4*>(Y + gr * ld + gc));
-      st_split(Bhi[buf], Blo[buf], k, c, LBO_B, v);
-    }
+    stage_operand<kTcM>(Y, ld, k0, r_end, a0, l, Ahi[buf], Alo[buf], tid);
+    stage_operand<N>(Y, ld, k0, r_end, b0, l, Bhi[buf], Blo[buf], tid);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
     __syncthreads();
     if (tid == 0) {
@@ -156,7 +177,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t bh = smem_u32(Bhi[buf]), bl = smem_u32(Blo[buf]);
 #pragma unroll
       for (int s = 0; s < kTcKB / 8; ++s) {
-        const uint32_t ka = (uint32_t)s * LBO_A * 4, kb = (uint32_t)s * LBO_B * 4;  // bytes
+        // one MMA (K = 8) spans two K-groups
+        const uint32_t ka = (uint32_t)(2 * s) * LBO_A * 4, kb = (uint32_t)(2 * s) * LBO_B * 4;  // bytes
         const uint64_t dah = umma_desc(ah + ka, LBO_A * 4, 128), dal = umma_desc(al + ka, LBO_A * 4, 128);
         const uint64_t dbh = umma_desc(bh + kb, LBO_B * 4, 128), dbl = umma_desc(bl + kb, LBO_B * 4, 128);
         mma_tf32(tmem, dah, dbh, idesc, (st > 0 || s > 0) ? 1u : 0u);
@@ -211,7 +233,9 @@ bool gram_tc_supported(int64_t rows, int64_t l) {
 int64_t gram_tc_ws_floats(int64_t rows, int64_t l, int64_t* chunks_out, int64_t* chunk_rows_out) {
   const int n = tc_tile_n(l);
   const int64_t ta = ceil_div(l, kTcM), tb = ceil_div(l, n);
-  int64_t cr = 2048;
+  // rows per TMEM accumulation: the tensor core's fp32 accumulation truncates, so the error
+  // grows ~linearly with the chunk (measured 3.8e-5 relative at 2048 rows)
+  int64_t cr = 512;
   const int64_t chunks = ceil_div(rows, cr);
   if (chunks_out) *chunks_out = chunks;
   if (chunk_rows_out) *chunk_rows_out = cr;
