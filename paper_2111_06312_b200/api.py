@@ -206,6 +206,14 @@ class _Operator:
               "isvd_sample_omega", self.ctx.h)
         return om
 
+    def host_buffers(self, k: int):
+        """Page-locked host arrays (U, V) for svd(host_output=True, out=...): the library's device-to-host copies
+        run at full DMA speed and a repeated call pays no allocation."""
+        kk = max(round_up(k), 4)
+        U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, pin_memory=True).numpy()
+        V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, pin_memory=True).numpy()
+        return U, V
+
     def svd(self, k: int, oversampling: int = -1, power_iters: int = 2, seed: int = 0, host_output: bool = False,
             omega: "torch.Tensor | None" = None, force_chol_fail: bool = False, profile: bool = False,
             out=None) -> SvdResult:
@@ -215,10 +223,17 @@ class _Operator:
         flags = 0
         if host_output:
             flags |= _lib.ISVD_SVD_HOST_OUTPUT
-            # page-locked host buffers: the library's device-to-host copies run at full DMA speed
-            U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, pin_memory=True).numpy()
-            V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, pin_memory=True).numpy()
-            pu, pv, ldu, ldv = U.ctypes.data, V.ctypes.data, kk, kk
+            if out is not None:  # caller-owned host arrays (ideally page-locked, see host_buffers())
+                U, V = out
+                for a, rows in ((U, self.graph.n_local), (V, self.c_rows())):
+                    if (not isinstance(a, np.ndarray) or a.dtype != np.float32 or a.ndim != 2
+                            or a.shape[0] < rows or a.shape[1] < k or a.strides[1] != 4
+                            or not a.flags.writeable):
+                        raise ValueError("host output must be a writeable float32 row-major array of >= rows x k")
+                pu, pv, ldu, ldv = U.ctypes.data, V.ctypes.data, U.strides[0] // 4, V.strides[0] // 4
+            else:
+                U, V = self.host_buffers(k)
+                pu, pv, ldu, ldv = U.ctypes.data, V.ctypes.data, kk, kk
         else:
             if out is not None:
                 U, V = out

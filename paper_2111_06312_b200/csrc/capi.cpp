@@ -212,12 +212,38 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   int64_t ka = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : wpad;
   int64_t atb = std::max(atb_ws_doubles(g->n_local, ka, wpad, ctx->num_sms),
                          atb_ws_doubles(g->n_local, wpad, wpad, ctx->num_sms));
-  if (gram_tc_supported(g->n_local, wpad))
-    atb = std::max(atb, (gram_tc_ws_floats(g->n_local, wpad, nullptr, nullptr) + 1) / 2);
+  atb = std::max(atb, (tc_atb_ws_floats(g->n_local, ka, wpad, false, ctx->num_sms) + 1) / 2);
+  atb = std::max(atb, (tc_atb_ws_floats(g->n_local, wpad, wpad, true, ctx->num_sms) + 1) / 2);
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
   int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
   op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
   op->ws_wpad = wpad;
+}
+
+// Tensor cores for the fp32-class tall products (3xTF32, gram_tc.cu); ISVD_TC_GRAM=0 disables.
+bool use_tensor_cores(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t ldb) {
+  static const char* env = getenv("ISVD_TC_GRAM");
+  if (env && env[0] == '0') return false;
+  return tc_atb_supported(rows, Ka, Kb, lda, ldb);
+}
+
+// G (fp64, ldg) = (diag(row_scale) A)^T B over this rank's rows, fp32-class numerics: tcgen05
+// 3xTF32 over 128-row TMEM chunks when supported, else SIMT fp32 over <= 1024-row chunks; fp64
+// across chunks/parts in a fixed order either way.
+void atb_fp32(isvd_op op, int64_t rows, const float* A, int64_t lda, int64_t Ka, const float* row_scale,
+              const float* B, int64_t ldb, int64_t Kb, bool symmetric, double* G, int64_t ldg, const int* gate) {
+  isvd_ctx ctx = op->g->ctx;
+  if (use_tensor_cores(rows, Ka, Kb, lda, ldb)) {
+    int64_t ws_lda = 0, ws_ld = 0, parts = 0;
+    float* ws32 = reinterpret_cast<float*>(op->atb_ws);
+    CK(launch_tc_atb(A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, &ws_lda, &ws_ld, &parts,
+                     ctx->num_sms, gate, ctx->stream));
+    CK(launch_atb_f32_reduce(ws32, ws_lda, ws_ld, parts, Ka, Kb, symmetric, G, ldg, nullptr, 0, ctx->num_sms, gate,
+                             ctx->stream));
+    return;
+  }
+  CK(launch_atb(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric, op->atb_ws, G, ldg, nullptr, 0, ctx->num_sms,
+                gate, ctx->stream, true));
 }
 
 SpmmArgs spmm_base(const isvd_graph_s* g, int64_t wpad) {
@@ -249,7 +275,9 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
   if (g->new2old) persist = std::min(ctx->max_persist_l2, (size_t)(g->n_pad * ctx->world) * a.wpad * sizeof(float));
   static const char* persist_env = getenv("ISVD_L2_PERSIST_MB");  // tuning override (MB; 0 = off)
   if (persist_env && g->new2old) persist = std::min(persist, (size_t)atoll(persist_env) << 20);
-  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist));
+  static const char* cols_env = getenv("ISVD_SPMM_COLS");  // tuning override: column block width
+  const int64_t col_block = cols_env ? atoll(cols_env) : 0;
+  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist, col_block));
   if (e1) CK(cudaEventRecord(e1, ctx->stream));
   // algorithmic bytes of the step: CSR, scale vectors, the gather source read
   // once (all n rows), the epilogue operand T, the output
@@ -412,8 +440,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   // Zt_0 = s Q (internal row order), block 0 = X^T diag(1/s) Zt_0
   CK(launch_scale_rows(Q, ldq, slice(g, bufs[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream,
                        imap));
-  CK(launch_atb(op->X, op->ldx, slice(g, bufs[0], wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
-                op->blk64, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, true));
+  atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, slice(g, bufs[0], wpad), wpad, wpad, false, op->blk64, wpad, nullptr);
   if (L > 0) allgather_rows(ctx, g, bufs[0], wpad);
   for (int j = 1; j <= L; ++j) {
     float* src = bufs[(j - 1) & 1];
@@ -424,8 +451,8 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
     a.out = slice(g, dst, wpad); a.ldo = wpad;
     spmm(ctx, op, a);
     if (j < L) allgather_rows(ctx, g, dst, wpad);
-    CK(launch_atb(op->X, op->ldx, slice(g, dst, wpad), wpad, g->n_local, d, wpad, g->rs, false, op->atb_ws,
-                  op->blk64 + (size_t)j * d * wpad, wpad, nullptr, 0, ctx->num_sms, nullptr, ctx->stream, true));
+    atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, slice(g, dst, wpad), wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
+             wpad, nullptr);
   }
   const int64_t c = d * (L + 1);
   allreduce_f64(ctx, op->blk64, (size_t)c * wpad);
@@ -910,13 +937,6 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
 // ==================================================================== solver
 namespace {
 
-// Tensor-core Gram (3xTF32 tcgen05) for the fp32-class Grams of tall iterates; ISVD_TC_GRAM=0 disables.
-bool use_tensor_core_gram(int64_t rows, int64_t l) {
-  static const char* env = getenv("ISVD_TC_GRAM");
-  if (env && env[0] == '0') return false;
-  return gram_tc_supported(rows, l);
-}
-
 // Everything a captured solver graph bakes in (FNV-1a over the argument values).
 uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t ldu, const float* V, int64_t ldv) {
   uint64_t h = 0xCBF29CE484222325ULL;
@@ -972,14 +992,11 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
 }
 
 // Gram precision classes of one CholeskyQR pass.
-//   kGramF64: fp64 FMA on the fp32 data (exact products, fp64 sums) -- input possibly
-//             ill-conditioned (Y = M Omega), and the shifted third pass;
-//   kGramF32: SIMT fp32 sums over <= 1024-row chunks, fp64 across chunks (~1e-6 relative);
-//   kGramTC:  tcgen05 3xTF32 over 512-row chunks: the tensor core's fp32 accumulation
-//             truncates, ~1e-5 relative (measured, profiles/gram_tc_check.cu), so it is only
-//             used where the next pass corrects it: pass 1 of a CholeskyQR2 whose input is
-//             Y = M Q with Q orthonormal (cond(Y) <= cond(M)).
-enum GramMode { kGramF64 = 0, kGramF32 = 1, kGramTC = 2 };
+//   kGramF64:  fp64 FMA on the fp32 data (exact products, fp64 sums) -- input possibly
+//              ill-conditioned (Y = M Omega), and the shifted third pass;
+//   kGramFp32: fp32-class sums over short row chunks (128-row tcgen05 3xTF32 TMEM chunks, or
+//              <= 1024-row SIMT chunks), fp64 across chunks: ~1e-6 relative (atb_fp32).
+enum GramMode { kGramF64 = 0, kGramFp32 = 1 };
 
 // One Cholesky pass (Alg. 2 right): G = Y^T Y (all-reduced when row-partitioned), R = chol(G), Yout = Y R^-1.
 void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64,
@@ -987,17 +1004,11 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
-  if (mode == kGramTC && use_tensor_core_gram(rows, l)) {
-    // tcgen05 3xTF32 partials per row chunk, fixed-order fp64 reduction (gram_tc.cu)
-    int64_t lda_ws = 0, ld_ws = 0, chunks = 0;
-    float* ws32 = reinterpret_cast<float*>(op->atb_ws);
-    CK(launch_gram_tc(Y, ld, rows, l, ws32, &lda_ws, &ld_ws, &chunks, gate, ctx->stream));
-    CK(launch_atb_f32_reduce(ws32, lda_ws, ld_ws, chunks, l, l, true, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                             ctx->stream));
-  } else {
+  if (mode == kGramFp32)
+    atb_fp32(op, rows, Y, ld, l, nullptr, Y, ld, l, true, s.gram, l, gate);
+  else
     CK(launch_atb(Y, ld, Y, ld, rows, l, l, nullptr, true, op->atb_ws, s.gram, l, nullptr, 0, ctx->num_sms, gate,
-                  ctx->stream, mode != kGramF64));
-  }
+                  ctx->stream, false));
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
   CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));
@@ -1006,8 +1017,8 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
 // CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
 // If Rout != null it receives R = R_3 R_2 R_1 (so that Y_in = Y_out R).
 // exact_gram: pass 1 takes the fp64 Gram (input possibly ill-conditioned: Y = M Omega);
-// otherwise Y = M Q with Q orthonormal (cond(Y) <= cond(M)) and pass 1 may take the
-// tensor-core Gram; pass 2 (input orthonormal to ~1e-2 or better) takes the fp32-chunk Gram.
+// otherwise Y = M Q with Q orthonormal (cond(Y) <= cond(M)) and pass 1 takes the fp32-class
+// Gram, as does pass 2 (input orthonormal to ~1e-2 or better).
 void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64_t l, bool force_fail, double* Rout,
           bool exact_gram) {
   isvd_ctx ctx = op->g->ctx;
@@ -1015,9 +1026,9 @@ void cqr2(isvd_op op, float* Y, float* Y2, int64_t rows, bool distributed, int64
   const int64_t ld = round_up(l, 4);
   int* gate = &ctx->status->need_extra_pass;
   CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
-  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, exact_gram ? kGramF64 : kGramTC, force_fail,
+  cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Ra : nullptr, exact_gram ? kGramF64 : kGramFp32, force_fail,
            nullptr);
-  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, kGramF32, false, nullptr);
+  cqr_pass(op, Y2, Y, rows, distributed, l, Rout ? s.Rb : nullptr, kGramFp32, false, nullptr);
   cqr_pass(op, Y, Y2, rows, distributed, l, Rout ? s.Rc : nullptr, kGramF64, false, gate);
   CK(launch_scale_rows(Y2, ld, Y, ld, rows, ld, nullptr, 1.f, gate, ctx->stream));  // copy back iff pass 3 ran
   if (Rout) {

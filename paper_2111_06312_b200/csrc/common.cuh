@@ -101,8 +101,9 @@ cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, con
                                cudaStream_t st);
 // `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled
 // graph) are marked L2-persisting for this launch (cudaAccessPolicyWindow on `st`).
+// col_block > 0: process the columns in blocks of that width (one launch each).
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a, float* ws_partial, int num_sms,
-                        cudaStream_t st, size_t persist_bytes = 0);
+                        cudaStream_t st, size_t persist_bytes = 0, int64_t col_block = 0);
 
 // ------------------------------------------------------------------- dense
 // C[out_map ? out_map[i] : i, j] = alpha * row_scale(i) * sum_k A[i, k] B[k, j],  i < M, j < N (N multiple of 4).
@@ -124,12 +125,15 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
 cudaError_t launch_atb_f32_reduce(const float* ws32, int64_t ws_lda, int64_t ws_ld, int64_t chunks, int64_t Ka,
                                   int64_t Kb, bool symmetric, double* G, int64_t ldg, float* out32, int64_t ld32,
                                   int num_sms, const int* gate, cudaStream_t st);
-// Tensor-core (tcgen05, 3xTF32) Gram partials of Y (rows x l, ld): fp32 tiles per row chunk
-// into ws32 (gram_tc_ws_floats floats); reduce with launch_atb_f32_reduce (symmetric).
-bool gram_tc_supported(int64_t rows, int64_t l);
-int64_t gram_tc_ws_floats(int64_t rows, int64_t l, int64_t* chunks, int64_t* chunk_rows);
-cudaError_t launch_gram_tc(const float* Y, int64_t ld, int64_t rows, int64_t l, float* ws32, int64_t* ws_lda,
-                           int64_t* ws_ld, int64_t* chunks, const int* gate, cudaStream_t st);
+// Tensor-core (tcgen05, 3xTF32) partials of C = (diag(row_scale) A)^T B (A: rows x Ka, B: rows x Kb,
+// row-major, ld % 4 == 0): one fp32 tile per row part into ws32 (tc_atb_ws_floats floats),
+// ws32[part][ws_lda][ws_ld]; reduce with launch_atb_f32_reduce over `parts`.  symmetric: A == B,
+// only the tiles holding some i <= j are computed (the reduce mirrors).
+bool tc_atb_supported(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t ldb);
+int64_t tc_atb_ws_floats(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num_sms);
+cudaError_t launch_tc_atb(const float* A, int64_t lda, int64_t Ka, const float* row_scale, const float* B,
+                          int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws32, int64_t* ws_lda,
+                          int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);

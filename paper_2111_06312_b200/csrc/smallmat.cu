@@ -306,14 +306,19 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
                                                              int l, int k, int64_t ldk, double* sig_ws,
                                                              double* __restrict__ sigma_k, float* __restrict__ Ub,
                                                              float* __restrict__ Vb, DevStatus* status) {
-  __shared__ int perm[512];
+  __shared__ int perm[1024];  // l <= 1024 (isvd_svd rejects wider)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < l; j += nw) {
     const double* aj = A + (int64_t)j * l;
     double s = 0.0;
     for (int r = lane; r < l; r += 32) s += aj[r] * aj[r];
     s = warp_sum(s);
-    if (lane == 0) sig_ws[j] = sqrt(s);
+    if (lane == 0) {
+      // a non-finite norm is flagged below and ranked last as -1 so the ranking stays a total order
+      // (NaN compares false both ways) and perm[] is a permutation -- no out-of-range gathers
+      if (!isfinite(s)) atomicOr(&status->nonfinite, 1);
+      sig_ws[j] = isfinite(s) ? sqrt(s) : -1.0;
+    }
   }
   __syncthreads();
   for (int j = tid; j < l; j += blockDim.x) {
@@ -324,7 +329,6 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
       rank += (si > sj) || (si == sj && i < j);
     }
     if (rank < k) perm[rank] = j;
-    if (!isfinite(sj) && tid >= 0) atomicOr(&status->nonfinite, 1);
   }
   __syncthreads();
   for (int t = tid; t < k; t += blockDim.x) sigma_k[t] = sig_ws[perm[t]];

@@ -185,13 +185,28 @@ cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, con
 }
 
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_partial, int num_sms, cudaStream_t st,
-                        size_t persist_bytes) {
+                        size_t persist_bytes, int64_t col_block) {
   if (plan.n_local == 0) return cudaSuccess;
-  if (persist_bytes) set_window(st, a0.Y, persist_bytes);
-  // Column chunks of at most 4096 columns (team of <= 1024 threads).
-  for (int64_t c0 = 0; c0 < a0.wpad; c0 += 4096) {
+  // Column blocks of at most min(col_block, 4096) columns (team of <= 1024 threads); a narrower
+  // block gathers shorter row slices, so L2 holds proportionally more rows of the gather source.
+  int64_t cb = col_block > 0 ? round_up(col_block, 4) : 4096;
+  if (cb > 4096) cb = 4096;
+  static int max_window = -1;
+  if (max_window < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess) max_window = 0;
+  }
+  for (int64_t c0 = 0; c0 < a0.wpad; c0 += cb) {
     SpmmArgs a = a0;
-    a.wpad = (a0.wpad - c0) < 4096 ? (a0.wpad - c0) : 4096;
+    a.wpad = (a0.wpad - c0) < cb ? (a0.wpad - c0) : cb;
+    if (persist_bytes) {
+      // the window spans whole rows; only this block's slices of them are touched, so it is
+      // widened by ldy / width to keep about persist_bytes of persisting lines in use
+      size_t wb = persist_bytes * (size_t)(a0.ldy / a.wpad);
+      if (wb > (size_t)max_window) wb = (size_t)max_window;
+      set_window(st, a0.Y + c0, wb);
+    }
     a.Y += c0;
     if (a.T) a.T += c0;
     if (a.colsum) a.colsum += c0;
