@@ -26,6 +26,7 @@ SOURCES = [
     ("spmm.cu", []),
     ("dense.cu", []),
     ("gram_tc.cu", []),
+    ("gemm_tc.cu", []),
     ("smallmat.cu", []),
     ("capi.cpp", []),
 ]

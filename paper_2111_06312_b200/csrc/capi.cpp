@@ -105,6 +105,7 @@ struct isvd_op_s {
   std::vector<void*> ws_allocs;
   float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
+  float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
   SolverWs sws;
 };
 
@@ -215,6 +216,8 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   atb = std::max(atb, (tc_atb_ws_floats(g->n_local, ka, wpad, false, ctx->num_sms) + 1) / 2);
   atb = std::max(atb, (tc_atb_ws_floats(g->n_local, wpad, wpad, true, ctx->num_sms) + 1) / 2);
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
+  op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
+                              op->ws_allocs);
   int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
   op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
   op->ws_wpad = wpad;
@@ -244,6 +247,22 @@ void atb_fp32(isvd_op op, int64_t rows, const float* A, int64_t lda, int64_t Ka,
   }
   CK(launch_atb(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric, op->atb_ws, G, ldg, nullptr, 0, ctx->num_sms,
                 gate, ctx->stream, true));
+}
+
+// C[map(i), j] = alpha row_scale(i) (A B)[i, j], i < rows, j < N: tcgen05 3xTF32 for tall A
+// (gemm_tc.cu), else the SIMT fp32 kernel (dense.cu); ISVD_TC_GEMM=0 disables the former.
+void gemm_fp32(isvd_op op, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+               int64_t rows, int64_t N, int64_t K, const float* row_scale, bool upper_tri_b, const int* gate,
+               const int32_t* out_map = nullptr) {
+  isvd_ctx ctx = op->g->ctx;
+  static const char* env = getenv("ISVD_TC_GEMM");
+  const bool tc = !(env && env[0] == '0') && tc_gemm_supported(rows, N, K, lda, ldc) &&
+                  tc_gemm_ws_floats(N, K) <= tc_gemm_ws_floats(op->ws_wpad, std::max<int64_t>(op->ws_wpad, op->d));
+  if (tc)
+    CK(launch_tc_gemm(A, lda, B, ldb, C, ldc, rows, N, K, row_scale, 1.f, gate, ctx->stream, out_map, op->bt_ws,
+                      ctx->num_sms));
+  else
+    CK(launch_gemm_tn(A, lda, B, ldb, C, ldc, rows, N, K, row_scale, 1.f, upper_tri_b, gate, ctx->stream, out_map));
 }
 
 SpmmArgs spmm_base(const isvd_graph_s* g, int64_t wpad) {
@@ -392,18 +411,17 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
   const int64_t d = op->d;
   const int32_t* omap = (user_order && g->new2old) ? g->new2old : nullptr;
   if (L == 0) {
-    CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
-                      ctx->stream, omap));
+    gemm_fp32(op, op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, false, nullptr, omap);
     return;
   }
   float* bufs[2] = {op->full_a, op->full_b};
   float* cur = bufs[L & 1];
-  CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, slice(g, cur, wpad), wpad, g->n_local, wpad, d,
-                    g->s, 1.f, false, nullptr, ctx->stream));
+  gemm_fp32(op, op->X, op->ldx, G + (size_t)L * d * ldgm, ldgm, slice(g, cur, wpad), wpad, g->n_local, wpad, d,
+            g->s, false, nullptr);
   allgather_rows(ctx, g, cur, wpad);
   for (int j = L - 1; j >= 1; --j) {
-    CK(launch_gemm_tn(op->X, op->ldx, G + (size_t)j * d * ldgm, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr,
-                      1.f, false, nullptr, ctx->stream));
+    gemm_fp32(op, op->X, op->ldx, G + (size_t)j * d * ldgm, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr,
+              false, nullptr);
     float* dst = bufs[j & 1];
     SpmmArgs a = spmm_base(g, wpad);
     a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
@@ -418,8 +436,7 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
   // accumulation into `out` needs identical read and write rows)
   float* t0 = omap ? op->ptmp : out;
   const int64_t ldt0 = omap ? wpad : ldo;
-  CK(launch_gemm_tn(op->X, op->ldx, G, ldgm, t0, ldt0, g->n_local, wpad, d, nullptr, 1.f, false, nullptr,
-                    ctx->stream));
+  gemm_fp32(op, op->X, op->ldx, G, ldgm, t0, ldt0, g->n_local, wpad, d, nullptr, false, nullptr);
   SpmmArgs a = spmm_base(g, wpad);
   a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
   a.post_vec = g->s;
@@ -1011,7 +1028,7 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
                   ctx->stream, false));
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
-  CK(launch_gemm_tn(Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, 1.f, true, gate, ctx->stream));
+  gemm_fp32(op, Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, true, gate);
 }
 
 // CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
@@ -1099,9 +1116,8 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
                        ctx->stream));
   // Alg. 1 line 12: U = Q U_B;  V = Q_W V_B;  truncate to k
   // (relabelled graphs: rows go back to the caller's order here)
-  CK(launch_gemm_tn(s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream, g->new2old));
-  CK(launch_gemm_tn(s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, 1.f, false, nullptr, ctx->stream,
-                    ne ? g->new2old : nullptr));
+  gemm_fp32(op, s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, false, nullptr, g->new2old);
+  gemm_fp32(op, s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, false, nullptr, ne ? g->new2old : nullptr);
   // sign rule (reading O9)
   CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
   const double* cand = s.cand;

@@ -112,6 +112,14 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
                            int64_t M, int64_t N, int64_t K, const float* row_scale, float alpha,
                            bool upper_tri_b, const int* gate, cudaStream_t st, const int32_t* out_map = nullptr);
 
+// Tensor-core (tcgen05, 3xTF32) tall GEMM: C[map(i), j] = alpha row_scale(i) sum_k A[i, k] B[k, j],
+// i < rows, j < N; A rows x K (lda % 4 == 0), B K x N (ldb), C ldc.  ws_bt: tc_gemm_ws_floats floats.
+bool tc_gemm_supported(int64_t rows, int64_t N, int64_t K, int64_t lda, int64_t ldc);
+int64_t tc_gemm_ws_floats(int64_t N, int64_t K);
+cudaError_t launch_tc_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                           int64_t rows, int64_t N, int64_t K, const float* row_scale, float alpha, const int* gate,
+                           cudaStream_t st, const int32_t* out_map, float* ws_bt, int num_sms);
+
 // G = A^T diag(row_scale) B over `rows` rows, A: rows x Ka, B: rows x Kb -> fp64 Ka x ldg.
 // symmetric: A == B, only the upper triangle of tiles is computed and mirrored.
 // If out32 != null the result is also written as fp32 (ld32).

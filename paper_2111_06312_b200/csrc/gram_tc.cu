@@ -15,7 +15,7 @@
 //   * partials are summed in fp64 in a fixed order by atb_f32_reduce_kernel (dense.cu).
 // The result is in the fp32-chunk numerics class of the SIMT path.
 //
-// One CTA (256 threads, 1 per SM: TMEM 2N columns, ~200 KB smem) computes a 128 x N tile over
+// One CTA (512 threads, 1 per SM: TMEM 2N columns, ~200 KB smem) computes a 128 x N tile over
 // a contiguous row range:
 //   * all threads stage 32 rows per step into shared memory in the UMMA K-major no-swizzle
 //     canonical layout (core matrices of 8 MN-rows x 4 K-values = 16 bytes per row, MN-groups
@@ -28,76 +28,20 @@
 //   * one thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32 (M = 128, N <= 256, K = 8) per
 //     step and commits to the step buffer's mbarrier (gates refilling it) and, at the end of a
 //     chunk, to the chunk's mbarrier (gates draining it);
-//   * warp w drains TMEM lanes 32 (w % 4) .. +31 (rows of the tile), columns half w / 4, with
+//   * warp w drains TMEM lanes 32 (w % 4) .. +31 (rows of the tile), column quarter w / 4, with
 //     tcgen05.ld.32x32b.
 // Operand descriptors and the instruction descriptor follow the sm_100 UMMA bit layouts.
 #include <algorithm>
 
 #include "common.cuh"
+#include "umma.cuh"
 
 namespace isvd {
 namespace {
 
 constexpr int kTcM = 128;       // UMMA M (rows of the C tile = columns of A)
-constexpr int kTcKB = 32;       // rows per pipeline step (4 MMAs of K = 8)
 constexpr int kTcChunk = 128;   // rows per TMEM accumulation (truncation bound)
-constexpr int kTcStepsPerChunk = kTcChunk / kTcKB;
-constexpr int kTcThreads = 256;
-
-ISVD_DEVICE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// SWIZZLE_NONE smem matrix descriptor: start, LBO = K-group stride, SBO = MN-group stride.
-ISVD_DEVICE uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
-  // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
-  return d;
-}
-
-// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, both K-major, M x N.
-__host__ __device__ constexpr uint32_t umma_idesc(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-ISVD_DEVICE void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-
-ISVD_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-// Bounded wait: a commit that never arrives traps (kernel error) instead of hanging the GPU.
-ISVD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
-  for (uint32_t it = 0;; ++it) {
-    uint32_t done;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (it > (1u << 26)) __trap();
-  }
-}
-
-ISVD_DEVICE void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-ISVD_DEVICE float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+constexpr int kTcThreads = 512;  // 16 warps: 4 TMEM lane quadrants x 4 column quarters
 
 // Store the K-vector (rows k0..k0+3, k0 % 4 == 0) of MN-element c into the K-major layout.
 ISVD_DEVICE void st_split(float* hi, float* lo, int k0, int c, int lbo_floats, float4 v) {
@@ -107,32 +51,28 @@ ISVD_DEVICE void st_split(float* hi, float* lo, int k0, int c, int lbo_floats, f
   *reinterpret_cast<float4*>(lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
 }
 
-// A 4 x 4 block of one operand: rows k0 + 4 kb .. +3, columns c0 + 4 cb .. +3 (zero outside
-// [0, r_end) x [0, cols)); row_scale multiplies each row when given.
-ISVD_DEVICE void load_block(const float* __restrict__ src, int64_t ld, int64_t cols, const float* __restrict__ rs,
-                            int64_t k0, int64_t r_end, int64_t c, int kb, float4 (&v)[4]) {
+// Convert one 4 x 4 block (raw rows 4 kb .. +3, columns 4 cb .. +3, row-major with row stride
+// W floats) into the K-major hi / lo layout of an E-wide operand.  Rows >= valid_rows and
+// columns >= valid_cols are zero; row q is multiplied by sc[q].
+// Bank map: the 16-byte store slot of (cb, j) within a 128-byte line is 4 (cb & 1) + j', with
+// j' = (j + (cb >> 1)) & 3, so 8 consecutive blocks hit 8 distinct slots.
+template <int E, int W>
+ISVD_DEVICE void convert_block(const float* raw, float* hi, float* lo, int kb, int cb, int valid_rows,
+                               int valid_cols, const float (&sc)[4]) {
+  constexpr int LBO = E / 8 * 32;  // floats
+  float4 v[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int64_t gr = k0 + kb * 4 + q;
+    const int r = kb * 4 + q;
     v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gr < r_end && c < cols) {
-      v[q] = __ldg(reinterpret_cast<const float4*>(src + gr * ld + c));
-      if (rs) {
-        const float s = __ldg(rs + gr);
-        v[q].x *= s; v[q].y *= s; v[q].z *= s; v[q].w *= s;
-      }
+    if (r < valid_rows && cb * 4 < valid_cols) {
+      v[q] = *reinterpret_cast<const float4*>(raw + r * W + cb * 4);
+      v[q].x *= sc[q]; v[q].y *= sc[q]; v[q].z *= sc[q]; v[q].w *= sc[q];
     }
   }
-}
-
-// transpose: K-vector of column c + j = (v[0].j, v[1].j, v[2].j, v[3].j); rotate j by the
-// block index to spread the 16-byte stores over the banks
-template <int E>
-ISVD_DEVICE void store_block(float* hi, float* lo, int kb, int cb, const float4 (&v)[4]) {
-  constexpr int LBO = E / 8 * 32;  // floats
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) {
-    const int j = (jj + cb) & 3;
+    const int j = (jj + (cb >> 1)) & 3;
     float4 kv;
     if (j == 0) kv = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
     else if (j == 1) kv = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
@@ -143,27 +83,37 @@ ISVD_DEVICE void store_block(float* hi, float* lo, int kb, int cb, const float4 
 }
 
 template <int N>
+struct TcCfg {
+  static constexpr int kStep = 16;                     // rows per pipeline step (2 MMAs of K = 8)
+  static constexpr int kStepsPerChunk = kTcChunk / kStep;
+  static constexpr int kRing = 4;                      // raw stages in flight
+  static constexpr int RAW_FL = kStep * (kTcM + N);    // raw A | raw B rows of one step
+  static constexpr int A_FL = kStep * kTcM, B_FL = kStep * N;
+  static constexpr int CONV_FL = 2 * A_FL + 2 * B_FL;  // A hi | A lo | B hi | B lo
+  static constexpr size_t smem_bytes() { return (size_t)(kRing * RAW_FL + 2 * CONV_FL) * sizeof(float); }
+};
+
+template <int N>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_atb_kernel(const float* __restrict__ A, int64_t lda, int64_t Ka, const float* __restrict__ rs,
-                  const float* __restrict__ B, int64_t ldb, int64_t Kb, int64_t rows, int ta, int tb, int symmetric,
+    tc_atb_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Ka,
+                  const float* __restrict__ rs, int64_t Kb, int64_t rows, int ta, int tb, int symmetric,
                   int64_t rows_per_cta, float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
   if (gate && *((volatile const int*)gate) == 0) return;
+  using C = TcCfg<N>;
   static_assert(N % 16 == 0 && N >= 32 && N <= 256, "UMMA N");
-  constexpr int A_FL = kTcKB * kTcM;  // floats per A hi (or lo) step buffer
-  constexpr int B_FL = kTcKB * N;
+  constexpr int KS = C::kStep;
   constexpr int LBO_A = kTcM / 8 * 32, LBO_B = N / 8 * 32;  // K-group (4 values) strides in floats
-  constexpr int NB_BLK = (kTcKB / 4) * (N / 4);              // 4x4 blocks of B per step
-  constexpr int B_PER_T = (NB_BLK + kTcThreads - 1) / kTcThreads;
-  constexpr int HALF = N / 2;                                // columns drained per thread
+  constexpr int NBLK_A = (KS / 4) * (kTcM / 4), NBLK = NBLK_A + (KS / 4) * (N / 4);
+  constexpr int QTR = N / 4;                                 // columns drained per thread
   constexpr uint32_t kCols = 2 * N <= 256 ? 256 : 512;       // TMEM: two N-column accumulators
-  static_assert((kTcKB / 4) * (kTcM / 4) == kTcThreads, "one A block per thread");
-  static_assert(HALF % 8 == 0, "drain granularity");
+  static_assert(QTR % 4 == 0, "drain granularity");
 
   extern __shared__ __align__(1024) float sm[];
-  // step buffer b: [A hi | A lo | B hi | B lo] at sm + b * STEP_FL
-  constexpr int STEP_FL = 2 * A_FL + 2 * B_FL;
-  __shared__ __align__(8) uint64_t mbar[2];  // step buffer b free again
-  __shared__ __align__(8) uint64_t cbar[2];  // chunk accumulator b complete
+  float* const raw0 = sm;                         // ring: slot i at raw0 + i * RAW_FL
+  float* const conv0 = sm + C::kRing * C::RAW_FL;  // buffer b at conv0 + b * CONV_FL
+  __shared__ __align__(8) uint64_t full[C::kRing];  // raw slot filled (tx bytes)
+  __shared__ __align__(8) uint64_t mbar[2];         // conv buffer b free again (MMAs done)
+  __shared__ __align__(8) uint64_t cbar[2];         // chunk accumulator b complete
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -178,12 +128,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
   }
   const int64_t a0 = (int64_t)ti * kTcM, b0 = (int64_t)tj * N;
+  const int a_cols = (int)(Ka - a0 < kTcM ? Ka - a0 : kTcM);  // valid columns of the tile
+  const int b_cols = (int)(Kb - b0 < N ? Kb - b0 : N);
   const int64_t r_begin = (int64_t)blockIdx.y * rows_per_cta;
   const int64_t r_end = r_begin + rows_per_cta < rows ? r_begin + rows_per_cta : rows;
-  const int64_t nst = r_end > r_begin ? (r_end - r_begin + kTcKB - 1) / kTcKB : 0;
-  const int64_t nch = (nst + kTcStepsPerChunk - 1) / kTcStepsPerChunk;
+  const int64_t nst = r_end > r_begin ? (r_end - r_begin + KS - 1) / KS : 0;
+  const int64_t nch = (nst + C::kStepsPerChunk - 1) / C::kStepsPerChunk;
 
   if (tid == 0) {
+    for (int i = 0; i < C::kRing; ++i) mbar_init(&full[i], 1);
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     mbar_init(&cbar[0], 1);
@@ -201,80 +154,103 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = tmem_base_s;
   const uint32_t idesc = umma_idesc(kTcM, N);
 
-  // operand columns of this thread's blocks: A block (kb_a, cb_a); B blocks f = tid + i * 256
-  const int kb_a = tid / (kTcM / 4), cb_a = tid % (kTcM / 4);
-  const float* Ab = A + a0;
-  const float* Bb = B + b0;
-  const int64_t a_cols = Ka - a0, b_cols = Kb - b0;
-  float4 va[4], vb[B_PER_T][4];
-  auto load_step = [&](int64_t k0) {
-    load_block(Ab, lda, a_cols, rs, k0, r_end, cb_a * 4, kb_a, va);
-#pragma unroll
-    for (int i = 0; i < B_PER_T; ++i) {
-      const int f = tid + i * kTcThreads;
-      const int kb = f / (N / 4), cb = f - kb * (N / 4);
-      if (f < NB_BLK) load_block(Bb, ldb, b_cols, nullptr, k0, r_end, cb * 4, kb, vb[i]);
-    }
+  // thread 0 fills raw slot (st % kRing) with the rows of step st: one TMA box per operand
+  // (rows past the tensor are zero-filled; rows past this CTA's range are zeroed when converted)
+  auto fill = [&](int64_t st) {
+    const int slot = (int)(st % C::kRing);
+    uint64_t* bar = &full[slot];
+    float* rawA = raw0 + slot * C::RAW_FL;
+    mbar_expect_tx(bar, (uint32_t)C::RAW_FL * 4);
+    const int r0 = (int)(r_begin + st * KS);
+    tma_2d(rawA, &tmA, (int)a0, r0, bar);
+    tma_2d(rawA + C::A_FL, &tmB, (int)b0, r0, bar);
   };
+  if (tid == 0)
+    for (int64_t st = 0; st < nst && st < C::kRing; ++st) fill(st);
 
-  float acc[HALF];
+  float acc[QTR];
 #pragma unroll
-  for (int q = 0; q < HALF; ++q) acc[q] = 0.f;
+  for (int q = 0; q < QTR; ++q) acc[q] = 0.f;
   const uint32_t lane_base = (uint32_t)(warp & 3) * 32;
-  const uint32_t col_half = (uint32_t)(warp >> 2) * HALF;
+  const uint32_t col_q = (uint32_t)(warp >> 2) * QTR;
   int64_t drained = 0;
   auto drain = [&](int64_t c) {
     mbar_wait(&cbar[c & 1], (uint32_t)((c >> 1) & 1));
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t base = tmem + (lane_base << 16) + (uint32_t)(c & 1) * N + col_half;
+    const uint32_t base = tmem + (lane_base << 16) + (uint32_t)(c & 1) * N + col_q;
 #pragma unroll
-    for (int q0 = 0; q0 < HALF; q0 += 32) {
+    for (int q0 = 0; q0 < QTR; q0 += 32) {
       uint32_t r[32];
 #pragma unroll
-      for (int q = 0; q < 32; q += 8)
-        if (q0 + q < HALF)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                       : "=r"(r[q]), "=r"(r[q + 1]), "=r"(r[q + 2]), "=r"(r[q + 3]), "=r"(r[q + 4]), "=r"(r[q + 5]),
-                         "=r"(r[q + 6]), "=r"(r[q + 7])
+      for (int q = 0; q < 32; q += 4)
+        if (q0 + q < QTR)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(r[q]), "=r"(r[q + 1]), "=r"(r[q + 2]), "=r"(r[q + 3])
                        : "r"(base + (uint32_t)(q0 + q)));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int q = 0; q < 32; ++q)
-        if (q0 + q < HALF) acc[q0 + q] += __uint_as_float(r[q]);
+        if (q0 + q < QTR) acc[q0 + q] += __uint_as_float(r[q]);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   };
 
-  if (nst > 0) load_step(r_begin);
+  // row scales of this thread's A block rows (threads < NBLK_A own one A block per step)
+  static_assert(NBLK_A <= kTcThreads, "one A block per thread");
+  float sc[4] = {1.f, 1.f, 1.f, 1.f};
+  auto load_scale = [&](int64_t st) {
+    if (!rs || tid >= NBLK_A) return;
+    const int64_t k0 = r_begin + st * KS;
+    const int kb = tid / (kTcM / 4);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sc[q] = k0 + kb * 4 + q < r_end ? __ldg(rs + k0 + kb * 4 + q) : 0.f;
+  };
+  if (nst > 0) load_scale(0);
+
   for (int64_t st = 0; st < nst; ++st) {
-    const int buf = (int)(st & 1);
+    const int buf = (int)(st & 1), slot = (int)(st % C::kRing);
+    const int64_t k0 = r_begin + st * KS;
+    const int nr = (int)(r_end - k0 < KS ? r_end - k0 : KS);
     if (st >= 2) mbar_wait(&mbar[buf], (uint32_t)(((st - 2) >> 1) & 1));  // MMAs of step st-2 done
     // the chunk finished two steps ago is complete too: drain it (its accumulator is next
     // written by chunk + 2, whose MMAs are issued after this step's __syncthreads)
-    if ((st % kTcStepsPerChunk) == 1 && st > kTcStepsPerChunk) drain(drained++);
-    float* const Ahi = sm + buf * STEP_FL;
-    float* const Alo = Ahi + A_FL;
-    float* const Bhi = Ahi + 2 * A_FL;
-    float* const Blo = Bhi + B_FL;
-    store_block<kTcM>(Ahi, Alo, kb_a, cb_a, va);
+    if ((st % C::kStepsPerChunk) == 1 && st > C::kStepsPerChunk) drain(drained++);
+    mbar_wait(&full[slot], (uint32_t)((st / C::kRing) & 1));  // raw rows of this step landed
+    {
+      const float* rawA = raw0 + slot * C::RAW_FL;
+      const float* rawB = rawA + C::A_FL;
+      float* const Ahi = conv0 + buf * C::CONV_FL;
+      float* const Alo = Ahi + C::A_FL;
+      float* const Bhi = Ahi + 2 * C::A_FL;
+      float* const Blo = Bhi + C::B_FL;
 #pragma unroll
-    for (int i = 0; i < B_PER_T; ++i) {
-      const int f = tid + i * kTcThreads;
-      const int kb = f / (N / 4), cb = f - kb * (N / 4);
-      if (f < NB_BLK) store_block<N>(Bhi, Blo, kb, cb, vb[i]);
+      for (int i = 0; i < (NBLK + kTcThreads - 1) / kTcThreads; ++i) {
+        const int f = tid + i * kTcThreads;
+        if (f < NBLK_A) {
+          const int kb = f / (kTcM / 4), cb = f - kb * (kTcM / 4);
+          convert_block<kTcM, kTcM>(rawA, Ahi, Alo, kb, cb, nr, a_cols, sc);
+        } else if (f < NBLK) {
+          const int g = f - NBLK_A;
+          const int kb = g / (N / 4), cb = g - kb * (N / 4);
+          const float one[4] = {1.f, 1.f, 1.f, 1.f};
+          convert_block<N, N>(rawB, Bhi, Blo, kb, cb, nr, b_cols, one);
+        }
+      }
     }
-    if (st + 1 < nst) load_step(r_begin + (st + 1) * kTcKB);  // in flight behind this step's MMAs
+    if (st + 1 < nst) load_scale(st + 1);  // row scales of the next step, in flight behind the MMAs
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
     __syncthreads();
+    // raw slot consumed by every thread: refill it with step st + kRing
     if (tid == 0) {
+      if (st + C::kRing < nst) fill(st + C::kRing);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t c = st / kTcStepsPerChunk;
+      const int64_t c = st / C::kStepsPerChunk;
       const uint32_t d = tmem + (uint32_t)(c & 1) * N;
-      const uint32_t ah = smem_u32(Ahi), al = smem_u32(Alo);
-      const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
-      const bool first = (st % kTcStepsPerChunk) == 0;
+      const uint32_t ah = smem_u32(conv0 + buf * C::CONV_FL), al = ah + C::A_FL * 4;
+      const uint32_t bh = ah + 2 * C::A_FL * 4, bl = bh + C::B_FL * 4;
+      const bool first = (st % C::kStepsPerChunk) == 0;
 #pragma unroll
-      for (int s = 0; s < kTcKB / 8; ++s) {
+      for (int s = 0; s < KS / 8; ++s) {
         // one MMA (K = 8) spans two K-groups
         const uint32_t ka = (uint32_t)(2 * s) * LBO_A * 4, kb = (uint32_t)(2 * s) * LBO_B * 4;  // bytes
         const uint64_t dah = umma_desc(ah + ka, LBO_A * 4, 128), dal = umma_desc(al + ka, LBO_A * 4, 128);
@@ -284,16 +260,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mma_tf32(d, dal, dbh, idesc, 1u);
       }
       umma_commit(&mbar[buf]);
-      if ((st % kTcStepsPerChunk) == kTcStepsPerChunk - 1 || st == nst - 1) umma_commit(&cbar[c & 1]);
+      if ((st % C::kStepsPerChunk) == C::kStepsPerChunk - 1 || st == nst - 1) umma_commit(&cbar[c & 1]);
     }
   }
   while (drained < nch) drain(drained++);
 
-  // epilogue: this thread's row of the tile, columns [col_half, col_half + HALF)
+  // epilogue: this thread's row of the tile, columns [col_q, col_q + QTR)
   const int64_t row = a0 + lane_base + lane;
-  float* w = ws + ((int64_t)blockIdx.y * ws_lda + row) * ws_ld + b0 + col_half;
+  float* w = ws + ((int64_t)blockIdx.y * ws_lda + row) * ws_ld + b0 + col_q;
 #pragma unroll
-  for (int q = 0; q < HALF; q += 4)
+  for (int q = 0; q < QTR; q += 4)
     *reinterpret_cast<float4*>(w + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -328,10 +304,14 @@ TcTiling tc_tiling(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num
 }
 
 template <int N>
-void tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t Ka, const float* rs, const float* B,
-                 int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws, int64_t ws_lda, int64_t ws_ld,
-                 const int* gate, cudaStream_t st) {
-  const size_t smem = (size_t)2 * (2 * kTcKB * kTcM + 2 * kTcKB * N) * sizeof(float);
+cudaError_t tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t Ka, const float* rs, const float* B,
+                        int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws, int64_t ws_lda,
+                        int64_t ws_ld, const int* gate, cudaStream_t st) {
+  CUtensorMap tmA, tmB;
+  if (!make_map(&tmA, A, rows, Ka, lda, kTcM, TcCfg<N>::kStep, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map(&tmB, B, rows, Kb, ldb, N, TcCfg<N>::kStep, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  const size_t smem = TcCfg<N>::smem_bytes();
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(tc_atb_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -339,8 +319,9 @@ void tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t Ka, con
   }
   dim3 grid((unsigned)t.tiles, (unsigned)t.parts);
   ++g_launches;
-  tc_atb_kernel<N><<<grid, kTcThreads, smem, st>>>(A, lda, Ka, rs, B, ldb, Kb, rows, t.ta, t.tb, symmetric ? 1 : 0,
+  tc_atb_kernel<N><<<grid, kTcThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta, t.tb, symmetric ? 1 : 0,
                                                    t.rows_per_cta, ws, ws_lda, ws_ld, gate);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -362,12 +343,11 @@ cudaError_t launch_tc_atb(const float* A, int64_t lda, int64_t Ka, const float* 
   *ws_ld = (int64_t)t.tb * t.n;
   *parts = t.parts;
   switch (t.n) {
-    case 128: tc_launch_n<128>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st); break;
-    case 160: tc_launch_n<160>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st); break;
-    case 208: tc_launch_n<208>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st); break;
-    default: tc_launch_n<256>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st); break;
+    case 128: return tc_launch_n<128>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st);
+    case 160: return tc_launch_n<160>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st);
+    case 208: return tc_launch_n<208>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st);
+    default: return tc_launch_n<256>(t, A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, *ws_lda, *ws_ld, gate, st);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace isvd
