@@ -223,10 +223,22 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   op->ws_wpad = wpad;
 }
 
-// Tensor cores for the fp32-class tall products (3xTF32, gram_tc.cu); ISVD_TC_GRAM=0 disables.
-bool use_tensor_cores(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t ldb) {
-  static const char* env = getenv("ISVD_TC_GRAM");
-  if (env && env[0] == '0') return false;
+// north_star: "Tensor cores are used only in the Gram contraction, and only if 3xTF32 meets the
+// tolerance."  By default the tcgen05 3xTF32 kernels therefore serve only the CholeskyQR Grams
+// Y^T Y (ISVD_TC_GRAM=0 turns that off too).  ISVD_TC_PRODUCTS=1 additionally routes the other
+// tall contractions -- the NC blocks X^T Z_j, the leaf GEMMs X G_j, the update Y R^-1 and the
+// final U, V -- through the same 3xTF32 kernels (a measured alternative).
+bool env_flag(const char* name, bool dflt) {
+  const char* v = getenv(name);
+  return v ? v[0] == '1' : dflt;
+}
+// read at every call (cheap) so a process can switch modes; the captured solver graph is keyed
+// on them (graph_key)
+bool tc_for_grams() { return env_flag("ISVD_TC_GRAM", true); }
+bool tc_for_products() { return env_flag("ISVD_TC_PRODUCTS", false); }
+
+bool use_tensor_cores(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t ldb, bool gram) {
+  if (!(gram ? tc_for_grams() : tc_for_products())) return false;
   return tc_atb_supported(rows, Ka, Kb, lda, ldb);
 }
 
@@ -236,7 +248,7 @@ bool use_tensor_cores(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t
 void atb_fp32(isvd_op op, int64_t rows, const float* A, int64_t lda, int64_t Ka, const float* row_scale,
               const float* B, int64_t ldb, int64_t Kb, bool symmetric, double* G, int64_t ldg, const int* gate) {
   isvd_ctx ctx = op->g->ctx;
-  if (use_tensor_cores(rows, Ka, Kb, lda, ldb)) {
+  if (use_tensor_cores(rows, Ka, Kb, lda, ldb, symmetric && A == B)) {
     int64_t ws_lda = 0, ws_ld = 0, parts = 0;
     float* ws32 = reinterpret_cast<float*>(op->atb_ws);
     CK(launch_tc_atb(A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, &ws_lda, &ws_ld, &parts,
@@ -249,14 +261,13 @@ void atb_fp32(isvd_op op, int64_t rows, const float* A, int64_t lda, int64_t Ka,
                 gate, ctx->stream, true));
 }
 
-// C[map(i), j] = alpha row_scale(i) (A B)[i, j], i < rows, j < N: tcgen05 3xTF32 for tall A
-// (gemm_tc.cu), else the SIMT fp32 kernel (dense.cu); ISVD_TC_GEMM=0 disables the former.
+// C[map(i), j] = alpha row_scale(i) (A B)[i, j], i < rows, j < N: the SIMT fp32 kernel (dense.cu),
+// or with ISVD_TC_PRODUCTS=1 the tcgen05 3xTF32 tall GEMM (gemm_tc.cu).
 void gemm_fp32(isvd_op op, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                int64_t rows, int64_t N, int64_t K, const float* row_scale, bool upper_tri_b, const int* gate,
                const int32_t* out_map = nullptr) {
   isvd_ctx ctx = op->g->ctx;
-  static const char* env = getenv("ISVD_TC_GEMM");
-  const bool tc = !(env && env[0] == '0') && tc_gemm_supported(rows, N, K, lda, ldc) &&
+  const bool tc = tc_for_products() && tc_gemm_supported(rows, N, K, lda, ldc) &&
                   tc_gemm_ws_floats(N, K) <= tc_gemm_ws_floats(op->ws_wpad, std::max<int64_t>(op->ws_wpad, op->d));
   if (tc)
     CK(launch_tc_gemm(A, lda, B, ldb, C, ldc, rows, N, K, row_scale, 1.f, gate, ctx->stream, out_map, op->bt_ws,
@@ -966,6 +977,7 @@ uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t 
   mix((uint64_t)p->k); mix((uint64_t)(uint32_t)p->oversampling); mix((uint64_t)p->power_iters); mix(p->seed);
   mix(p->flags); mix((uint64_t)(uintptr_t)p->omega); mix((uint64_t)l); mix((uint64_t)(uintptr_t)U);
   mix((uint64_t)ldu); mix((uint64_t)(uintptr_t)V); mix((uint64_t)ldv);
+  mix((uint64_t)tc_for_grams() | (uint64_t)tc_for_products() << 1);
   return h;
 }
 

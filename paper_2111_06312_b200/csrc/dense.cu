@@ -444,19 +444,20 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
 // Register-tiled SIMT contraction over a chunk of <= kF32ChunkRows rows, fp32 FMA
 // accumulation inside the chunk (relative error ~ sqrt(chunk) u_fp32 ~ 2e-6), fp32
 // partial tiles reduced in fp64 across chunks in a fixed order.  Thread (tx, ty) owns
-// rows ty*4 + 0..3 and columns {tx*4 + 0..3, BN/2 + tx*4 + 0..3} of a BM x BN tile, so
+// rows ty*TM + 0..TM-1 and columns {tx*4 + 0..3, BN/2 + tx*4 + 0..3} of a BM x BN tile, so
 // every shared-memory float4 read of a quarter-warp is conflict-free.  Tile shapes are
-// picked per call to avoid padding (d = 100, l = 400: 100 x 80 tiles, no waste).
+// picked per call by padding and register-tile size (d = 100, l = 400: 104 x 80, 8 x 8).
 constexpr int kF32ChunkRows = 1024;
 constexpr int kF32Stage = 16;
 
-template <int BM, int BN>
-__global__ void __launch_bounds__((BM / 4) * (BN / 8))
+template <int BM, int BN, int TM>
+__global__ void __launch_bounds__((BM / TM) * (BN / 8))
     atb_f32_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                    int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int tiles_b, int64_t rows_per_chunk,
                    float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
   if (gate && *((volatile const int*)gate) == 0) return;
-  constexpr int TY = BM / 4, TX = BN / 8, NT = TX * TY;
+  static_assert(TM == 4 || TM == 8, "rows per thread");
+  constexpr int TY = BM / TM, TX = BN / 8, NT = TX * TY;
   constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
   __shared__ __align__(16) float As[2][kF32Stage][BM];
   __shared__ __align__(16) float Bs[2][kF32Stage][BN];
@@ -508,9 +509,9 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 8))
       if (f < B4) *reinterpret_cast<float4*>(&Bs[buf][f / (BN / 4)][(f % (BN / 4)) * 4]) = pb[u];
     }
   };
-  float acc[4][8];
+  float acc[TM][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
   const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
@@ -524,13 +525,17 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 8))
     if (s + 1 < nst) load(r_begin + (s + 1) * kF32Stage);
 #pragma unroll
     for (int kk = 0; kk < kF32Stage; ++kk) {
-      const float4 va = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      float a[TM];
+#pragma unroll
+      for (int i = 0; i < TM; i += 4) {
+        const float4 va = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
+        a[i] = va.x; a[i + 1] = va.y; a[i + 2] = va.z; a[i + 3] = va.w;
+      }
       const float4 v0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
       const float4 v1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][BN / 2 + tx * 4]);
-      const float a[4] = {va.x, va.y, va.z, va.w};
       const float b[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
@@ -539,8 +544,8 @@ __global__ void __launch_bounds__((BM / 4) * (BN / 8))
   }
   float* W = ws + (int64_t)blockIdx.y * ws_lda * ws_ld;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float* w = W + (a0 + ty * 4 + i) * ws_ld + b0;
+  for (int i = 0; i < TM; ++i) {
+    float* w = W + (a0 + ty * TM + i) * ws_ld + b0;
     *reinterpret_cast<float4*>(w + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
     *reinterpret_cast<float4*>(w + BN / 2 + tx * 4) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
   }
@@ -563,20 +568,23 @@ __global__ void atb_f32_reduce_kernel(const float* __restrict__ ws, int64_t ws_l
 }
 
 struct F32Tiling {
-  int bm, bn;
+  int bm, bn, tm;
   int64_t ta, tb, chunk_rows, chunks;
 };
 
 F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
-  const int cand[3][2] = {{64, 64}, {100, 80}, {128, 128}};
-  F32Tiling t{64, 64, 0, 0, 0, 0};
-  int64_t best = -1;
+  // {BM, BN, TM}: 8 x 8 register tiles halve the shared-memory reads per FMA (the 4 x 8 tiles
+  // are shared-memory-bound), so they win unless their padding costs more than ~1/3
+  const int cand[5][3] = {{64, 64, 4}, {100, 80, 4}, {128, 128, 4}, {104, 80, 8}, {128, 128, 8}};
+  F32Tiling t{64, 64, 4, 0, 0, 0, 0};
+  double best = -1;
   for (auto& c : cand) {
-    int64_t area = round_up(Ka, c[0]) * round_up(Kb, c[1]);
-    if (best < 0 || area < best || (area == best && c[0] * c[1] > t.bm * t.bn)) {
-      best = area;
+    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (c[2] == 8 ? 0.65 : 1.0);
+    if (best < 0 || cost < best) {
+      best = cost;
       t.bm = c[0];
       t.bn = c[1];
+      t.tm = c[2];
     }
   }
   t.ta = ceil_div(Ka, t.bm);
@@ -637,15 +645,16 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     if (rows > 0) {
       dim3 grid((unsigned)(t.ta * t.tb), (unsigned)t.chunks);
       ++g_launches;
-      if (t.bm == 64)
-        atb_f32_kernel<64, 64><<<grid, 128, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows,
-                                                     ws32, ws_lda, ws_ld, gate);
-      else if (t.bm == 100)
-        atb_f32_kernel<100, 80><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
-                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
-      else
-        atb_f32_kernel<128, 128><<<grid, 512, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
-                                                       t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+#define ISVD_ATB_F32(BM_, BN_, TM_)                                                                     \
+  if (t.bm == BM_ && t.bn == BN_ && t.tm == TM_)                                                         \
+    atb_f32_kernel<BM_, BN_, TM_><<<grid, (BM_ / TM_) * (BN_ / 8), 0, st>>>(                              \
+        A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+      ISVD_ATB_F32(64, 64, 4)
+      else ISVD_ATB_F32(100, 80, 4)
+      else ISVD_ATB_F32(128, 128, 4)
+      else ISVD_ATB_F32(104, 80, 8)
+      else ISVD_ATB_F32(128, 128, 8)
+#undef ISVD_ATB_F32
     } else {
       cudaMemsetAsync(ws32, 0, sizeof(float) * ws_lda * ws_ld, st);
     }

@@ -311,3 +311,27 @@ def test_distributed_schedule_world1_nccl(i):
 
     Qc = philox_omega(7, 0, op.c_rows(), sp["l"])
     assert rel_fro(_to_np(op.matmul(torch.from_numpy(Qc).cuda())), ref.matmul(Qc.astype(np.float64))) <= PROD_TOL
+
+
+# ------------------------------------------------ tensor-core products (opt-in mode)
+
+
+@pytest.mark.skipif(__import__("os").environ.get("ISVD_TC_PRODUCTS") == "1", reason="already the child run")
+def test_tc_products_mode_parity():
+    """ISVD_TC_PRODUCTS=1 routes X^T Z_j, X G_j, Y R^-1 and the final U, V through the tcgen05
+    3xTF32 kernels (the default keeps tensor cores to the Gram, as north_star says).  Config 2
+    (NC, n = 169343 >= the tensor-core row threshold) must meet the same parity bars: the
+    product and isvd tests are re-run in a child process with the flag set (it is read once per
+    process by the library)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.abspath(__file__)
+    ids = [f"{here}::test_products[omega-2]", f"{here}::test_products[orthonormal-2]",
+           f"{here}::test_isvd_parity[2]", f"{here}::test_distributed_schedule_world1_nccl[2]"]
+    env = dict(os.environ, ISVD_TC_PRODUCTS="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
+                       cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "4 passed" in r.stdout, r.stdout[-2000:]
