@@ -80,7 +80,7 @@ struct SolverWs {
   int64_t key_l = -1, key_k = -1;
   std::vector<void*> allocs;
   float *Qc = nullptr, *Qc2 = nullptr, *Yr = nullptr, *Yr2 = nullptr, *Rinv32 = nullptr, *Ub = nullptr,
-        *Vb = nullptr, *Utmp = nullptr, *Vtmp = nullptr, *sgn = nullptr;
+        *Vb = nullptr, *Utmp = nullptr, *Vtmp = nullptr, *sgn = nullptr, *Rfold = nullptr, *Ub2 = nullptr;
   double *gram = nullptr, *Ra = nullptr, *Rb = nullptr, *Rc = nullptr, *Rab = nullptr, *Rfin = nullptr,
          *chol_ws = nullptr, *jac_ws = nullptr, *sigma = nullptr, *cand = nullptr, *cand_all = nullptr,
          *absmax_ws = nullptr;
@@ -1003,6 +1003,8 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
   s.Yr = f(rr * ld);
   s.Yr2 = f(rr * ld);
   s.Rinv32 = f(ld * ld);
+  s.Rfold = f(ld * ld);
+  s.Ub2 = f(l * ldk);
   s.Ub = f(l * ldk);
   s.Vb = f(l * ldk);
   s.Utmp = f(rr * ldk);
@@ -1029,7 +1031,7 @@ enum GramMode { kGramF64 = 0, kGramFp32 = 1 };
 
 // One Cholesky pass (Alg. 2 right): G = Y^T Y (all-reduced when row-partitioned), R = chol(G), Yout = Y R^-1.
 void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distributed, int64_t l, double* R64,
-              GramMode mode, bool force_fail, const int* gate) {
+              GramMode mode, bool force_fail, const int* gate, const int* gemm_gate = nullptr) {
   isvd_ctx ctx = op->g->ctx;
   SolverWs& s = op->sws;
   const int64_t ld = round_up(l, 4);
@@ -1040,7 +1042,7 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
                   ctx->stream, false));
   if (distributed) allreduce_f64(ctx, s.gram, (size_t)l * l);
   CK(launch_chol_inv(s.gram, l, (int)l, ld, s.Rinv32, R64, s.chol_ws, ctx->status, force_fail, gate, ctx->stream));
-  gemm_fp32(op, Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, true, gate);
+  gemm_fp32(op, Y, ld, s.Rinv32, ld, Yout, ld, rows, ld, l, nullptr, true, gemm_gate ? gemm_gate : gate);
 }
 
 // CholeskyQR2 (+ a third, device-gated pass after a shifted factorisation): result in Y.
@@ -1092,6 +1094,27 @@ isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* 
 // ------------------------------------------------------------------ the solver body
 namespace {
 
+// CholeskyQR2 of a tall Y whose orthonormal factor is only ever consumed through products with
+// small matrices (M^T Q, then Q U_B): the second pass's update Q2 = Q1 R2^-1 -- a full tall GEMM
+// -- is not formed; Q1 is returned (in Y2) with Rfold = R2^-1, and consumers apply Rfold on the
+// small side: M^T Q2 = (M^T Q1) Rfold, Q2 U_B = Q1 (Rfold U_B).  Exact in exact arithmetic;
+// R2 = I + O(eps1) is perfectly conditioned, so nothing is lost in floating point.
+// If the device flags a shifted factorisation, Q2 is formed after all (gated GEMM), the shifted
+// third pass runs on it into Y2, and Rfold = I.  Returns the buffer holding the tall factor.
+float* cqr2_deferred(isvd_op op, float* Y, float* Y2, int64_t rows, int64_t l, bool force_fail, bool exact_gram) {
+  isvd_ctx ctx = op->g->ctx;
+  SolverWs& s = op->sws;
+  const int64_t ld = round_up(l, 4);
+  int* gate = &ctx->status->need_extra_pass;
+  CK(cudaMemsetAsync(gate, 0, sizeof(int), ctx->stream));
+  cqr_pass(op, Y, Y2, rows, true, l, nullptr, exact_gram ? kGramF64 : kGramFp32, force_fail, nullptr);
+  // pass 2: Gram + Cholesky of Q1; Q2 = Q1 R2^-1 only if a third pass will need it
+  cqr_pass(op, Y2, Y, rows, true, l, nullptr, kGramFp32, false, nullptr, gate);
+  CK(launch_select_rfold(s.Rinv32, s.Rfold, (int)l, ld, gate, ctx->stream));
+  cqr_pass(op, Y, Y2, rows, true, l, nullptr, kGramF64, false, gate);
+  return Y2;
+}
+
 void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int64_t ldu, float* V, int64_t ldv) {
   isvd_graph g = op->g;
   isvd_ctx ctx = g->ctx;
@@ -1110,25 +1133,51 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   } else {
     CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, omap, ctx->stream));
   }
+  // r-side orthonormalisation: with a small c side (NC) the second CholeskyQR update is folded
+  // into the small products (cqr2_deferred); otherwise the plain CholeskyQR2
+  const bool fold = !ne && 4 * cr <= g->n;  // NC: c = d (L + 1) rows, replicated on every rank
+  float* q_r = s.Yr;  // buffer holding the r-side orthonormal factor (times Rfold when folding)
+  auto orth_r = [&](bool exact) {
+    if (fold) {
+      q_r = cqr2_deferred(op, s.Yr, s.Yr2, rr, l, force, exact);
+    } else {
+      cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr, exact);
+      q_r = s.Yr;
+    }
+  };
+  // W = M^T Q into Qc (Q = q_r Rfold when folding)
+  auto mt_q = [&]() {
+    if (fold) {
+      op_matmul_T(op, q_r, ld, s.Qc2, ld, ld, false);
+      gemm_fp32(op, s.Qc2, ld, s.Rfold, ld, s.Qc, ld, cr, ld, l, nullptr, false, nullptr);
+    } else {
+      op_matmul_T(op, q_r, ld, s.Qc, ld, ld, false);
+    }
+  };
   // Alg. 1 lines 5-8
   for (int it = 0; it < p->power_iters; ++it) {
-    op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);                // M Q       (r x l)
-    cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr, it == 0);  // orthonorm
-    op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);              // M^T Q     (c x l)
-    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr, true);      // orthonorm
+    op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);            // M Q       (r x l)
+    orth_r(it == 0);                                         // orthonorm
+    mt_q();                                                  // M^T Q     (c x l)
+    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr, true);  // orthonorm
   }
   // Alg. 1 line 9: Q <- orthonorm(M Q)
   op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);
-  cqr2(op, s.Yr, s.Yr2, rr, true, l, force, nullptr, p->power_iters == 0);
+  orth_r(p->power_iters == 0);
   // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
-  op_matmul_T(op, s.Yr, ld, s.Qc, ld, ld, false);
+  mt_q();
   cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin, true);
   // Alg. 1 line 11: svd(B) with B = R^T Q_W^T -> one-sided Jacobi on R^T
   CK(launch_jacobi_svd(s.Rfin, (int)l, (int)k, ldk, s.sigma, s.Ub, s.Vb, s.jac_ws, ctx->status, ctx->num_sms,
                        ctx->stream));
   // Alg. 1 line 12: U = Q U_B;  V = Q_W V_B;  truncate to k
   // (relabelled graphs: rows go back to the caller's order here)
-  gemm_fp32(op, s.Yr, ld, s.Ub, ldk, U, ldu, rr, ldk, l, nullptr, false, nullptr, g->new2old);
+  const float* ub = s.Ub;
+  if (fold) {  // U = (Q1 Rfold) U_B = Q1 (Rfold U_B)
+    gemm_fp32(op, s.Rfold, ld, s.Ub, ldk, s.Ub2, ldk, l, ldk, l, nullptr, false, nullptr);
+    ub = s.Ub2;
+  }
+  gemm_fp32(op, q_r, ld, ub, ldk, U, ldu, rr, ldk, l, nullptr, false, nullptr, g->new2old);
   gemm_fp32(op, s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, false, nullptr, ne ? g->new2old : nullptr);
   // sign rule (reading O9)
   CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));

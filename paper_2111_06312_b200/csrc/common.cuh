@@ -142,6 +142,8 @@ int64_t tc_atb_ws_floats(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, i
 cudaError_t launch_tc_atb(const float* A, int64_t lda, int64_t Ka, const float* row_scale, const float* B,
                           int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws32, int64_t* ws_lda,
                           int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st);
+// out = *flag ? I : Rinv  (l x l, ld x ld fp32; the deferred CholeskyQR2 factor)
+cudaError_t launch_select_rfold(const float* Rinv, float* out, int l, int64_t ld, const int* flag, cudaStream_t st);
 // out32[i, j] = (float) G[i, j]
 cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t ldo, int64_t rows,
                               int64_t cols, cudaStream_t st);

@@ -347,6 +347,19 @@ __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __res
   }
 }
 
+// Rfold = flag ? I : Rinv (l x l in an ld x ld fp32 buffer; padding zero): the factor a deferred
+// CholeskyQR2 leaves for its consumers (capi.cpp cqr2_deferred).
+__global__ void select_rfold_kernel(const float* __restrict__ Rinv, float* __restrict__ out, int l, int64_t ld,
+                                    const int* flag) {
+  const bool ident = *((volatile const int*)flag) != 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ld * ld; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ld, j = e - (e / ld) * ld;
+    float v = 0.f;
+    if (i < l && j < l) v = ident ? (i == j ? 1.f : 0.f) : Rinv[e];
+    out[e] = v;
+  }
+}
+
 // ------------------------------------------------------------ sign rule
 constexpr int64_t kAbsmaxRows = 4096;
 
@@ -749,6 +762,11 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
     Jout = J;
   }
   ++g_launches; jacobi_finish_kernel<<<1, 1024, 0, st>>>(Aout, Jout, l, k, ldk, sig, sigma_k, Ub, Vb, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_rfold(const float* Rinv, float* out, int l, int64_t ld, const int* flag, cudaStream_t st) {
+  ++g_launches; select_rfold_kernel<<<grid_for(ld * ld, 256, 148), 256, 0, st>>>(Rinv, out, l, ld, flag);
   return cudaGetLastError();
 }
 

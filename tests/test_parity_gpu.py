@@ -189,6 +189,16 @@ def test_cholesky_fallback_still_in_parity(ctx):
     _check_isvd(res, _oracle_result(0), sp["k"], "cfg0/fallback")
 
 
+def test_cholesky_fallback_nc_deferred_update_in_parity(ctx):
+    """NC (small c side): the r-side CholeskyQR2 defers its second update into the small
+    products (Rfold); a forced shifted factorisation must form Q2, run the third pass and
+    switch Rfold to I -- and still meet parity."""
+    op, _, cfg, sp = _op(ctx, 2)
+    res = op.svd(sp["k"], -1 if cfg["p"] is None else cfg["p"], sp["q"], sp["seed"], force_chol_fail=True)
+    assert res.chol_fallbacks > 0
+    _check_isvd(res, _oracle_result(2), sp["k"], "cfg2/fallback")
+
+
 # ------------------------------------------------------------ edge cases
 
 
