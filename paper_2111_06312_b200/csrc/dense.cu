@@ -450,14 +450,16 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
 constexpr int kF32ChunkRows = 1024;
 constexpr int kF32Stage = 16;
 
-template <int BM, int BN, int TM>
-__global__ void __launch_bounds__((BM / TM) * (BN / 8))
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
     atb_f32_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                    int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int tiles_b, int64_t rows_per_chunk,
                    float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
   if (gate && *((volatile const int*)gate) == 0) return;
   static_assert(TM == 4 || TM == 8, "rows per thread");
-  constexpr int TY = BM / TM, TX = BN / 8, NT = TX * TY;
+  static_assert(TN == 8 || TN == 16, "columns per thread");
+  constexpr int TY = BM / TM, TX = BN / TN, NT = TX * TY;
+  constexpr int QN = TN / 4, CS = BN / QN;  // thread column groups: tx*4 + q*CS, q < QN
   constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
   __shared__ __align__(16) float As[2][kF32Stage][BM];
   __shared__ __align__(16) float Bs[2][kF32Stage][BN];
@@ -509,11 +511,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / 8))
       if (f < B4) *reinterpret_cast<float4*>(&Bs[buf][f / (BN / 4)][(f % (BN / 4)) * 4]) = pb[u];
     }
   };
-  float acc[TM][8];
+  float acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
   const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
   if (nst > 0) {
     load(r_begin);
@@ -531,13 +533,16 @@ __global__ void __launch_bounds__((BM / TM) * (BN / 8))
         const float4 va = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
         a[i] = va.x; a[i + 1] = va.y; a[i + 2] = va.z; a[i + 3] = va.w;
       }
-      const float4 v0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-      const float4 v1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][BN / 2 + tx * 4]);
-      const float b[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float b[TN];
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(&Bs[buf][kk][q * CS + tx * 4]);
+        b[4 * q] = v.x; b[4 * q + 1] = v.y; b[4 * q + 2] = v.z; b[4 * q + 3] = v.w;
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     if (s + 1 < nst) store(buf ^ 1);
     __syncthreads();
@@ -546,8 +551,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / 8))
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     float* w = W + (a0 + ty * TM + i) * ws_ld + b0;
-    *reinterpret_cast<float4*>(w + tx * 4) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-    *reinterpret_cast<float4*>(w + BN / 2 + tx * 4) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+#pragma unroll
+    for (int q = 0; q < QN; ++q)
+      *reinterpret_cast<float4*>(w + q * CS + tx * 4) =
+          make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
   }
 }
 
@@ -568,23 +575,28 @@ __global__ void atb_f32_reduce_kernel(const float* __restrict__ ws, int64_t ws_l
 }
 
 struct F32Tiling {
-  int bm, bn, tm;
+  int bm, bn, tm, tn;
   int64_t ta, tb, chunk_rows, chunks;
 };
 
 F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   // {BM, BN, TM}: 8 x 8 register tiles halve the shared-memory reads per FMA (the 4 x 8 tiles
   // are shared-memory-bound), so they win unless their padding costs more than ~1/3
-  const int cand[5][3] = {{64, 64, 4}, {100, 80, 4}, {128, 128, 4}, {104, 80, 8}, {128, 128, 8}};
-  F32Tiling t{64, 64, 4, 0, 0, 0, 0};
+  // {BM, BN, TM, TN}; cost = padded area x shared-memory floats per FMA ((TM + TN) / (TM TN)):
+  // on B200 (128 FP32 lanes, 128 B/clk of shared memory per SM) small register tiles are
+  // shared-memory-bound.  (8 x 16 tiles need 255 registers; at 2 CTAs per SM they measured
+  // slower than 8 x 8 -- 0.95 vs 0.88 s per config-4 isvd -- and are not offered.)
+  const int cand[5][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8}};
+  F32Tiling t{64, 64, 4, 8, 0, 0, 0, 0};
   double best = -1;
   for (auto& c : cand) {
-    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (c[2] == 8 ? 0.65 : 1.0);
+    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (double)(c[2] + c[3]) / (c[2] * c[3]);
     if (best < 0 || cost < best) {
       best = cost;
       t.bm = c[0];
       t.bn = c[1];
       t.tm = c[2];
+      t.tn = c[3];
     }
   }
   t.ta = ceil_div(Ka, t.bm);
@@ -645,15 +657,15 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     if (rows > 0) {
       dim3 grid((unsigned)(t.ta * t.tb), (unsigned)t.chunks);
       ++g_launches;
-#define ISVD_ATB_F32(BM_, BN_, TM_)                                                                     \
-  if (t.bm == BM_ && t.bn == BN_ && t.tm == TM_)                                                         \
-    atb_f32_kernel<BM_, BN_, TM_><<<grid, (BM_ / TM_) * (BN_ / 8), 0, st>>>(                              \
+#define ISVD_ATB_F32(BM_, BN_, TM_, TN_)                                                                \
+  if (t.bm == BM_ && t.bn == BN_ && t.tm == TM_ && t.tn == TN_)                                          \
+    atb_f32_kernel<BM_, BN_, TM_, TN_><<<grid, (BM_ / TM_) * (BN_ / TN_), 0, st>>>(                       \
         A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows, ws32, ws_lda, ws_ld, gate);
-      ISVD_ATB_F32(64, 64, 4)
-      else ISVD_ATB_F32(100, 80, 4)
-      else ISVD_ATB_F32(128, 128, 4)
-      else ISVD_ATB_F32(104, 80, 8)
-      else ISVD_ATB_F32(128, 128, 8)
+      ISVD_ATB_F32(64, 64, 4, 8)
+      else ISVD_ATB_F32(100, 80, 4, 8)
+      else ISVD_ATB_F32(128, 128, 4, 8)
+      else ISVD_ATB_F32(104, 80, 8, 8)
+      else ISVD_ATB_F32(128, 128, 8, 8)
 #undef ISVD_ATB_F32
     } else {
       cudaMemsetAsync(ws32, 0, sizeof(float) * ws_lda * ws_ld, st);
