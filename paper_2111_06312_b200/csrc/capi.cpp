@@ -694,10 +694,14 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     // caller-ordered input/output is mapped at the boundary (X, Omega, U, V, matmul I/O).
     // The order is computed on the host from the degrees; the index renaming runs on the GPU.
     if (relabel) {
+      // stable counting sort by decreasing degree: O(n + max degree)
       std::vector<int32_t> order(n_local), new_of_old(n_local);
-      for (int64_t i = 0; i < n_local; ++i) order[i] = (int32_t)i;
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int32_t a, int32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+      int64_t dmax = 0;
+      for (int64_t i = 0; i < n_local; ++i) dmax = std::max(dmax, rp[i + 1] - rp[i]);
+      std::vector<int64_t> start(dmax + 2, 0);
+      for (int64_t i = 0; i < n_local; ++i) ++start[dmax - (rp[i + 1] - rp[i]) + 1];
+      for (int64_t b = 1; b <= dmax + 1; ++b) start[b] += start[b - 1];
+      for (int64_t i = 0; i < n_local; ++i) order[start[dmax - (rp[i + 1] - rp[i])]++] = (int32_t)i;
       for (int64_t t = 0; t < n_local; ++t) new_of_old[order[t]] = (int32_t)t;
       std::vector<int64_t> rp2(n_local + 1);
       rp2[0] = 0;
