@@ -10,6 +10,8 @@
 //                once when staged in shared memory, fp64 FMA, deterministic
 //                fixed-order reduction of the per-CTA partials (no atomics).
 //  K15 colsum    1^T Q in fp64 for the rank-1 term of Eq. 3.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace isvd {
@@ -318,6 +320,120 @@ __global__ void __launch_bounds__(ATB_THREADS)
       if constexpr (sizeof(S) == 8) v = acc[i][j];
       else v = accs[i * 8 + j][tid];
       W[(a0 + tmap(ty, i)) * ws_ld + b0 + tmap(tx, j)] = v;
+    }
+}
+
+// Exact fp64 A^T diag(s) B on the FP64 tensor cores (mma.sync m8n8k4 f64): the product of two
+// fp32 values is exact in fp64 and the sums are fp64, as in atb_kernel<double>, whose FMA form is
+// bound by shared-memory reads (8x8 fp64 fragments: 128 B per 64 DFMA).  Same tiles, chunks and
+// workspace layout as atb_kernel (64 x 64 output tile per CTA, upper tiles when symmetric, one
+// fp64 partial tile per row chunk, reduced by atb_reduce_kernel).  4 warps, each a 32 x 32 quarter
+// as 4 x 4 MMA tiles of 8 x 8; operands staged as fp32 (row stride 72: the fragment loads of a
+// warp hit 32 distinct banks) and widened to fp64 in registers.
+constexpr int ATBD_THREADS = 128;
+constexpr int ATBD_LD = ATB_T + 8;
+
+ISVD_DEVICE void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(ATBD_THREADS)
+    atb_dmma_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                    int64_t rows, int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric,
+                    int tiles_a, int tiles_b, int64_t rows_per_chunk, double* __restrict__ ws, int64_t ws_ld,
+                    const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  __shared__ __align__(16) float As[2][ATB_R][ATBD_LD];
+  __shared__ __align__(16) float Bs[2][ATB_R][ATBD_LD];
+  int ti = 0, tj = 0;
+  {
+    int t = blockIdx.x;
+    if (symmetric) {
+      while (t >= tiles_a - ti) { t -= tiles_a - ti; ++ti; }
+      tj = ti + t;
+    } else {
+      ti = t / tiles_b;
+      tj = t - ti * tiles_b;
+    }
+  }
+  const int64_t a0 = (int64_t)ti * ATB_T, b0 = (int64_t)tj * ATB_T;
+  const int64_t chunk = blockIdx.y;
+  const int64_t r_begin = chunk * rows_per_chunk;
+  const int64_t r_end = r_begin + rows_per_chunk < rows ? r_begin + rows_per_chunk : rows;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  // staging: 16 rows x 64 columns = 256 float4 per operand, 2 per thread
+  float4 pa[2], pb[2];
+  auto load = [&](int64_t r0) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int f = tid + u * ATBD_THREADS;
+      const int rr = f >> 4, cc = (f & 15) * 4;
+      const int64_t gr = r0 + rr;
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
+      if (gr < r_end) {
+        if (a0 + cc < Ka) va = __ldg(reinterpret_cast<const float4*>(A + gr * lda + a0 + cc));
+        if (b0 + cc < Kb) vb = __ldg(reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc));
+        if (row_scale) {
+          const float sc = __ldg(row_scale + gr);
+          vb.x *= sc; vb.y *= sc; vb.z *= sc; vb.w *= sc;
+        }
+      }
+      pa[u] = va;
+      pb[u] = vb;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int f = tid + u * ATBD_THREADS;
+      const int rr = f >> 4, cc = (f & 15) * 4;
+      *reinterpret_cast<float4*>(&As[buf][rr][cc]) = pa[u];
+      *reinterpret_cast<float4*>(&Bs[buf][rr][cc]) = pb[u];
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t nst = (r_end - r_begin + ATB_R - 1) / ATB_R;
+  if (nst > 0) {
+    load(r_begin);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t st = 0; st < nst; ++st) {
+    const int buf = (int)(st & 1);
+    if (st + 1 < nst) load(r_begin + (st + 1) * ATB_R);
+#pragma unroll
+    for (int k0 = 0; k0 < ATB_R; k0 += 4) {
+      // A fragment (8 x 4, row): A[m = g][k = q] = Y[k0 + q][col + g]; B (4 x 8, col): B[k = q][n = g]
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        fa[i] = (double)As[buf][k0 + q][wm * 32 + i * 8 + g];
+        fb[i] = (double)Bs[buf][k0 + q][wn * 32 + i * 8 + g];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    if (st + 1 < nst) store(buf ^ 1);
+    __syncthreads();
+  }
+  // D[m = g][n = 2 q + {0, 1}] of tile (i, j) -> ws[chunk][a][b]
+  double* W = ws + chunk * (int64_t)((Ka + ATB_T - 1) / ATB_T * ATB_T) * ws_ld;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = a0 + wm * 32 + i * 8 + g, c = b0 + wn * 32 + j * 8 + 2 * q;
+      *reinterpret_cast<double2*>(&W[r * ws_ld + c]) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
 }
 
@@ -645,6 +761,12 @@ int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   return f64_path > f32_path ? f64_path : f32_path;
 }
 
+// the exact fp64 Grams on the FP64 tensor cores (mma.sync f64) unless ISVD_DMMA=0
+static bool atb_dmma_enabled() {
+  const char* v = getenv("ISVD_DMMA");
+  return !(v && v[0] == '0');
+}
+
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka, int64_t Kb,
                        const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg, float* out32,
                        int64_t ld32, int num_sms, const int* gate, cudaStream_t st,
@@ -687,6 +809,9 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     if (f32_stage)
       atb_kernel<float><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
                                                       (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
+    else if (atb_dmma_enabled())
+      atb_dmma_kernel<<<grid, ATBD_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
+                                                     (int)ta, (int)tb, rpc, ws, ws_ld, gate);
     else
       atb_kernel<double><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
                                                        (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
