@@ -22,6 +22,31 @@ namespace {
 // shared-memory float4 read of a quarter-warp covers 128 contiguous bytes (no bank conflicts).
 // A is stored transposed with 4 floats of padding per k-row so the transposing stores do
 // not conflict either.  __launch_bounds__(., 2): <= 128 registers, two CTAs per SM.
+// Thread -> (tx, ty) of a register-tiled kernel whose thread reads B float4 tx*4 (and A
+// float4 ty*4) of each smem row.  A quarter-warp's 8 float4 reads must hit 8 distinct 16-byte
+// bank groups: with TX a multiple of 8 the plain tid % TX mapping does that; with TX = 10 no
+// cyclic window of 8 consecutive tx can (tx and tx + 8 share banks), so the first 8 TY threads
+// take tx = 0..7 (one ty per quarter-warp) and the last 2 TY take tx = 8, 9 (four ty per
+// quarter-warp: 2 distinct B and 4 distinct A float4s).
+template <int TX>
+ISVD_DEVICE void thread_xy(int tid, int* tx, int* ty) {
+  if constexpr (TX % 8 == 0 || TX < 8) {
+    *tx = tid % TX;
+    *ty = tid / TX;
+  } else {
+    static_assert(TX == 10, "tile width");
+    const int ty_n = blockDim.x / TX;
+    if (tid < 8 * ty_n) {
+      *tx = tid & 7;
+      *ty = tid >> 3;
+    } else {
+      const int t = tid - 8 * ty_n;
+      *tx = 8 + (t & 1);
+      *ty = t >> 1;
+    }
+  }
+}
+
 template <int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
     gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
@@ -35,7 +60,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN];
   const int tid = threadIdx.x;
-  const int tx = tid % TX, ty = tid / TX;
+  int tx, ty;
+  thread_xy<TX>(tid, &tx, &ty);
   const int64_t m0 = (int64_t)blockIdx.y * BM;
   const int64_t n0 = (int64_t)blockIdx.x * BN;
   int64_t kend = K;
@@ -579,7 +605,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
   __shared__ __align__(16) float As[2][kF32Stage][BM];
   __shared__ __align__(16) float Bs[2][kF32Stage][BN];
-  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  const int tid = threadIdx.x;
+  int tx, ty;
+  thread_xy<TX>(tid, &tx, &ty);
   const int ti = blockIdx.x / tiles_b, tj = blockIdx.x - ti * tiles_b;
   const int64_t a0 = (int64_t)ti * BM, b0 = (int64_t)tj * BN;
   const int64_t r_begin = (int64_t)blockIdx.y * rows_per_chunk;
