@@ -592,6 +592,17 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
 constexpr int kF32ChunkRows = 1024;
 constexpr int kF32Stage = 16;
 
+// 16-byte asynchronous global -> shared copy (LDGSTS); src_bytes = 0 zero-fills
+ISVD_DEVICE void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+ISVD_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+ISVD_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     atb_f32_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
@@ -603,8 +614,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   constexpr int TY = BM / TM, TX = BN / TN, NT = TX * TY;
   constexpr int QN = TN / 4, CS = BN / QN;  // thread column groups: tx*4 + q*CS, q < QN
   constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
-  __shared__ __align__(16) float As[2][kF32Stage][BM];
-  __shared__ __align__(16) float Bs[2][kF32Stage][BN];
+  // cp.async ring depth: 3 stages where they fit the 48 KB of static shared memory
+  constexpr int kF32Ring = 3 * (kF32Stage * (BM + BN) + kF32Stage) * 4 <= 48 * 1024 ? 3 : 2;
+  __shared__ __align__(16) float As[kF32Ring][kF32Stage][BM];
+  __shared__ __align__(16) float Bs[kF32Ring][kF32Stage][BN];
+  __shared__ __align__(16) float Ss[kF32Ring][kF32Stage];  // row scales of the stage (applied to A)
   const int tid = threadIdx.x;
   int tx, ty;
   thread_xy<TX>(tid, &tx, &ty);
@@ -612,47 +626,28 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const int64_t a0 = (int64_t)ti * BM, b0 = (int64_t)tj * BN;
   const int64_t r_begin = (int64_t)blockIdx.y * rows_per_chunk;
   const int64_t r_end = r_begin + rows_per_chunk < rows ? r_begin + rows_per_chunk : rows;
-  float4 pa[(A4 + NT - 1) / NT], pb[(B4 + NT - 1) / NT];
-  auto load = [&](int64_t r0) {
-#pragma unroll
-    for (int u = 0; u < (A4 + NT - 1) / NT; ++u) {
-      int f = tid + u * NT;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  // issue the copies of stage s (rows r_begin + 16 s ..) into ring slot s % kF32Ring; rows and
+  // columns outside the operands are zero-filled
+  auto issue = [&](int64_t s) {
+    const int slot = (int)(s % kF32Ring);
+    const int64_t r0 = r_begin + s * kF32Stage;
+    for (int f = tid; f < A4 + B4; f += NT) {
       if (f < A4) {
-        int rr = f / (BM / 4), cc = (f % (BM / 4)) * 4;
-        int64_t gr = r0 + rr;
-        if (gr < r_end && a0 + cc < Ka) v = __ldg(reinterpret_cast<const float4*>(A + gr * lda + a0 + cc));
+        const int rr = f / (BM / 4), cc = (f % (BM / 4)) * 4;
+        const int64_t gr = r0 + rr;
+        const bool ok = gr < r_end && a0 + cc < Ka;
+        cp_async16(&As[slot][rr][cc], ok ? A + gr * lda + a0 + cc : A, ok ? 16 : 0);
+      } else {
+        const int g = f - A4;
+        const int rr = g / (BN / 4), cc = (g % (BN / 4)) * 4;
+        const int64_t gr = r0 + rr;
+        const bool ok = gr < r_end && b0 + cc < Kb;
+        cp_async16(&Bs[slot][rr][cc], ok ? B + gr * ldb + b0 + cc : B, ok ? 16 : 0);
       }
-      pa[u] = v;
     }
-#pragma unroll
-    for (int u = 0; u < (B4 + NT - 1) / NT; ++u) {
-      int f = tid + u * NT;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (f < B4) {
-        int rr = f / (BN / 4), cc = (f % (BN / 4)) * 4;
-        int64_t gr = r0 + rr;
-        if (gr < r_end && b0 + cc < Kb) {
-          v = __ldg(reinterpret_cast<const float4*>(B + gr * ldb + b0 + cc));
-          if (row_scale) {
-            float s = __ldg(row_scale + gr);
-            v.x *= s; v.y *= s; v.z *= s; v.w *= s;
-          }
-        }
-      }
-      pb[u] = v;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < (A4 + NT - 1) / NT; ++u) {
-      int f = tid + u * NT;
-      if (f < A4) *reinterpret_cast<float4*>(&As[buf][f / (BM / 4)][(f % (BM / 4)) * 4]) = pa[u];
-    }
-#pragma unroll
-    for (int u = 0; u < (B4 + NT - 1) / NT; ++u) {
-      int f = tid + u * NT;
-      if (f < B4) *reinterpret_cast<float4*>(&Bs[buf][f / (BN / 4)][(f % (BN / 4)) * 4]) = pb[u];
+    if (row_scale && tid < kF32Stage) {
+      const int64_t gr = r0 + tid;
+      Ss[slot][tid] = gr < r_end ? __ldg(row_scale + gr) : 0.f;
     }
   };
   float acc[TM][TN];
@@ -661,21 +656,25 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
   const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
-  if (nst > 0) {
-    load(r_begin);
-    store(0);
+#pragma unroll
+  for (int s = 0; s < kF32Ring - 1; ++s) {
+    if (s < nst) issue(s);
+    cp_async_commit();
   }
-  __syncthreads();
   for (int64_t s = 0; s < nst; ++s) {
-    const int buf = (int)(s & 1);
-    if (s + 1 < nst) load(r_begin + (s + 1) * kF32Stage);
+    cp_async_wait<kF32Ring - 2>();  // stage s landed (this thread's copies)
+    __syncthreads();                // ... everyone's; and slot (s - 1) % ring is free
+    if (s + kF32Ring - 1 < nst) issue(s + kF32Ring - 1);
+    cp_async_commit();
+    const int buf = (int)(s % kF32Ring);
 #pragma unroll
     for (int kk = 0; kk < kF32Stage; ++kk) {
       float a[TM];
+      const float sc = row_scale ? Ss[buf][kk] : 1.f;
 #pragma unroll
       for (int i = 0; i < TM; i += 4) {
         const float4 va = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + i]);
-        a[i] = va.x; a[i + 1] = va.y; a[i + 2] = va.z; a[i + 3] = va.w;
+        a[i] = va.x * sc; a[i + 1] = va.y * sc; a[i + 2] = va.z * sc; a[i + 3] = va.w * sc;
       }
       float b[TN];
 #pragma unroll
@@ -688,9 +687,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
-    if (s + 1 < nst) store(buf ^ 1);
-    __syncthreads();
   }
+  cp_async_wait<0>();
   float* W = ws + (int64_t)blockIdx.y * ws_lda * ws_ld;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
