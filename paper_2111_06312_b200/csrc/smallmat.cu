@@ -301,6 +301,126 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
   }
 }
 
+// Block one-sided Jacobi (cooperative grid of P CTAs): the l columns are cut into 2P blocks of
+// b columns; in each outer round CTA p takes the block pair the round-robin tournament gives it,
+// loads those 2b columns of A and J into shared memory, runs one inner sweep over all
+// (2b choose 2) column pairs there (2b - 1 inner rounds of b disjoint pairs, a warp per pair,
+// norms carried as in jacobi_kernel), and writes the columns back; one grid barrier per outer
+// round.  Every column pair meets in every outer sweep, so the outer sweep is a (reordered)
+// full Jacobi sweep: 2P - 1 grid barriers per sweep instead of l - 1.
+constexpr int kJbThreads = 256;
+
+__global__ void __launch_bounds__(kJbThreads) jacobi_block_kernel(const double* __restrict__ R, int l, int b,
+                                                                  double* A, double* J, int* counters,
+                                                                  DevStatus* status, int max_sweeps) {
+  extern __shared__ double smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int P = gridDim.x, nb = 2 * P;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kJbThreads / 32;
+  double* sA = smem;                           // 2b columns of A (l each)
+  double* sJ = smem + (int64_t)2 * b * l;      // 2b columns of J
+  double* snrm = smem + (int64_t)4 * b * l;    // 2b squared norms
+  int* scol = reinterpret_cast<int*>(snrm + 2 * b);  // global column of local slot (or -1)
+  for (int64_t t = blockIdx.x * (int64_t)kJbThreads + tid; t < (int64_t)l * l; t += (int64_t)P * kJbThreads) {
+    A[t] = R[t];
+    const int64_t j = t / l, i = t - j * l;
+    J[t] = (i == j) ? 1.0 : 0.0;
+  }
+  if (blockIdx.x == 0 && tid == 0) { counters[0] = 0; counters[1] = 0; }
+  grid.sync();
+  const double tol = (double)l * 1.1102230246251565e-16;
+  const int m2 = 2 * b;  // local columns (even)
+  int sweep = 0;
+  for (sweep = 0; sweep < max_sweeps; ++sweep) {
+    int* cnt = counters + (sweep & 1);
+    for (int round = 0; round < nb - 1; ++round) {
+      const int bi = rr_index(blockIdx.x, round, nb), bj = rr_index(nb - 1 - blockIdx.x, round, nb);
+      // load the two blocks (slot q < b: block bi, else bj)
+      for (int q = tid; q < m2; q += kJbThreads) {
+        const int c = (q < b ? bi : bj) * b + (q % b);
+        scol[q] = c < l ? c : -1;
+      }
+      __syncthreads();
+      for (int64_t t = tid; t < (int64_t)m2 * l; t += kJbThreads) {
+        const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+        const int c = scol[q];
+        sA[t] = c >= 0 ? A[(int64_t)c * l + r] : 0.0;
+        sJ[t] = c >= 0 ? J[(int64_t)c * l + r] : 0.0;
+      }
+      __syncthreads();
+      for (int q = warp; q < m2; q += nw) {
+        const double* a = sA + (int64_t)q * l;
+        double v = 0.0;
+        for (int r = lane; r < l; r += 32) v += a[r] * a[r];
+        v = warp_sum(v);
+        if (lane == 0) snrm[q] = v;
+      }
+      __syncthreads();
+      // inner sweep: m2 - 1 rounds of m2 / 2 disjoint pairs
+      for (int ir = 0; ir < m2 - 1; ++ir) {
+        for (int pp = warp; pp < m2 / 2; pp += nw) {
+          int i = rr_index(pp, ir, m2), j = rr_index(m2 - 1 - pp, ir, m2);
+          if (scol[i] < 0 || scol[j] < 0) continue;
+          if (scol[i] > scol[j]) { const int t = i; i = j; j = t; }  // orient as in the global order
+          double* ai = sA + (int64_t)i * l;
+          double* aj = sA + (int64_t)j * l;
+          double g0 = 0.0, g1 = 0.0;  // two chains: the dot is latency-bound
+          int r = lane;
+#pragma unroll 4
+          for (; r + 32 < l; r += 64) {
+            g0 += ai[r] * aj[r];
+            g1 += ai[r + 32] * aj[r + 32];
+          }
+          if (r < l) g0 += ai[r] * aj[r];
+          const double ga = warp_sum(g0 + g1);
+          const double al = snrm[i], be = snrm[j];
+          if (al > 0.0 && be > 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+#pragma unroll 4
+            for (int r2 = lane; r2 < l; r2 += 32) {
+              const double x = ai[r2], y = aj[r2];
+              ai[r2] = c * x - s * y;
+              aj[r2] = s * x + c * y;
+            }
+            double* ji = sJ + (int64_t)i * l;
+            double* jj = sJ + (int64_t)j * l;
+#pragma unroll 4
+            for (int r2 = lane; r2 < l; r2 += 32) {
+              const double x = ji[r2], y = jj[r2];
+              ji[r2] = c * x - s * y;
+              jj[r2] = s * x + c * y;
+            }
+            if (lane == 0) {
+              atomicAdd(cnt, 1);
+              snrm[i] = al - t * ga;
+              snrm[j] = be + t * ga;
+            }
+          }
+          __syncwarp();
+        }
+        __syncthreads();
+      }
+      for (int64_t t = tid; t < (int64_t)m2 * l; t += kJbThreads) {
+        const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+        const int c = scol[q];
+        if (c >= 0) {
+          A[(int64_t)c * l + r] = sA[t];
+          J[(int64_t)c * l + r] = sJ[t];
+        }
+      }
+      grid.sync();
+    }
+    const int rotations = *((volatile int*)cnt);
+    grid.sync();
+    if (blockIdx.x == 0 && tid == 0) counters[(sweep + 1) & 1] = 0;
+    grid.sync();
+    if (rotations == 0) { ++sweep; break; }
+  }
+  if (blockIdx.x == 0 && tid == 0) status->jacobi_sweeps = sweep;
+}
+
 // sigma_j = ||A_j||; descending order; Ub = A_perm / sigma, Vb = J_perm (first k columns).
 __global__ void __launch_bounds__(1024) jacobi_finish_kernel(const double* __restrict__ A, const double* __restrict__ J,
                                                              int l, int k, int64_t ldk, double* sig_ws,
@@ -744,6 +864,34 @@ cudaError_t launch_jacobi_svd(const double* R, int l, int k, int64_t ldk, double
       }
       --g_launches;
       (void)cudaGetLastError();
+    }
+  }
+  if (!done && !getenv("ISVD_JACOBI_PAIRWISE")) {
+    // block Jacobi: blocks of b columns, 2P blocks, P CTAs.  b = 8 gives each of the 8 warps one
+    // pair per inner round; b = 4 when 16 columns of A and J do not fit 200 KB of shared memory
+    for (int b : {8, 4}) {
+      const int P = (int)ceil_div(l, 2 * b);
+      const size_t smem = (size_t)(4 * b * l + 2 * b) * sizeof(double) + 2 * b * sizeof(int);
+      if (smem > 200 * 1024 || P > num_sms) continue;
+      static bool battr = false;
+      if (!battr) {
+        cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        battr = true;
+      }
+      void* args[] = {(void*)&R, (void*)&l, (void*)&b, (void*)&A, (void*)&J, (void*)&counters, (void*)&status,
+                      (void*)&max_sweeps};
+      ++g_launches;
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)jacobi_block_kernel, dim3(P), dim3(kJbThreads), args,
+                                                  smem, st);
+      if (e != cudaSuccess) {
+        --g_launches;
+        (void)cudaGetLastError();
+        continue;
+      }
+      Aout = A;
+      Jout = J;
+      done = true;
+      break;
     }
   }
   if (!done) {
