@@ -15,21 +15,21 @@
 //   * partials are summed in fp64 in a fixed order by atb_f32_reduce_kernel (dense.cu).
 // The result is in the fp32-chunk numerics class of the SIMT path.
 //
-// One CTA (512 threads, 1 per SM: TMEM 2N columns, ~200 KB smem) computes a 128 x N tile over
-// a contiguous row range:
-//   * all threads stage 32 rows per step into shared memory in the UMMA K-major no-swizzle
-//     canonical layout (core matrices of 8 MN-rows x 4 K-values = 16 bytes per row, MN-groups
-//     128 B apart, K-groups E/8*128 B apart), split into hi / lo: each thread holds 4 x 4 blocks
-//     (4 rows, one float4 each) in registers, transposes them and stores 4-value K-vectors.
-//     The global loads of step t+1 are issued right after step t is stored, so one full step
-//     of loads (~48 KB per SM) is in flight behind the MMAs.  (The MN-major operand form of
-//     kind::tf32, which would take the row-major tiles as they are, produced no output on this
-//     driver in every descriptor variant tried -- profiles/umma_mn_probe.cu.)
-//   * one thread issues 4 k-steps x 3 tcgen05.mma.kind::tf32 (M = 128, N <= 256, K = 8) per
-//     step and commits to the step buffer's mbarrier (gates refilling it) and, at the end of a
-//     chunk, to the chunk's mbarrier (gates draining it);
-//   * warp w drains TMEM lanes 32 (w % 4) .. +31 (rows of the tile), column quarter w / 4, with
-//     tcgen05.ld.32x32b.
+// One CTA (18 warps, 1 per SM: TMEM 2N columns, ~200 KB smem) computes a 128 x N tile over a
+// contiguous row range, in 16-row steps:
+//   * the producer warp TMA-loads (cp.async.bulk.tensor.2d, no swizzle) the raw row-major tiles
+//     A[16 x 128] and B[16 x N] into a 3-deep ring (rows past the tensor are zero-filled);
+//   * 16 converter warps rewrite each raw tile into the UMMA K-major no-swizzle canonical layout
+//     (core matrices of 8 MN-rows x 4 K-values = 16 bytes per row, MN-groups 128 B apart,
+//     K-groups E/8*128 B apart), split into hi / lo: a thread reads a 4 x 4 block (4 rows, one
+//     float4 each), transposes it and stores four 4-value K-vectors into a 3-deep ring.  (The
+//     MN-major operand form of kind::tf32, which would take the row-major tiles as they are,
+//     produced no output in every descriptor variant tried -- profiles/umma_mn_probe.cu.)
+//   * the MMA warp issues 2 k-steps x 3 tcgen05.mma.kind::tf32 (M = 128, N <= 256, K = 8) per
+//     step, commits to the converted slot's "empty" barrier and, at the end of a chunk, to the
+//     chunk accumulator's "full" barrier;
+//   * the converter warps drain each finished chunk (tcgen05.ld.32x32b: warp w reads TMEM lanes
+//     32 (w % 4) .. +31, column quarter w / 4) and release the accumulator.
 // Operand descriptors and the instruction descriptor follow the sm_100 UMMA bit layouts.
 #include <algorithm>
 
@@ -41,7 +41,6 @@ namespace {
 
 constexpr int kTcM = 128;       // UMMA M (rows of the C tile = columns of A)
 constexpr int kTcChunk = 128;   // rows per TMEM accumulation (truncation bound)
-constexpr int kTcThreads = 512;  // 16 warps: 4 TMEM lane quadrants x 4 column quarters
 
 // Store the K-vector (rows k0..k0+3, k0 % 4 == 0) of MN-element c into the K-major layout.
 ISVD_DEVICE void st_split(float* hi, float* lo, int k0, int c, int lbo_floats, float4 v) {
@@ -86,15 +85,28 @@ template <int N>
 struct TcCfg {
   static constexpr int kStep = 16;                     // rows per pipeline step (2 MMAs of K = 8)
   static constexpr int kStepsPerChunk = kTcChunk / kStep;
-  static constexpr int kRing = 4;                      // raw stages in flight
+  static constexpr int kRaw = 3;                       // TMA ring of raw row tiles
+  static constexpr int kConv = 3;                      // ring of converted (K-major hi / lo) operands
   static constexpr int RAW_FL = kStep * (kTcM + N);    // raw A | raw B rows of one step
   static constexpr int A_FL = kStep * kTcM, B_FL = kStep * N;
   static constexpr int CONV_FL = 2 * A_FL + 2 * B_FL;  // A hi | A lo | B hi | B lo
-  static constexpr size_t smem_bytes() { return (size_t)(kRing * RAW_FL + 2 * CONV_FL) * sizeof(float); }
+  static constexpr size_t smem_bytes() { return (size_t)(kRaw * RAW_FL + kConv * CONV_FL) * sizeof(float); }
 };
 
+// Warp roles (warp specialisation; hand-offs through mbarriers, no CTA-wide barrier per step):
+//   warps 0..15  converters + drainers: raw tile -> K-major hi / lo operands; every chunk, warp w
+//                drains TMEM lane quadrant w % 4, column quarter w / 4 into its register sums
+//   warp 16      TMA producer (lane 0)
+//   warp 17      MMA issuer (lane 0)
+// Measured at config 4 (Gram 2.45M x 400): 7.77 ms; 8 converter warps (168 registers, no spill)
+// 9.2 ms; the CTA-barrier lockstep form 7.95 ms.  The conversion's shared-memory traffic
+// (TMA write, transposing read/write of hi and lo, MMA operand reads: ~150 KB per 16-row step)
+// is the limit, not the hand-offs.
+constexpr int kTcConvWarps = 16;
+constexpr int kTcWsThreads = (kTcConvWarps + 2) * 32;
+
 template <int N>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcWsThreads, 1)
     tc_atb_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t Ka,
                   const float* __restrict__ rs, int64_t Kb, int64_t rows, int ta, int tb, int symmetric,
                   int64_t rows_per_cta, float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
@@ -103,17 +115,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   static_assert(N % 16 == 0 && N >= 32 && N <= 256, "UMMA N");
   constexpr int KS = C::kStep;
   constexpr int LBO_A = kTcM / 8 * 32, LBO_B = N / 8 * 32;  // K-group (4 values) strides in floats
+  constexpr int CT = kTcConvWarps * 32;                      // converter threads
   constexpr int NBLK_A = (KS / 4) * (kTcM / 4), NBLK = NBLK_A + (KS / 4) * (N / 4);
-  constexpr int QTR = N / 4;                                 // columns drained per thread
+  constexpr int QTR = N / (kTcConvWarps / 4);               // columns drained per thread
   constexpr uint32_t kCols = 2 * N <= 256 ? 256 : 512;       // TMEM: two N-column accumulators
   static_assert(QTR % 4 == 0, "drain granularity");
+  static_assert(NBLK_A <= CT, "A blocks in the first round");
 
   extern __shared__ __align__(1024) float sm[];
-  float* const raw0 = sm;                         // ring: slot i at raw0 + i * RAW_FL
-  float* const conv0 = sm + C::kRing * C::RAW_FL;  // buffer b at conv0 + b * CONV_FL
-  __shared__ __align__(8) uint64_t full[C::kRing];  // raw slot filled (tx bytes)
-  __shared__ __align__(8) uint64_t mbar[2];         // conv buffer b free again (MMAs done)
-  __shared__ __align__(8) uint64_t cbar[2];         // chunk accumulator b complete
+  float* const raw0 = sm;                          // raw slot i at raw0 + i * RAW_FL
+  float* const conv0 = sm + C::kRaw * C::RAW_FL;   // conv slot i at conv0 + i * CONV_FL
+  __shared__ __align__(8) uint64_t raw_full[C::kRaw], raw_empty[C::kRaw];
+  __shared__ __align__(8) uint64_t conv_full[C::kConv], conv_empty[C::kConv];
+  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -136,11 +150,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int64_t nch = (nst + C::kStepsPerChunk - 1) / C::kStepsPerChunk;
 
   if (tid == 0) {
-    for (int i = 0; i < C::kRing; ++i) mbar_init(&full[i], 1);
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_init(&cbar[0], 1);
-    mbar_init(&cbar[1], 1);
+    for (int i = 0; i < C::kRaw; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&raw_empty[i], kTcConvWarps);
+    }
+    for (int i = 0; i < C::kConv; ++i) {
+      mbar_init(&conv_full[i], kTcConvWarps);
+      mbar_init(&conv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kTcConvWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -152,125 +173,130 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
-  const uint32_t idesc = umma_idesc(kTcM, N);
 
-  // thread 0 fills raw slot (st % kRing) with the rows of step st: one TMA box per operand
-  // (rows past the tensor are zero-filled; rows past this CTA's range are zeroed when converted)
-  auto fill = [&](int64_t st) {
-    const int slot = (int)(st % C::kRing);
-    uint64_t* bar = &full[slot];
-    float* rawA = raw0 + slot * C::RAW_FL;
-    mbar_expect_tx(bar, (uint32_t)C::RAW_FL * 4);
-    const int r0 = (int)(r_begin + st * KS);
-    tma_2d(rawA, &tmA, (int)a0, r0, bar);
-    tma_2d(rawA + C::A_FL, &tmB, (int)b0, r0, bar);
-  };
-  if (tid == 0)
-    for (int64_t st = 0; st < nst && st < C::kRing; ++st) fill(st);
-
-  float acc[QTR];
-#pragma unroll
-  for (int q = 0; q < QTR; ++q) acc[q] = 0.f;
-  const uint32_t lane_base = (uint32_t)(warp & 3) * 32;
-  const uint32_t col_q = (uint32_t)(warp >> 2) * QTR;
-  int64_t drained = 0;
-  auto drain = [&](int64_t c) {
-    mbar_wait(&cbar[c & 1], (uint32_t)((c >> 1) & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t base = tmem + (lane_base << 16) + (uint32_t)(c & 1) * N + col_q;
-#pragma unroll
-    for (int q0 = 0; q0 < QTR; q0 += 32) {
-      uint32_t r[32];
-#pragma unroll
-      for (int q = 0; q < 32; q += 4)
-        if (q0 + q < QTR)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(r[q]), "=r"(r[q + 1]), "=r"(r[q + 2]), "=r"(r[q + 3])
-                       : "r"(base + (uint32_t)(q0 + q)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (q0 + q < QTR) acc[q0 + q] += __uint_as_float(r[q]);
+  if (warp == kTcConvWarps) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int64_t st = 0; st < nst; ++st) {
+        const int slot = (int)(st % C::kRaw);
+        if (st >= C::kRaw) mbar_wait(&raw_empty[slot], (uint32_t)((st / C::kRaw - 1) & 1));
+        float* rawA = raw0 + slot * C::RAW_FL;
+        mbar_expect_tx(&raw_full[slot], (uint32_t)C::RAW_FL * 4);
+        const int r0 = (int)(r_begin + st * KS);
+        tma_2d(rawA, &tmA, (int)a0, r0, &raw_full[slot]);
+        tma_2d(rawA + C::A_FL, &tmB, (int)b0, r0, &raw_full[slot]);
+      }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  };
-
-  // row scales of this thread's A block rows (threads < NBLK_A own one A block per step)
-  static_assert(NBLK_A <= kTcThreads, "one A block per thread");
-  float sc[4] = {1.f, 1.f, 1.f, 1.f};
-  auto load_scale = [&](int64_t st) {
-    if (!rs || tid >= NBLK_A) return;
-    const int64_t k0 = r_begin + st * KS;
-    const int kb = tid / (kTcM / 4);
+  } else if (warp == kTcConvWarps + 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(kTcM, N);
+      for (int64_t st = 0; st < nst; ++st) {
+        const int cs = (int)(st % C::kConv);
+        const int64_t ch = st / C::kStepsPerChunk;
+        const bool first = (st % C::kStepsPerChunk) == 0;
+        if (first && ch >= 2) mbar_wait(&acc_empty[ch & 1], (uint32_t)((ch / 2 - 1) & 1));  // drained
+        mbar_wait(&conv_full[cs], (uint32_t)((st / C::kConv) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(ch & 1) * N;
+        const uint32_t ah = smem_u32(conv0 + cs * C::CONV_FL), al = ah + C::A_FL * 4;
+        const uint32_t bh = ah + 2 * C::A_FL * 4, bl = bh + C::B_FL * 4;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) sc[q] = k0 + kb * 4 + q < r_end ? __ldg(rs + k0 + kb * 4 + q) : 0.f;
-  };
-  if (nst > 0) load_scale(0);
-
-  for (int64_t st = 0; st < nst; ++st) {
-    const int buf = (int)(st & 1), slot = (int)(st % C::kRing);
-    const int64_t k0 = r_begin + st * KS;
-    const int nr = (int)(r_end - k0 < KS ? r_end - k0 : KS);
-    if (st >= 2) mbar_wait(&mbar[buf], (uint32_t)(((st - 2) >> 1) & 1));  // MMAs of step st-2 done
-    // the chunk finished two steps ago is complete too: drain it (its accumulator is next
-    // written by chunk + 2, whose MMAs are issued after this step's __syncthreads)
-    if ((st % C::kStepsPerChunk) == 1 && st > C::kStepsPerChunk) drain(drained++);
-    mbar_wait(&full[slot], (uint32_t)((st / C::kRing) & 1));  // raw rows of this step landed
-    {
-      const float* rawA = raw0 + slot * C::RAW_FL;
-      const float* rawB = rawA + C::A_FL;
-      float* const Ahi = conv0 + buf * C::CONV_FL;
-      float* const Alo = Ahi + C::A_FL;
-      float* const Bhi = Ahi + 2 * C::A_FL;
-      float* const Blo = Bhi + C::B_FL;
+        for (int s = 0; s < KS / 8; ++s) {
+          // one MMA (K = 8) spans two K-groups
+          const uint32_t ka = (uint32_t)(2 * s) * LBO_A * 4, kb = (uint32_t)(2 * s) * LBO_B * 4;  // bytes
+          const uint64_t dah = umma_desc(ah + ka, LBO_A * 4, 128), dal = umma_desc(al + ka, LBO_A * 4, 128);
+          const uint64_t dbh = umma_desc(bh + kb, LBO_B * 4, 128), dbl = umma_desc(bl + kb, LBO_B * 4, 128);
+          mma_tf32(d, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
+          mma_tf32(d, dah, dbl, idesc, 1u);
+          mma_tf32(d, dal, dbh, idesc, 1u);
+        }
+        umma_commit(&conv_empty[cs]);
+        if ((st % C::kStepsPerChunk) == C::kStepsPerChunk - 1 || st == nst - 1) umma_commit(&acc_full[ch & 1]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- converters / drainers
+    float acc[QTR];
 #pragma unroll
-      for (int i = 0; i < (NBLK + kTcThreads - 1) / kTcThreads; ++i) {
-        const int f = tid + i * kTcThreads;
-        if (f < NBLK_A) {
-          const int kb = f / (kTcM / 4), cb = f - kb * (kTcM / 4);
-          convert_block<kTcM, kTcM>(rawA, Ahi, Alo, kb, cb, nr, a_cols, sc);
-        } else if (f < NBLK) {
-          const int g = f - NBLK_A;
-          const int kb = g / (N / 4), cb = g - kb * (N / 4);
-          const float one[4] = {1.f, 1.f, 1.f, 1.f};
-          convert_block<N, N>(rawB, Bhi, Blo, kb, cb, nr, b_cols, one);
+    for (int q = 0; q < QTR; ++q) acc[q] = 0.f;
+    const uint32_t lane_base = (uint32_t)(warp & 3) * 32;
+    const uint32_t col_q = (uint32_t)(warp >> 2) * QTR;  // column group of this warp
+    int64_t drained = 0;
+    auto drain = [&](int64_t c) {
+      mbar_wait(&acc_full[c & 1], (uint32_t)((c >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + (lane_base << 16) + (uint32_t)(c & 1) * N + col_q;
+#pragma unroll
+      for (int q0 = 0; q0 < QTR; q0 += 16) {
+        uint32_t r[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 4)
+          if (q0 + q < QTR)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r[q]), "=r"(r[q + 1]), "=r"(r[q + 2]), "=r"(r[q + 3])
+                         : "r"(base + (uint32_t)(q0 + q)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q0 + q < QTR) acc[q0 + q] += __uint_as_float(r[q]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[c & 1]);
+    };
+    // blocks f = tid + i CT (A blocks first, all in round 0); row scales of the next step for them
+    const bool is_a = tid < NBLK_A;
+    const int kb = is_a ? tid / (kTcM / 4) : 0;
+    float sc[4] = {1.f, 1.f, 1.f, 1.f};
+    auto load_scale = [&](int64_t st) {
+      if (!rs || !is_a) return;
+      const int64_t k0 = r_begin + st * KS;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sc[q] = k0 + kb * 4 + q < r_end ? __ldg(rs + k0 + kb * 4 + q) : 0.f;
+    };
+    if (nst > 0) load_scale(0);
+    const float one[4] = {1.f, 1.f, 1.f, 1.f};
+    for (int64_t st = 0; st < nst; ++st) {
+      const int rslot = (int)(st % C::kRaw), cs = (int)(st % C::kConv);
+      const int64_t k0 = r_begin + st * KS;
+      const int nr = (int)(r_end - k0 < KS ? r_end - k0 : KS);
+      // the chunk that ended two steps ago: drain it (its accumulator is next written by chunk
+      // + 2, which the MMA warp starts only after every warp arrived on acc_empty)
+      if ((st % C::kStepsPerChunk) == 1 && st > C::kStepsPerChunk) drain(drained++);
+      if (st >= C::kConv) mbar_wait(&conv_empty[cs], (uint32_t)((st / C::kConv - 1) & 1));
+      mbar_wait(&raw_full[rslot], (uint32_t)((st / C::kRaw) & 1));
+      {
+        const float* rawA = raw0 + rslot * C::RAW_FL;
+        float* const Ahi = conv0 + cs * C::CONV_FL;
+#pragma unroll
+        for (int i = 0; i < (NBLK + CT - 1) / CT; ++i) {
+          const int f = tid + i * CT;
+          if (f < NBLK_A) {
+            convert_block<kTcM, kTcM>(rawA, Ahi, Ahi + C::A_FL, f / (kTcM / 4), f % (kTcM / 4), nr, a_cols, sc);
+          } else if (f < NBLK) {
+            const int g = f - NBLK_A;
+            convert_block<N, N>(rawA + C::A_FL, Ahi + 2 * C::A_FL, Ahi + 2 * C::A_FL + C::B_FL, g / (N / 4),
+                                g % (N / 4), nr, b_cols, one);
+          }
         }
       }
-    }
-    if (st + 1 < nst) load_scale(st + 1);  // row scales of the next step, in flight behind the MMAs
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-    __syncthreads();
-    // raw slot consumed by every thread: refill it with step st + kRing
-    if (tid == 0) {
-      if (st + C::kRing < nst) fill(st + C::kRing);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t c = st / C::kStepsPerChunk;
-      const uint32_t d = tmem + (uint32_t)(c & 1) * N;
-      const uint32_t ah = smem_u32(conv0 + buf * C::CONV_FL), al = ah + C::A_FL * 4;
-      const uint32_t bh = ah + 2 * C::A_FL * 4, bl = bh + C::B_FL * 4;
-      const bool first = (st % C::kStepsPerChunk) == 0;
-#pragma unroll
-      for (int s = 0; s < KS / 8; ++s) {
-        // one MMA (K = 8) spans two K-groups
-        const uint32_t ka = (uint32_t)(2 * s) * LBO_A * 4, kb = (uint32_t)(2 * s) * LBO_B * 4;  // bytes
-        const uint64_t dah = umma_desc(ah + ka, LBO_A * 4, 128), dal = umma_desc(al + ka, LBO_A * 4, 128);
-        const uint64_t dbh = umma_desc(bh + kb, LBO_B * 4, 128), dbl = umma_desc(bl + kb, LBO_B * 4, 128);
-        mma_tf32(d, dah, dbh, idesc, (first && s == 0) ? 0u : 1u);
-        mma_tf32(d, dah, dbl, idesc, 1u);
-        mma_tf32(d, dal, dbh, idesc, 1u);
+      if (st + 1 < nst) load_scale(st + 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&raw_empty[rslot]);
+        mbar_arrive(&conv_full[cs]);
       }
-      umma_commit(&mbar[buf]);
-      if ((st % C::kStepsPerChunk) == C::kStepsPerChunk - 1 || st == nst - 1) umma_commit(&cbar[c & 1]);
     }
-  }
-  while (drained < nch) drain(drained++);
-
-  // epilogue: this thread's row of the tile, columns [col_q, col_q + QTR)
-  const int64_t row = a0 + lane_base + lane;
-  float* w = ws + ((int64_t)blockIdx.y * ws_lda + row) * ws_ld + b0 + col_q;
+    while (drained < nch) drain(drained++);
+    // epilogue: this thread's row of the tile, columns [col_q, col_q + QTR)
+    const int64_t row = a0 + lane_base + lane;
+    float* w = ws + ((int64_t)blockIdx.y * ws_lda + row) * ws_ld + b0 + col_q;
 #pragma unroll
-  for (int q = 0; q < QTR; q += 4)
-    *reinterpret_cast<float4*>(w + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+    for (int q = 0; q < QTR; q += 4)
+      *reinterpret_cast<float4*>(w + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -319,7 +345,7 @@ cudaError_t tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t 
   }
   dim3 grid((unsigned)t.tiles, (unsigned)t.parts);
   ++g_launches;
-  tc_atb_kernel<N><<<grid, kTcThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta, t.tb, symmetric ? 1 : 0,
+  tc_atb_kernel<N><<<grid, kTcWsThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta, t.tb, symmetric ? 1 : 0,
                                                    t.rows_per_cta, ws, ws_lda, ws_ld, gate);
   return cudaGetLastError();
 }

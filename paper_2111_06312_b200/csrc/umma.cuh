@@ -58,6 +58,10 @@ ISVD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+ISVD_DEVICE void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Non-blocking probe: has the phase with this parity completed?
 ISVD_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t done;
