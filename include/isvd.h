@@ -114,7 +114,11 @@ enum {
 isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
                               const int64_t* row_ptr, const int32_t* col_idx, uint32_t flags,
                               isvd_graph* out);
-isvd_status isvd_graph_destroy(isvd_graph g); /* ISVD_ERR_BUSY while ops reference it */
+/* ISVD_ERR_BUSY while ops reference it.  Device memory of destroyed graphs / operators goes
+ * back to the context's cache (reused by later graphs / operators of the same sizes, trimmed
+ * when an allocation fails) and is released by isvd_ctx_destroy; ISVD_NO_POOL=1 frees it
+ * immediately instead. */
+isvd_status isvd_graph_destroy(isvd_graph g);
 isvd_status isvd_graph_info(isvd_graph g, int64_t* n_global, int64_t* n_local, int64_t* nnz_local,
                             int64_t* max_degree);
 

@@ -14,8 +14,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/isvd.h"
@@ -53,6 +56,13 @@ struct isvd_ctx_s {
   int spmm_steps = 0;
   double spmm_alg_bytes = 0.0;
   std::vector<cudaEvent_t> prof_events;  // pairs
+  // caching device allocator: buffers released by destroyed graphs / ops / workspaces are kept
+  // (by exact rounded size) and handed out again, so rebuilding a graph + operator of the same
+  // shape pays no cudaMalloc/cudaFree (they cost ~ms per GB-sized buffer); trimmed on OOM and
+  // released by isvd_ctx_destroy
+  std::mutex pool_mu;
+  std::multimap<size_t, void*> pool_free;
+  std::unordered_map<void*, size_t> pool_size;
 };
 
 struct isvd_graph_s {
@@ -146,14 +156,59 @@ void set_err(isvd_ctx ctx, const std::string& m) {
     }                                                                                                         \
   } while (0)
 
+void pool_trim(isvd_ctx ctx) {
+  std::lock_guard<std::mutex> lk(ctx->pool_mu);
+  for (auto& kv : ctx->pool_free) {
+    ctx->pool_size.erase(kv.second);
+    cudaFree(kv.second);
+  }
+  ctx->pool_free.clear();
+}
+
 void* dmalloc(isvd_ctx ctx, size_t bytes, std::vector<void*>& list) {
   void* p = nullptr;
-  if (bytes == 0) bytes = 16;
-  CK(cudaMalloc(&p, bytes));
+  bytes = (bytes + 511) / 512 * 512;
+  if (bytes == 0) bytes = 512;
+  {
+    std::lock_guard<std::mutex> lk(ctx->pool_mu);
+    auto it = ctx->pool_free.find(bytes);
+    if (it != ctx->pool_free.end()) {
+      p = it->second;
+      ctx->pool_free.erase(it);
+    }
+  }
+  if (!p) {
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      (void)cudaGetLastError();
+      pool_trim(ctx);  // cached blocks of other sizes may be what is missing
+      CK(cudaMalloc(&p, bytes));
+    }
+    std::lock_guard<std::mutex> lk(ctx->pool_mu);
+    ctx->pool_size[p] = bytes;
+  }
   list.push_back(p);
   // padding columns of every iterate must read as zero: workspaces start cleared
   CK(cudaMemset(p, 0, bytes));
   return p;
+}
+
+// return a dmalloc'd buffer to the context's cache (the device may still be using it: callers
+// synchronise the stream before releasing, as they did before cudaFree)
+void dfree(isvd_ctx ctx, void* p) {
+  if (!p) return;
+  static const bool no_pool = getenv("ISVD_NO_POOL") && getenv("ISVD_NO_POOL")[0] == '1';
+  std::lock_guard<std::mutex> lk(ctx->pool_mu);
+  if (no_pool) {
+    ctx->pool_size.erase(p);
+    cudaFree(p);
+    return;
+  }
+  auto it = ctx->pool_size.find(p);
+  if (it == ctx->pool_size.end()) {
+    cudaFree(p);
+    return;
+  }
+  ctx->pool_free.insert({it->second, p});
 }
 
 struct DeviceGuard {
@@ -195,7 +250,7 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   isvd_ctx ctx = g->ctx;
   if (wpad <= op->ws_wpad) return;
   CK(cudaStreamSynchronize(ctx->stream));
-  for (void* p : op->ws_allocs) cudaFree(p);
+  for (void* p : op->ws_allocs) dfree(ctx, p);
   op->ws_allocs.clear();
   if (op->sws.graph_exec) {  // the captured solver referenced the freed buffers
     cudaGraphExecDestroy(op->sws.graph_exec);
@@ -619,6 +674,7 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
   DeviceGuard dg(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  pool_trim(ctx);
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -673,8 +729,9 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     std::vector<void*> tmp;
     struct TmpFree {
       std::vector<void*>& v;
-      ~TmpFree() { for (void* q : v) cudaFree(q); }
-    } tmp_free{tmp};
+      isvd_ctx c;
+      ~TmpFree() { for (void* q : v) dfree(c, q); }
+    } tmp_free{tmp, ctx};
     g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
     g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nnz + kIdxPad), g->allocs);
     int32_t* ci_in = relabel ? (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), tmp) : g->col_idx;
@@ -800,7 +857,7 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       CK(cudaMemcpy(p.seg_beg, seg_beg.data(), sizeof(int64_t) * seg_beg.size(), cudaMemcpyHostToDevice));
   });
   if (st != ISVD_OK) {
-    for (void* p : g->allocs) cudaFree(p);
+    for (void* p : g->allocs) dfree(ctx, p);
     delete g;
     return st;
   }
@@ -814,7 +871,7 @@ isvd_status isvd_graph_destroy(isvd_graph g) {
   if (g->refs.load() > 0) return ISVD_ERR_BUSY;
   DeviceGuard dg(g->ctx->device);
   cudaStreamSynchronize(g->ctx->stream);
-  for (void* p : g->allocs) cudaFree(p);
+  for (void* p : g->allocs) dfree(g->ctx, p);
   g->ctx->live_graphs--;
   delete g;
   return ISVD_OK;
@@ -884,7 +941,7 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
             CK(launch_scale_rows(src, desc->ldx, x, desc->ldx, g->n_local, desc->ldx, nullptr, 1.f, nullptr,
                                  ctx->stream, g->new2old));
             CK(cudaStreamSynchronize(ctx->stream));
-            for (void* q : stage) cudaFree(q);
+            for (void* q : stage) dfree(ctx, q);
           }
         }
         op->X = x;
@@ -909,10 +966,10 @@ isvd_status isvd_op_shape(isvd_op op, int64_t* rows, int64_t* cols) {
   return ISVD_OK;
 }
 
-static void free_solver_ws(SolverWs& s) {
+static void free_solver_ws(isvd_ctx ctx, SolverWs& s) {
   if (s.graph_exec) cudaGraphExecDestroy(s.graph_exec);
   s.graph_exec = nullptr;
-  for (void* p : s.allocs) cudaFree(p);
+  for (void* p : s.allocs) dfree(ctx, p);
   s.allocs.clear();
   s.key_l = s.key_k = -1;
 }
@@ -921,9 +978,9 @@ isvd_status isvd_op_destroy(isvd_op op) {
   if (!op) return ISVD_ERR_INVALID_ARG;
   DeviceGuard dg(op->g->ctx->device);
   cudaStreamSynchronize(op->g->ctx->stream);
-  for (void* p : op->ws_allocs) cudaFree(p);
-  free_solver_ws(op->sws);
-  if (op->own_x) cudaFree((void*)op->X);
+  for (void* p : op->ws_allocs) dfree(op->g->ctx, p);
+  free_solver_ws(op->g->ctx, op->sws);
+  if (op->own_x) dfree(op->g->ctx, (void*)op->X);
   op->g->refs--;
   delete op;
   return ISVD_OK;
@@ -997,7 +1054,7 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
   if (s.key_l == l && s.key_k == k) return;
   isvd_ctx ctx = op->g->ctx;
   CK(cudaStreamSynchronize(ctx->stream));
-  free_solver_ws(s);
+  free_solver_ws(ctx, s);
   const int64_t ld = round_up(l, 4), ldk = round_up(k, 4);
   const int64_t rr = std::max<int64_t>(op->g->n_local, 1), cr = std::max<int64_t>(c_rows_local(op), 1);
   auto f = [&](int64_t n) { return (float*)dmalloc(ctx, sizeof(float) * n, s.allocs); };
