@@ -709,8 +709,18 @@ __global__ void atb_f32_reduce_kernel(const float* __restrict__ ws, int64_t ws_l
     int64_t i = t / Kb, j = t - (t / Kb) * Kb;
     int64_t si = i, sj = j;
     if (symmetric && i > j) { si = j; sj = i; }
-    double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += (double)ws[((int64_t)c * ws_lda + si) * ws_ld + sj];
+    // 8 interleaved partial sums (independent loads in flight), combined in a fixed order:
+    // deterministic, and no longer one dependent add per chunk
+    double p[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    const float* src = ws + si * ws_ld + sj;
+    const int64_t cstride = ws_lda * ws_ld;
+    int c = 0;
+    for (; c + 8 <= nchunks; c += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) p[u] += (double)src[(int64_t)(c + u) * cstride];
+    }
+    for (int u = 0; c < nchunks; ++c, ++u) p[u] += (double)src[(int64_t)c * cstride];
+    const double s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
     if (G) G[i * ldg + j] = s;
     if (out32) out32[i * ld32 + j] = (float)s;
   }
