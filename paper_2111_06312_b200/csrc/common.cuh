@@ -23,6 +23,16 @@ struct DevStatus {
 ISVD_DEVICE float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 ISVD_DEVICE void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 ISVD_DEVICE float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+// paired fp32 FMA (sm_100 FFMA2: same FLOP rate as FFMA, half the issue slots; a scalar first
+// operand compiles to the .F32 broadcast form): d = a * b + c, elementwise, round-to-nearest
+ISVD_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
 #endif
 
 // Kernels enqueued by this host thread (each launcher adds the number it launched);

@@ -128,11 +128,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
     }
   };
 
-  float acc[TM][TN];
+  float2 acc[TM][TN / 2];  // column pairs (FFMA2)
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
   int64_t ntiles = (kend + BK - 1) / BK;
   if (ntiles > 0) {
@@ -164,7 +164,9 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[kk & 1][i], b[kk & 1][j], acc[i][j]);
+        for (int j = 0; j < TN / 2; ++j)
+          acc[i][j] = ffma2(make_float2(a[kk & 1][i], a[kk & 1][i]),
+                            make_float2(b[kk & 1][2 * j], b[kk & 1][2 * j + 1]), acc[i][j]);
     }
     if (t + 1 < ntiles) {
       store_tiles(buf ^ 1);
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
       int64_t gn = n0 + (j / 4) * 4 * TX + tx * 4;
       if (gn < N)
         *reinterpret_cast<float4*>(C + (out_map ? (int64_t)out_map[gm] : gm) * ldc + gn) =
-            make_float4(s * acc[i][j], s * acc[i][j + 1], s * acc[i][j + 2], s * acc[i][j + 3]);
+            make_float4(s * acc[i][j / 2].x, s * acc[i][j / 2].y, s * acc[i][j / 2 + 1].x, s * acc[i][j / 2 + 1].y);
     }
   }
 }
@@ -650,11 +652,11 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       Ss[slot][tid] = gr < r_end ? __ldg(row_scale + gr) : 0.f;
     }
   };
-  float acc[TM][TN];
+  float2 acc[TM][TN / 2];  // column pairs (FFMA2)
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
   const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
 #pragma unroll
   for (int s = 0; s < kF32Ring - 1; ++s) {
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN / 2; ++j) acc[i][j] = ffma2(make_float2(a[i], a[i]), make_float2(b[2 * j], b[2 * j + 1]), acc[i][j]);
     }
   }
   cp_async_wait<0>();
@@ -696,7 +698,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 #pragma unroll
     for (int q = 0; q < QN; ++q)
       *reinterpret_cast<float4*>(w + q * CS + tx * 4) =
-          make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
+          make_float4(acc[i][2 * q].x, acc[i][2 * q].y, acc[i][2 * q + 1].x, acc[i][2 * q + 1].y);
   }
 }
 
