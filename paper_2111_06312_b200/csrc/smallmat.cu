@@ -766,7 +766,9 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, flo
   // Blocked (panel) algorithm: one CTA for l <= kCholSmemMax (whole matrix in its shared
   // memory), a cluster of 8 / 16 CTAs sharing it through DSMEM above that.
   if (l <= 512 && !getenv("ISVD_CHOL_UNBLOCKED")) {
-    const int CS = l <= kCholSmemMax ? 1 : (l <= 400 ? 8 : 16);
+    int CS = l <= kCholSmemMax ? 1 : (l <= 400 ? 8 : 16);
+    if (const char* e = getenv("ISVD_CHOL_CLUSTER"))  // tuning override: 8 or 16 (l > kCholSmemMax)
+      if (l > kCholSmemMax && (atoi(e) == 8 || atoi(e) == 16)) CS = atoi(e);
     const int nblk = (l + kPanel - 1) / kPanel;
     const int rows_max = ((nblk + CS - 1) / CS) * kPanel;
     size_t smem = sizeof(double) * ((size_t)rows_max * l + (size_t)kPanel * l + (size_t)rows_max * kPanel);
