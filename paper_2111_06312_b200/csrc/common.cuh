@@ -133,7 +133,8 @@ cudaError_t launch_tc_gemm(const float* A, int64_t lda, const float* B, int64_t 
 // G = A^T diag(row_scale) B over `rows` rows, A: rows x Ka, B: rows x Kb -> fp64 Ka x ldg.
 // symmetric: A == B, only the upper triangle of tiles is computed and mirrored.
 // If out32 != null the result is also written as fp32 (ld32).
-// f32_stage: fp32 sums over 16-row stages added into fp64 (else fp64 FMA throughout).
+// f32_stage: fp32 sums over <= 1024-row chunks (register-tiled SIMT), fixed-order fp64 across
+// chunks; else exact fp64 (fp64 tensor cores, or DFMA with ISVD_DMMA=0).
 int64_t atb_ws_doubles(int64_t rows, int64_t Ka, int64_t Kb, int num_sms);
 cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t rows, int64_t Ka,
                        int64_t Kb, const float* row_scale, bool symmetric, double* ws, double* G, int64_t ldg,

@@ -195,12 +195,10 @@ constexpr int ATB_R = 16;   // rows per smem stage
 
 constexpr int ATB_THREADS = 64;  // 8 x 8 threads, each an 8 x 8 register tile of the 64 x 64 output tile
 
-// S = double: operands promoted to fp64 once when staged, fp64 FMA (exact products of the
-//   fp32 inputs, fp64 sums): used for Grams whose input may be ill-conditioned.
-// S = float: fp32 FMA over each 16-row stage, the stage sums added into fp64 accumulators
-//   (relative error ~16 u_fp32 per stage sum): X^T Z products and the Gram of the second
-//   CholeskyQR pass (input already orthonormal to ~1e-6).
-template <typename S>
+// Exact fp64 A^T B by DFMA (ISVD_DMMA=0; the default is atb_dmma_kernel): operands promoted to
+// fp64 once when staged, fp64 FMA (exact products of the fp32 inputs, fp64 sums), for Grams
+// whose input may be ill-conditioned.
+using S = double;
 __global__ void __launch_bounds__(ATB_THREADS)
     atb_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb, int64_t rows,
                int64_t Ka, int64_t Kb, const float* __restrict__ row_scale, int symmetric, int tiles_a,
@@ -254,32 +252,17 @@ __global__ void __launch_bounds__(ATB_THREADS)
     for (int u = 0; u < 4; ++u) {
       int f = tid + u * ATB_THREADS;
       int rr = f >> 4, cc = (f & 15) * 4;
-      if constexpr (sizeof(S) == 8) {
-        double2* da = reinterpret_cast<double2*>(&As[buf][rr][cc]);
-        double2* db = reinterpret_cast<double2*>(&Bs[buf][rr][cc]);
-        da[0] = make_double2(pa[u].x, pa[u].y); da[1] = make_double2(pa[u].z, pa[u].w);
-        db[0] = make_double2(pb[u].x, pb[u].y); db[1] = make_double2(pb[u].z, pb[u].w);
-      } else {
-        *reinterpret_cast<float4*>(&As[buf][rr][cc]) = pa[u];
-        *reinterpret_cast<float4*>(&Bs[buf][rr][cc]) = pb[u];
-      }
+      double2* da = reinterpret_cast<double2*>(&As[buf][rr][cc]);
+      double2* db = reinterpret_cast<double2*>(&Bs[buf][rr][cc]);
+      da[0] = make_double2(pa[u].x, pa[u].y); da[1] = make_double2(pa[u].z, pa[u].w);
+      db[0] = make_double2(pb[u].x, pb[u].y); db[1] = make_double2(pb[u].z, pb[u].w);
     }
   };
-  // fp64 accumulators: registers for S = double; shared memory for S = float (frees the
-  // registers for the fp32 stage sums; element q of thread t at accs[q][t], conflict-free)
-  constexpr int kAccRegs = sizeof(S) == 8 ? 8 : 1;
-  double acc[kAccRegs][kAccRegs == 8 ? 8 : 1];
-  __shared__ double accs[sizeof(S) == 8 ? 1 : 64][ATB_THREADS];
-  if constexpr (sizeof(S) == 8) {
+  double acc[8][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 64; ++q) accs[q][tid] = 0.0;
-    acc[0][0] = 0.0;
-  }
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
   const int64_t nst = (r_end - r_begin + ATB_R - 1) / ATB_R;
   if (nst > 0) {
     load(r_begin);
@@ -289,64 +272,34 @@ __global__ void __launch_bounds__(ATB_THREADS)
   for (int64_t st = 0; st < nst; ++st) {
     const int buf = (int)(st & 1);
     if (st + 1 < nst) load(r_begin + (st + 1) * ATB_R);
-    if constexpr (sizeof(S) == 8) {
 #pragma unroll 4
-      for (int r = 0; r < ATB_R; ++r) {
-        double a[8], b[8];
-        // 4 x LDS.128 per operand; 8 lanes of a phase read 128 contiguous bytes (no conflicts)
+    for (int r = 0; r < ATB_R; ++r) {
+      double a[8], b[8];
+      // 4 x LDS.128 per operand; 8 lanes of a phase read 128 contiguous bytes (no conflicts)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double2 va = *reinterpret_cast<const double2*>(&As[buf][r][q * 16 + ty * 2]);
-          double2 vb = *reinterpret_cast<const double2*>(&Bs[buf][r][q * 16 + tx * 2]);
-          a[2 * q] = va.x; a[2 * q + 1] = va.y;
-          b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i % kAccRegs][j % (kAccRegs == 8 ? 8 : 1)] =
-              fma(a[i], b[j], acc[i % kAccRegs][j % (kAccRegs == 8 ? 8 : 1)]);
-      }
-    } else {
-      float part[8][8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) part[i][j] = 0.f;
-#pragma unroll 4
-      for (int r = 0; r < ATB_R; ++r) {
-        float a[8], b[8];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          float4 va = *reinterpret_cast<const float4*>(&As[buf][r][q * 32 + ty * 4]);
-          float4 vb = *reinterpret_cast<const float4*>(&Bs[buf][r][q * 32 + tx * 4]);
-          a[4 * q] = va.x; a[4 * q + 1] = va.y; a[4 * q + 2] = va.z; a[4 * q + 3] = va.w;
-          b[4 * q] = vb.x; b[4 * q + 1] = vb.y; b[4 * q + 2] = vb.z; b[4 * q + 3] = vb.w;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) part[i][j] = fmaf(a[i], b[j], part[i][j]);
+      for (int q = 0; q < 4; ++q) {
+        double2 va = *reinterpret_cast<const double2*>(&As[buf][r][q * 16 + ty * 2]);
+        double2 vb = *reinterpret_cast<const double2*>(&Bs[buf][r][q * 16 + tx * 2]);
+        a[2 * q] = va.x; a[2 * q + 1] = va.y;
+        b[2 * q] = vb.x; b[2 * q + 1] = vb.y;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) accs[i * 8 + j][tid] += (double)part[i][j];
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
     if (st + 1 < nst) store(buf ^ 1);
     __syncthreads();
   }
   // partial tile -> ws[chunk][a][b]  (ws_ld = padded Kb).  Register element (i, j) of thread
   // (tx, ty) is tile row rowmap(ty, i), column rowmap(tx, j).
-  auto tmap = [](int t, int q) { return sizeof(S) == 8 ? (q >> 1) * 16 + t * 2 + (q & 1) : (q >> 2) * 32 + t * 4 + (q & 3); };
+  auto tmap = [](int t, int q) { return (q >> 1) * 16 + t * 2 + (q & 1); };
   double* W = ws + chunk * (int64_t)((Ka + ATB_T - 1) / ATB_T * ATB_T) * ws_ld;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      double v;
-      if constexpr (sizeof(S) == 8) v = acc[i][j];
-      else v = accs[i * 8 + j][tid];
+      const double v = acc[i][j];
       W[(a0 + tmap(ty, i)) * ws_ld + b0 + tmap(tx, j)] = v;
     }
 }
@@ -844,15 +797,12 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
   if (rows > 0) {
     dim3 grid((unsigned)ntiles, (unsigned)ch);
     ++g_launches;
-    if (f32_stage)
-      atb_kernel<float><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
-                                                      (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
-    else if (atb_dmma_enabled())
+    if (atb_dmma_enabled())
       atb_dmma_kernel<<<grid, ATBD_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
                                                      (int)ta, (int)tb, rpc, ws, ws_ld, gate);
     else
-      atb_kernel<double><<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
-                                                       (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
+      atb_kernel<<<grid, ATB_THREADS, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric ? 1 : 0,
+                                               (int)ta, (int)tb, rpc, ws, ws_ld, gate, 0);
   } else {
     cudaMemsetAsync(ws, 0, sizeof(double) * ka_pad * ws_ld, st);
     ch = 1;
