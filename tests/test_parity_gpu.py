@@ -345,3 +345,43 @@ def test_tc_products_mode_parity():
                        cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "4 passed" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.skipif(__import__("os").environ.get("ISVD_ALT_PATHS") == "1", reason="already the child run")
+def test_alternative_kernel_paths_parity():
+    """The switchable alternatives stay in parity: DFMA exact Gram (ISVD_DMMA=0), pairwise
+    cooperative Jacobi (ISVD_JACOBI_PAIRWISE=1), SIMT Grams (ISVD_TC_GRAM=0), no allocator cache
+    (ISVD_NO_POOL=1) -- all at once, configs 2 (NC, l = 256) and 3 (NE, l = 160), in a child
+    process (some switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.abspath(__file__)
+    ids = [f"{here}::test_isvd_parity[2]", f"{here}::test_isvd_parity[3]", f"{here}::test_products[orthonormal-2]"]
+    env = dict(os.environ, ISVD_ALT_PATHS="1", ISVD_DMMA="0", ISVD_JACOBI_PAIRWISE="1", ISVD_TC_GRAM="0",
+               ISVD_NO_POOL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
+                       cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout, r.stdout[-2000:]
+
+
+def test_allocator_cache_reuse_is_exact(ctx):
+    """Graphs and operators rebuilt from the context's buffer cache give bitwise-identical
+    results (workspaces are re-zeroed on reuse)."""
+    import paper_2111_06312_b200 as isvd
+
+    cfg, g, X, sp = config_inputs(0)
+    p = -1 if cfg["p"] is None else cfg["p"]
+    outs = []
+    for _ in range(3):
+        graph = isvd.Graph(ctx, g.n, g.row_ptr, g.col_idx)
+        op = isvd.NE(graph, sp["weights"], sp["lambda_ones"])
+        r = op.svd(sp["k"], p, sp["q"], sp["seed"])
+        outs.append((r.S.copy(), _to_np(r.U)))
+        op.close()
+        graph.close()
+    for S, U in outs[1:]:
+        assert np.array_equal(S, outs[0][0])
+        assert np.array_equal(U, outs[0][1])
