@@ -568,12 +568,14 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   static_assert(TN == 8 || TN == 16, "columns per thread");
   constexpr int TY = BM / TM, TX = BN / TN, NT = TX * TY;
   constexpr int QN = TN / 4, CS = BN / QN;  // thread column groups: tx*4 + q*CS, q < QN
-  constexpr int A4 = kF32Stage * BM / 4, B4 = kF32Stage * BN / 4;  // float4 per stage
-  // cp.async ring depth: 3 stages where they fit the 48 KB of static shared memory
-  constexpr int kF32Ring = 3 * (kF32Stage * (BM + BN) + kF32Stage) * 4 <= 48 * 1024 ? 3 : 2;
-  __shared__ __align__(16) float As[kF32Ring][kF32Stage][BM];
-  __shared__ __align__(16) float Bs[kF32Ring][kF32Stage][BN];
-  __shared__ __align__(16) float Ss[kF32Ring][kF32Stage];  // row scales of the stage (applied to A)
+  // rows per stage: 32 where two stages fit the 48 KB of static shared memory (half the CTA
+  // barriers of 16-row stages), else 16; ring depth 3 where it fits, else 2
+  constexpr int SR = 2 * (32 * (BM + BN) + 32) * 4 <= 48 * 1024 ? 32 : kF32Stage;
+  constexpr int A4 = SR * BM / 4, B4 = SR * BN / 4;  // float4 per stage
+  constexpr int kF32Ring = 3 * (SR * (BM + BN) + SR) * 4 <= 48 * 1024 ? 3 : 2;
+  __shared__ __align__(16) float As[kF32Ring][SR][BM];
+  __shared__ __align__(16) float Bs[kF32Ring][SR][BN];
+  __shared__ __align__(16) float Ss[kF32Ring][SR];  // row scales of the stage (applied to A)
   const int tid = threadIdx.x;
   int tx, ty;
   thread_xy<TX>(tid, &tx, &ty);
@@ -585,7 +587,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   // columns outside the operands are zero-filled
   auto issue = [&](int64_t s) {
     const int slot = (int)(s % kF32Ring);
-    const int64_t r0 = r_begin + s * kF32Stage;
+    const int64_t r0 = r_begin + s * SR;
     for (int f = tid; f < A4 + B4; f += NT) {
       if (f < A4) {
         const int rr = f / (BM / 4), cc = (f % (BM / 4)) * 4;
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
         cp_async16(&Bs[slot][rr][cc], ok ? B + gr * ldb + b0 + cc : B, ok ? 16 : 0);
       }
     }
-    if (row_scale && tid < kF32Stage) {
+    if (row_scale && tid < SR) {
       const int64_t gr = r0 + tid;
       Ss[slot][tid] = gr < r_end ? __ldg(row_scale + gr) : 0.f;
     }
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  const int64_t nst = (r_end - r_begin + kF32Stage - 1) / kF32Stage;
+  const int64_t nst = (r_end - r_begin + SR - 1) / SR;
 #pragma unroll
   for (int s = 0; s < kF32Ring - 1; ++s) {
     if (s < nst) issue(s);
@@ -623,7 +625,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     cp_async_commit();
     const int buf = (int)(s % kF32Ring);
 #pragma unroll
-    for (int kk = 0; kk < kF32Stage; ++kk) {
+    for (int kk = 0; kk < SR; ++kk) {
       float a[TM];
       const float sc = row_scale ? Ss[buf][kk] : 1.f;
 #pragma unroll
