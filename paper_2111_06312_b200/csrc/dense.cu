@@ -521,10 +521,16 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
                            const int* gate, cudaStream_t st, const int32_t* out_map) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (N > 64 && round_up(N, 80) < round_up(N, 128)) {  // e.g. N = 400: 5 x 80 instead of 4 x 128
+    // 16-deep K stages halve the CTA barriers for long K (Y R^-1: 12.0 -> 11.7 ms at config 4);
+    // for short K (X G_j, K = d = 100) the 8-deep ones waste less on the ragged last stage
     dim3 grid((unsigned)ceil_div(N, 80), (unsigned)ceil_div(M, 128));
     ++g_launches;
-    gemm_tn_kernel<128, 80, 8, 8, 8><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                         upper_tri_b ? 1 : 0, gate, out_map);
+    if (K >= 256)
+      gemm_tn_kernel<128, 80, 16, 8, 8><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                             upper_tri_b ? 1 : 0, gate, out_map);
+    else
+      gemm_tn_kernel<128, 80, 8, 8, 8><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                            upper_tri_b ? 1 : 0, gate, out_map);
   } else if (N > 64) {
     dim3 grid((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
