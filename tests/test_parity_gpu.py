@@ -351,7 +351,7 @@ def test_tc_products_mode_parity():
 def test_alternative_kernel_paths_parity():
     """The switchable alternatives stay in parity: DFMA exact Gram (ISVD_DMMA=0), pairwise
     cooperative Jacobi (ISVD_JACOBI_PAIRWISE=1), SIMT Grams (ISVD_TC_GRAM=0), no allocator cache
-    (ISVD_NO_POOL=1) -- all at once, configs 2 (NC, l = 256) and 3 (NE, l = 160), in a child
+    (ISVD_NO_POOL=1), NC dense terms overlapped on a second stream (ISVD_OVERLAP=1) -- all at once, configs 2 (NC, l = 256) and 3 (NE, l = 160), in a child
     process (some switches are read once per process)."""
     import os
     import subprocess
@@ -360,7 +360,7 @@ def test_alternative_kernel_paths_parity():
     here = os.path.abspath(__file__)
     ids = [f"{here}::test_isvd_parity[2]", f"{here}::test_isvd_parity[3]", f"{here}::test_products[orthonormal-2]"]
     env = dict(os.environ, ISVD_ALT_PATHS="1", ISVD_DMMA="0", ISVD_JACOBI_PAIRWISE="1", ISVD_TC_GRAM="0",
-               ISVD_NO_POOL="1")
+               ISVD_NO_POOL="1", ISVD_OVERLAP="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
                        cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
