@@ -27,6 +27,7 @@ SOURCES = [
     ("dense.cu", []),
     ("gram_tc.cu", []),
     ("gemm_tc.cu", []),
+    ("graph_build.cu", []),
     ("smallmat.cu", []),
     ("capi.cpp", []),
 ]

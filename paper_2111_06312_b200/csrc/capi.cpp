@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -812,6 +813,16 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     REQ(rb == row_begin && nl == n_local, ISVD_ERR_INVALID_ARG,
         "row partition must equal isvd_partition(n, world, rank)");
     const bool dev = flags & ISVD_PTR_DEVICE;
+    // ISVD_TRACE=1: host-side phase times of the graph build on stderr
+    static const bool trace = getenv("ISVD_TRACE") && getenv("ISVD_TRACE")[0] == '1';
+    auto t_last = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+      if (!trace) return;
+      auto t = std::chrono::steady_clock::now();
+      fprintf(stderr, "[isvd] graph_create %-10s %8.2f ms\n", name,
+              std::chrono::duration<double, std::milli>(t - t_last).count());
+      t_last = t;
+    };
     std::vector<int64_t> rp(n_local + 1);
     if (dev) CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
     else memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1));
@@ -848,36 +859,32 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       for (int64_t e = 0; e < nnz; ++e)
         REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
     }
+    phase("csr_upload");
     // Degree relabelling (single rank, large graphs; SURVEY 8(d2) "allowed optimisation"):
     // internal row t is caller row order[t], in decreasing degree, so the hub rows that take
     // most gathers form one contiguous prefix of every iterate, which the SpMM marks
     // L2-persisting.  A symmetric permutation of A: singular values are unchanged and every
     // caller-ordered input/output is mapped at the boundary (X, Omega, U, V, matmul I/O).
     // The order is computed on the host from the degrees; the index renaming runs on the GPU.
+    int64_t maxd = 0;
+    for (int64_t i = 0; i < n_local; ++i) maxd = std::max(maxd, rp[i + 1] - rp[i]);
+    g->max_deg = maxd;
+    // row_ptr of the caller's order on the device (the relabelling and the plan read it there)
+    int64_t* d_rp_in = relabel ? (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp) : g->row_ptr;
+    CK(cudaMemcpyAsync(d_rp_in, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice, ctx->stream));
+    const size_t temp_bytes = graph_build_temp_bytes(n_local);
+    void* temp = dmalloc(ctx, temp_bytes, tmp);
     if (relabel) {
-      // stable counting sort by decreasing degree: O(n + max degree)
-      std::vector<int32_t> order(n_local), new_of_old(n_local);
-      int64_t dmax = 0;
-      for (int64_t i = 0; i < n_local; ++i) dmax = std::max(dmax, rp[i + 1] - rp[i]);
-      std::vector<int64_t> start(dmax + 2, 0);
-      for (int64_t i = 0; i < n_local; ++i) ++start[dmax - (rp[i + 1] - rp[i]) + 1];
-      for (int64_t b = 1; b <= dmax + 1; ++b) start[b] += start[b - 1];
-      for (int64_t i = 0; i < n_local; ++i) order[start[dmax - (rp[i + 1] - rp[i])]++] = (int32_t)i;
-      for (int64_t t = 0; t < n_local; ++t) new_of_old[order[t]] = (int32_t)t;
-      std::vector<int64_t> rp2(n_local + 1);
-      rp2[0] = 0;
-      for (int64_t t = 0; t < n_local; ++t) rp2[t + 1] = rp2[t] + (rp[order[t] + 1] - rp[order[t]]);
-      int64_t* d_rp_old = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+      // stable sort by decreasing degree (device radix sort), maps, new row_ptr, renamed indices
+      uint32_t* keys2 = (uint32_t*)dmalloc(ctx, sizeof(uint32_t) * 2 * n_local, tmp);
+      int32_t* idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, tmp);
+      int64_t* deg_tmp = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
       int32_t* d_new_of_old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, tmp);
       g->new2old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, g->allocs);
-      CK(cudaMemcpy(d_rp_old, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(d_new_of_old, new_of_old.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(g->new2old, order.data(), sizeof(int32_t) * n_local, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(g->row_ptr, rp2.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
-      CK(launch_relabel_csr(d_rp_old, ci_in, g->new2old, d_new_of_old, g->row_ptr, g->col_idx, n_local,
+      CK(launch_degree_order(d_rp_in, n_local, keys2, idx, g->new2old, d_new_of_old, deg_tmp, g->row_ptr, temp,
+                             temp_bytes, ctx->stream));
+      CK(launch_relabel_csr(d_rp_in, ci_in, g->new2old, d_new_of_old, g->row_ptr, g->col_idx, n_local,
                             ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      rp.swap(rp2);
       if (ctx->max_persist_l2 > 0) {
         static bool limit_set = false;  // process-wide L2 set-aside for persisting accesses
         if (!limit_set) {
@@ -885,80 +892,47 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
           limit_set = true;
         }
       }
-    } else {
-      CK(cudaMemcpy(g->row_ptr, rp.data(), sizeof(int64_t) * (n_local + 1), cudaMemcpyHostToDevice));
     }
+    phase("relabel");
     // degrees (integers) -> scale vectors computed once in fp64, stored fp32 (reading O3)
-    std::vector<float> inv(n_local), s(n_local), s2(n_local), rs(n_local);
-    int64_t maxd = 0;
-    for (int64_t i = 0; i < n_local; ++i) {
-      int64_t d = rp[i + 1] - rp[i];
-      maxd = std::max(maxd, d);
-      inv[i] = d > 0 ? (float)(1.0 / (double)d) : 0.f;
-      s[i] = (float)(1.0 / std::sqrt((double)d + 1.0));
-      s2[i] = (float)(1.0 / ((double)d + 1.0));
-      rs[i] = (float)std::sqrt((double)d + 1.0);
-    }
-    g->max_deg = maxd;
     size_t nb = sizeof(float) * std::max<int64_t>(n_local, 1);
     g->inv_deg = (float*)dmalloc(ctx, nb, g->allocs);
     g->s = (float*)dmalloc(ctx, nb, g->allocs);
     g->s2 = (float*)dmalloc(ctx, nb, g->allocs);
     g->rs = (float*)dmalloc(ctx, nb, g->allocs);
-    if (n_local > 0) {
-      CK(cudaMemcpy(g->inv_deg, inv.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(g->s, s.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(g->s2, s2.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(g->rs, rs.data(), sizeof(float) * n_local, cudaMemcpyHostToDevice));
-    }
+    CK(launch_scales(g->row_ptr, n_local, g->inv_deg, g->s, g->s2, g->rs, ctx->stream));
+    phase("scales");
     // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
-    // split, their partial sums combined by the fixup pass in segment order.
-    std::vector<int32_t> seg_row, seg_len, seg_slot, split_row, split_slot0, split_nslot;
-    std::vector<int64_t> seg_beg;
-    seg_row.reserve(n_local);
-    int32_t slots = 0;
-    for (int64_t i = 0; i < n_local; ++i) {
-      int64_t d = rp[i + 1] - rp[i];
-      if (d <= kSegEdges) {
-        seg_row.push_back((int32_t)i);
-        seg_beg.push_back(rp[i]);
-        seg_len.push_back((int32_t)d);
-        seg_slot.push_back(-1);
-      } else {
-        int32_t ns = (int32_t)((d + kSegEdges - 1) / kSegEdges);
-        split_row.push_back((int32_t)i);
-        split_slot0.push_back(slots);
-        split_nslot.push_back(ns);
-        for (int32_t t = 0; t < ns; ++t) {
-          int64_t b = rp[i] + (int64_t)t * kSegEdges;
-          int64_t e = std::min(rp[i + 1], b + kSegEdges);
-          seg_row.push_back((int32_t)i);
-          seg_beg.push_back(b);
-          seg_len.push_back((int32_t)(e - b));
-          seg_slot.push_back(slots + t);
-        }
-        slots += ns;
-      }
-    }
+    // split, their partial sums combined by the fixup pass in segment order (graph_build.cu)
+    int64_t* nseg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+    int64_t* seg_off = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+    int32_t* cnt32 = (int32_t*)dmalloc(ctx, sizeof(int32_t) * 4 * (n_local + 1), tmp);
+    int32_t *nsplit = cnt32, *nslot = cnt32 + (n_local + 1), *split_off = cnt32 + 2 * (n_local + 1),
+            *slot_off = cnt32 + 3 * (n_local + 1);
+    CK(launch_plan_count(g->row_ptr, n_local, nseg, nsplit, nslot, seg_off, split_off, slot_off, temp, temp_bytes,
+                         ctx->stream));
+    int64_t tot_seg = 0;
+    int32_t tot_split = 0, tot_slot = 0;
+    CK(cudaMemcpyAsync(&tot_seg, seg_off + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&tot_split, split_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&tot_slot, slot_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     SpmmPlan& p = g->plan;
     p.n_local = n_local;
-    p.n_seg = (int64_t)seg_row.size();
-    p.n_split_rows = (int64_t)split_row.size();
-    p.n_slots = slots;
-    auto up32 = [&](const std::vector<int32_t>& v) {
-      int32_t* d = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<size_t>(v.size(), 1), g->allocs);
-      if (!v.empty()) CK(cudaMemcpy(d, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice));
-      return d;
-    };
-    p.seg_row = up32(seg_row);
-    p.seg_len = up32(seg_len);
-    p.seg_slot = up32(seg_slot);
-    p.split_row = up32(split_row);
-    p.split_slot0 = up32(split_slot0);
-    p.split_nslot = up32(split_nslot);
-    p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<size_t>(seg_beg.size(), 1), g->allocs);
-    if (!seg_beg.empty())
-      CK(cudaMemcpy(p.seg_beg, seg_beg.data(), sizeof(int64_t) * seg_beg.size(), cudaMemcpyHostToDevice));
+    p.n_seg = tot_seg;
+    p.n_split_rows = tot_split;
+    p.n_slots = tot_slot;
+    auto d32 = [&](int64_t n) { return (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(n, 1), g->allocs); };
+    p.seg_row = d32(tot_seg);
+    p.seg_len = d32(tot_seg);
+    p.seg_slot = d32(tot_seg);
+    p.split_row = d32(tot_split);
+    p.split_slot0 = d32(tot_split);
+    p.split_nslot = d32(tot_split);
+    p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<int64_t>(tot_seg, 1), g->allocs);
+    CK(launch_plan_fill(g->row_ptr, n_local, seg_off, split_off, slot_off, p, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    phase("plan");
   });
   if (st != ISVD_OK) {
     for (void* p : g->allocs) dfree(ctx, p);

@@ -109,6 +109,19 @@ int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
 cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const int32_t* order,
                                const int32_t* new_of_old, const int64_t* rp_new, int32_t* ci_new, int64_t n,
                                cudaStream_t st);
+// Device-side graph build (graph_build.cu): degree order (stable, decreasing degree) with its
+// maps and the relabelled row_ptr; fp64-derived scale vectors; SpMM segment plan (count + scan,
+// then fill once the host has read the totals).  temp: graph_build_temp_bytes(n) bytes.
+size_t graph_build_temp_bytes(int64_t n);
+cudaError_t launch_degree_order(const int64_t* rp, int64_t n, uint32_t* keys2, int32_t* idx, int32_t* order,
+                                int32_t* new_of_old, int64_t* deg_tmp, int64_t* rp_new, void* temp, size_t temp_bytes,
+                                cudaStream_t st);
+cudaError_t launch_scales(const int64_t* rp, int64_t n, float* inv, float* s, float* s2, float* rs, cudaStream_t st);
+cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32_t* nsplit, int32_t* nslot,
+                              int64_t* seg_off, int32_t* split_off, int32_t* slot_off, void* temp, size_t temp_bytes,
+                              cudaStream_t st);
+cudaError_t launch_plan_fill(const int64_t* rp, int64_t n, const int64_t* seg_off, const int32_t* split_off,
+                             const int32_t* slot_off, const SpmmPlan& p, cudaStream_t st);
 // `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled
 // graph) are marked L2-persisting for this launch (cudaAccessPolicyWindow on `st`).
 // col_block > 0: process the columns in blocks of that width (one launch each).

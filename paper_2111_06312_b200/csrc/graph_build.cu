@@ -1,0 +1,142 @@
+// Device-side graph build for isvd_graph_create: degree relabelling order, fp64-derived scale
+// vectors and the SpMM segment plan, computed from the device row_ptr (so the host neither sorts
+// nor uploads O(n) arrays).  Results are identical to the host formulation they replace:
+//   * order: stable sort by decreasing degree (CUB radix sort of 0xFFFFFFFF - degree, which is
+//     stable) -- the same permutation as a stable counting sort;
+//   * scales: 1/d, (d+1)^-1/2, (d+1)^-1, (d+1)^1/2 computed in fp64 (IEEE division / sqrt, as on
+//     the host) and rounded to fp32 (reading O3);
+//   * plan: rows of <= kSegEdges edges are one segment, longer rows ceil(d / kSegEdges) segments
+//     whose partial sums go to consecutive slots, slots numbered in row order.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace isvd {
+namespace {
+
+__global__ void degree_keys_kernel(const int64_t* __restrict__ rp, int64_t n, uint32_t* __restrict__ keys,
+                                   int32_t* __restrict__ idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = 0xFFFFFFFFu - (uint32_t)(rp[i + 1] - rp[i]);
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void relabel_maps_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ order, int64_t n,
+                                    int32_t* __restrict__ new_of_old, int64_t* __restrict__ deg_new) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t == n) {
+      deg_new[n] = 0;
+      continue;
+    }
+    const int32_t o = order[t];
+    new_of_old[o] = (int32_t)t;
+    deg_new[t] = rp[o + 1] - rp[o];
+  }
+}
+
+__global__ void scales_kernel(const int64_t* __restrict__ rp, int64_t n, float* __restrict__ inv,
+                              float* __restrict__ s, float* __restrict__ s2, float* __restrict__ rs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)(rp[i + 1] - rp[i]);
+    inv[i] = d > 0.0 ? (float)(1.0 / d) : 0.f;
+    s[i] = (float)(1.0 / sqrt(d + 1.0));
+    s2[i] = (float)(1.0 / (d + 1.0));
+    rs[i] = (float)sqrt(d + 1.0);
+  }
+}
+
+__global__ void plan_count_kernel(const int64_t* __restrict__ rp, int64_t n, int64_t* __restrict__ nseg,
+                                  int32_t* __restrict__ nsplit, int32_t* __restrict__ nslot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == n) {
+      nseg[n] = 0; nsplit[n] = 0; nslot[n] = 0;
+      continue;
+    }
+    const int64_t d = rp[i + 1] - rp[i];
+    const bool split = d > kSegEdges;
+    const int64_t ns = split ? (d + kSegEdges - 1) / kSegEdges : 1;
+    nseg[i] = ns;
+    nsplit[i] = split ? 1 : 0;
+    nslot[i] = split ? (int32_t)ns : 0;
+  }
+}
+
+__global__ void plan_fill_kernel(const int64_t* __restrict__ rp, int64_t n, const int64_t* __restrict__ seg_off,
+                                 const int32_t* __restrict__ split_off, const int32_t* __restrict__ slot_off,
+                                 SpmmPlan p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = rp[i], e0 = rp[i + 1], d = e0 - b0;
+    const int64_t s0 = seg_off[i];
+    if (d <= kSegEdges) {
+      p.seg_row[s0] = (int32_t)i;
+      p.seg_beg[s0] = b0;
+      p.seg_len[s0] = (int32_t)d;
+      p.seg_slot[s0] = -1;
+    } else {
+      const int32_t ns = (int32_t)((d + kSegEdges - 1) / kSegEdges), slot0 = slot_off[i], r = split_off[i];
+      p.split_row[r] = (int32_t)i;
+      p.split_slot0[r] = slot0;
+      p.split_nslot[r] = ns;
+      for (int32_t t = 0; t < ns; ++t) {
+        const int64_t b = b0 + (int64_t)t * kSegEdges;
+        const int64_t e = b + kSegEdges < e0 ? b + kSegEdges : e0;
+        p.seg_row[s0 + t] = (int32_t)i;
+        p.seg_beg[s0 + t] = b;
+        p.seg_len[s0 + t] = (int32_t)(e - b);
+        p.seg_slot[s0 + t] = slot0 + t;
+      }
+    }
+  }
+}
+
+unsigned grid_n(int64_t n) { return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n + 1, 256), 1), 148 * 16); }
+
+}  // namespace
+
+size_t graph_build_temp_bytes(int64_t n) {
+  size_t a = 0, b = 0, c = 0, d = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)n);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int64_t*)nullptr, (int64_t*)nullptr, (int)(n + 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, (int)(n + 1));
+  d = std::max(std::max(a, b), c);
+  return d + 256;
+}
+
+cudaError_t launch_degree_order(const int64_t* rp, int64_t n, uint32_t* keys2, int32_t* idx, int32_t* order,
+                                int32_t* new_of_old, int64_t* deg_tmp, int64_t* rp_new, void* temp, size_t temp_bytes,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; degree_keys_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, keys2, idx);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys2, keys2 + n, idx, order, (int)n, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  ++g_launches; relabel_maps_kernel<<<grid_n(n), 256, 0, st>>>(rp, order, n, new_of_old, deg_tmp);
+  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, deg_tmp, rp_new, (int)(n + 1), st);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_scales(const int64_t* rp, int64_t n, float* inv, float* s, float* s2, float* rs, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; scales_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, inv, s, s2, rs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32_t* nsplit, int32_t* nslot,
+                              int64_t* seg_off, int32_t* split_off, int32_t* slot_off, void* temp, size_t temp_bytes,
+                              cudaStream_t st) {
+  ++g_launches; plan_count_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, nseg, nsplit, nslot);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nseg, seg_off, (int)(n + 1), st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nsplit, split_off, (int)(n + 1), st);
+  if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nslot, slot_off, (int)(n + 1), st);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_plan_fill(const int64_t* rp, int64_t n, const int64_t* seg_off, const int32_t* split_off,
+                             const int32_t* slot_off, const SpmmPlan& p, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; plan_fill_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, seg_off, split_off, slot_off, p);
+  return cudaGetLastError();
+}
+
+}  // namespace isvd
