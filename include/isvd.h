@@ -136,8 +136,9 @@ typedef struct {
                              Fig. 1 uses (C-q+1)/(C(C+1)/2) (reading O1).  NC: NULL. */
   double lambda_ones;     /* NE: coefficient of the rank-1 term -lambda 1 1^T (Eq. 3, P:145;
                              configs: 1/n).  Applied matrix-free in fp64.           */
-  double lambda_adj;      /* NE: coefficient of +lambda A (Eq. 3's -lambda(1 - A)); must be 0
-                             in this build (ISVD_ERR_UNSUPPORTED otherwise).  */
+  double lambda_adj;      /* NE: coefficient of +lambda A (Eq. 3's -lambda (1 1^T - A), P:145;
+                             the configs use 0).  Applied as one extra SpMM of Q per product,
+                             added in the last Horner step's epilogue.       */
   const float* X;         /* NC: this rank's rows of X, n_local x d, row-major, leading dim ldx */
   int64_t d, ldx;         /* NC: feature width d (>= 1) and leading dimension (multiple of 4) */
   uint32_t x_flags;       /* NC: ISVD_PTR_DEVICE and/or ISVD_BORROW                           */

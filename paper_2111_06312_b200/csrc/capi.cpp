@@ -110,6 +110,7 @@ struct isvd_op_s {
   int terms = 0;
   std::vector<double> w;
   double lambda_ones = 0.0;
+  double lambda_adj = 0.0;  // NE: coefficient of the +lambda A term (Eq. 3)
   const float* X = nullptr;
   int64_t d = 0, ldx = 0;
   bool own_x = false;
@@ -119,6 +120,7 @@ struct isvd_op_s {
   float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
   float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
+  float* adjbuf = nullptr;  // NE with lambda_adj != 0: lambda_adj A Q (internal row order)
   SolverWs sws;
 };
 
@@ -279,6 +281,9 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
   op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
                               op->ws_allocs);
+  op->adjbuf = op->lambda_adj != 0.0
+                   ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs)
+                   : nullptr;
   int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
   op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
   op->ws_wpad = wpad;
@@ -388,6 +393,18 @@ float* slice(const isvd_graph_s* g, float* full, int64_t ld) { return full + (si
 // M Q = sum_c w_c T^c Q - lambda 1 (1^T Q), T = D^-1 A   (Eq. 3)
 // Horner: H_C = w_C Q; H_c = w_c Q + D^-1 A H_{c+1}; M Q = D^-1 A H_1 - lambda 1 cs^T.
 // user_order: Q and out are in the caller's row order (relabelled graphs map at the boundary).
+// The +lambda_adj A Q term of Eq. 3's -lambda (1 1^T - A): one extra SpMM step over
+// the full rows of Q into adjbuf (internal row order), added by the last Horner step's epilogue
+// (SURVEY 8(f) f1).  A is symmetric, so M^T takes the same term.
+void ne_adj_term(isvd_ctx ctx, isvd_op op, const float* qfull, int64_t ldq, int64_t wpad) {
+  isvd_graph g = op->g;
+  SpmmArgs a = spmm_base(g, wpad);
+  a.Y = qfull; a.ldy = ldq;
+  a.post_coef = (float)op->lambda_adj;
+  a.out = op->adjbuf; a.ldo = wpad;
+  spmm(ctx, op, a);
+}
+
 void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
                bool user_order) {
   isvd_graph g = op->g;
@@ -410,6 +427,7 @@ void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out
     src = op->full_a;
     lds = wpad;
   }
+  if (op->adjbuf) ne_adj_term(ctx, op, src, lds, wpad);  // adjbuf = lambda_adj A Q
   float* bufs[2] = {op->full_b, op->full_c};
   for (int c = C - 1; c >= 1; --c) {
     float* dst_full = bufs[c & 1];
@@ -429,6 +447,7 @@ void ne_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out
   a.post_vec = g->inv_deg;
   a.post_coef = (C == 1) ? (float)op->w[0] : 1.f;
   a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
+  if (op->adjbuf) { a.T = op->adjbuf; a.ldt = wpad; }
   a.out = out; a.ldo = ldo; a.out_map = omap;
   spmm(ctx, op, a);
 }
@@ -447,6 +466,18 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
     Q = op->ptmp;
     ldq = wpad;
     omap = g->new2old;
+  }
+  if (op->adjbuf) {  // A^T = A (symmetric): the same lambda_adj A Q, gathered from Q's full rows
+    const float* qf = Q;
+    int64_t ldqf = ldq;
+    if (ctx->dist) {
+      CK(launch_scale_rows(Q, ldq, slice(g, op->full_b, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr,
+                           ctx->stream));
+      allgather_rows(ctx, g, op->full_b, wpad);
+      qf = op->full_b;
+      ldqf = wpad;
+    }
+    ne_adj_term(ctx, op, qf, ldqf, wpad);
   }
   CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, g->inv_deg, (float)op->w[C - 1],
                        nullptr, ctx->stream));
@@ -467,6 +498,7 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   SpmmArgs a = spmm_base(g, wpad);
   a.Y = src; a.ldy = wpad;
   a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
+  if (op->adjbuf) { a.T = op->adjbuf; a.ldt = wpad; }
   a.out = out; a.ldo = ldo; a.out_map = omap;
   spmm(ctx, op, a);
 }
@@ -980,11 +1012,12 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
     if (desc->kind == ISVD_OP_POWER_SUM) {
       REQ(desc->num_terms >= 1, ISVD_ERR_INVALID_ARG, "NE needs C >= 1 powers");
       REQ(desc->weights != nullptr, ISVD_ERR_INVALID_ARG, "NE weights are null");
-      REQ(desc->lambda_adj == 0.0, ISVD_ERR_UNSUPPORTED, "lambda_adj != 0 (the +lambda A term) is not built yet");
       op->w.assign(desc->weights, desc->weights + desc->num_terms);
       for (double x : op->w) REQ(std::isfinite(x), ISVD_ERR_NONFINITE, "non-finite weight");
-      REQ(std::isfinite(desc->lambda_ones), ISVD_ERR_NONFINITE, "non-finite lambda");
+      REQ(std::isfinite(desc->lambda_ones) && std::isfinite(desc->lambda_adj), ISVD_ERR_NONFINITE,
+          "non-finite lambda");
       op->lambda_ones = desc->lambda_ones;
+      op->lambda_adj = desc->lambda_adj;
     } else if (desc->kind == ISVD_OP_STACKED_PROPAGATION) {
       REQ(desc->num_terms >= 0, ISVD_ERR_INVALID_ARG, "NC needs L >= 0");
       REQ(desc->d >= 1, ISVD_ERR_INVALID_ARG, "NC feature width d must be >= 1");

@@ -385,3 +385,36 @@ def test_allocator_cache_reuse_is_exact(ctx):
     for S, U in outs[1:]:
         assert np.array_equal(S, outs[0][0])
         assert np.array_equal(U, outs[0][1])
+
+
+# --------------------------------------------- paper-exact NE: +lambda A, Fig. 1 weights
+
+
+@pytest.mark.parametrize("i", [0, 1])
+def test_ne_paper_exact_lambda_adj_and_fig1_weights(ctx, i):
+    """Eq. 3 as printed: M = sum_c w_c T^c - lambda (1 1^T - A) with the Fig. 1 triangular weights
+     -- the +lambda A term is one extra SpMM of Q in the library.  Products and the isvd
+    against the oracle's NEOperator(lambda_adj = lambda)."""
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import NEOperator, adjacency, context_weights, isvd, philox_omega
+
+    cfg, g, X, sp = config_inputs(i)
+    C = len(sp["weights"])
+    w = context_weights(C)
+    lam = sp["lambda_ones"]
+    A = adjacency(g.n, g.row_ptr, g.col_idx)
+    ref = NEOperator(A, w, lam, lambda_adj=lam)
+    graph = isvd_mod.Graph(ctx, g.n, g.row_ptr, g.col_idx)
+    op = isvd_mod.NE(graph, w, lam, lambda_adj=lam)
+    rng = np.random.default_rng(77 + i)
+    Q = rng.standard_normal((g.n, sp["l"])).astype(np.float32)
+    Y = _to_np(op.matmul(torch.from_numpy(Q).cuda()))
+    assert rel_fro(Y, ref.matmul(Q.astype(np.float64))) <= PROD_TOL
+    W = _to_np(op.matmul_T(torch.from_numpy(Q).cuda()))
+    assert rel_fro(W, ref.matmul_T(Q.astype(np.float64))) <= PROD_TOL
+    p = -1 if cfg["p"] is None else cfg["p"]
+    res = op.svd(sp["k"], p, sp["q"], sp["seed"])
+    om = philox_omega(sp["seed"], 0, ref.shape[1], sp["l"])
+    print(_check_isvd(res, isvd(ref, sp["k"], om, sp["q"]), sp["k"], f"cfg{i}/paper-exact"))
+    op.close()
+    graph.close()
