@@ -16,10 +16,13 @@ from .isvd_oracle import (  # noqa: F401
     NEOperator,
     adjacency,
     context_weights,
+    embeddings,
     exact_svd,
     isvd,
+    least_norm,
     orthonorm_cholesky,
     orthonorm_qr,
+    pinv_diag,
     sign_fix,
     sym_norm_adj,
     transition,

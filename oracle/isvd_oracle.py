@@ -303,3 +303,45 @@ def exact_svd_tall(blocks, k: int):
         return Mr @ V[:, :k] / s_all[:k]
 
     return s_all[:k].copy(), V[:, :k].copy(), s_all, Ufun
+
+
+# ---------------------------------------------------------------------------
+# After the SVD: embeddings (Eq. 5) and the least-norm parameters (Eq. 7)
+# ---------------------------------------------------------------------------
+
+
+def embeddings(U, s, V):
+    """L = U S^1/2, R = V S^1/2 (Eq. 5): <L_i, R_j> = (U S V^T)_ij."""
+    r = np.sqrt(np.asarray(s, dtype=np.float64))
+    return np.asarray(U, dtype=np.float64) * r, np.asarray(V, dtype=np.float64) * r
+
+
+def pinv_diag(s, n_rows: int, n_cols: int):
+    """S^+ of Eq. 7: reciprocates the non-zero entries of diag(S).  "Non-zero" is read
+    numerically (reading O24): s_i > max(n_rows, n_cols) * eps_fp64 * max(s), LAPACK/numpy's
+    default cut for a pseudoinverse."""
+    s = np.asarray(s, dtype=np.float64)
+    if s.size == 0:
+        return s.copy()
+    tol = max(n_rows, n_cols) * np.finfo(np.float64).eps * s.max()
+    out = np.zeros_like(s)
+    nz = s > tol
+    out[nz] = 1.0 / s[nz]
+    return out
+
+
+def least_norm(U, s, V, Y, rows=None, shape=None):
+    """W* = M^+ Y ~ V S^+ U^T Y (Eq. 7), multiplied right to left:
+    T = U^T Y (k x y), then S^+ T, then V (S^+ T).  ``rows`` (semi-supervised option (i),
+    P:209-210) keeps only the labelled rows of U and Y.  ``shape`` = (r, c) of M for the
+    numerical-zero cut of S^+ (default: the shapes of U and V)."""
+    U = np.asarray(U, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    if rows is not None:
+        U = U[rows]
+        Y = Y[rows]
+    r, c = shape if shape is not None else (U.shape[0], V.shape[0])
+    T = U.T @ Y
+    T = pinv_diag(s, r, c)[:, None] * T
+    return V @ T

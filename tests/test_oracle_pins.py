@@ -428,3 +428,73 @@ def test_exact_svd_tall_matches_lapack_svd():
     rows = np.arange(0, 300, 7)
     Ur = Ufun(rows)
     assert np.allclose(np.abs(np.sum(Ur * Ue[rows], axis=0)) / np.linalg.norm(Ur, axis=0) / np.linalg.norm(Ue[rows], axis=0), 1.0, atol=1e-8)
+
+
+# ---------------------------------------------------------- Eq. 5 embeddings, Eq. 7 W*
+
+
+def test_embeddings_inner_products_are_the_low_rank_matrix():
+    """<L_i, R_j> = U_i^T S V_j -- checked against the product of the factors."""
+    from oracle import embeddings
+
+    rng = np.random.default_rng(11)
+    U = rng.standard_normal((9, 3))
+    V = rng.standard_normal((7, 3))
+    s = np.array([3.0, 2.0, 0.5])
+    L, R = embeddings(U, s, V)
+    want = np.einsum("ik,k,jk->ij", U, s, V)
+    assert np.allclose(L @ R.T, want, rtol=0, atol=1e-13)
+
+
+def test_least_norm_identity_design_matrix_recovers_labels():
+    """M = I, k = n: W* = Y exactly (Theorem 1)."""
+    from oracle import exact_svd, least_norm
+
+    n = 6
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((n, 2))
+    U, s, V, _ = exact_svd(np.eye(n), n)
+    W = least_norm(U, s, V, Y)
+    assert np.allclose(W, Y, rtol=0, atol=1e-14)
+
+
+def test_least_norm_equals_lapack_minimum_norm_least_squares():
+    """Rank-deficient 12 x 5 M (rank 3), k = 5 >= rank: V S^+ U^T Y is the minimum-norm least-squares
+    solution (Theorem 1) -- the same minimiser LAPACK's gelsd (np.linalg.lstsq) returns by a
+    different algorithm; a truncated k = 3 gives it too (the cut S^+ drops the zero singular values)."""
+    from oracle import exact_svd, least_norm
+
+    rng = np.random.default_rng(5)
+    M = rng.standard_normal((12, 3)) @ rng.standard_normal((3, 5))
+    Y = rng.standard_normal((12, 4))
+    want = np.linalg.lstsq(M, Y, rcond=None)[0]
+    for k in (5, 3):
+        U, s, V, _ = exact_svd(M, k)
+        W = least_norm(U, s, V, Y, shape=M.shape)
+        assert np.allclose(W, want, rtol=0, atol=1e-12), k
+    # and the minimum norm: any other least-squares solution (add a null-space vector) is longer
+    null = np.linalg.svd(M)[2][-1]
+    assert np.linalg.norm(want) < np.linalg.norm(want + np.outer(null, np.ones(4)))
+
+
+def test_least_norm_row_subset_is_the_labelled_problem():
+    """Semi-supervised option (i): rows of U and Y restricted to the labelled set equal
+    the formula applied to the gathered rows."""
+    from oracle import least_norm
+
+    rng = np.random.default_rng(8)
+    U = np.linalg.qr(rng.standard_normal((20, 4)))[0]
+    V = np.linalg.qr(rng.standard_normal((6, 4)))[0]
+    s = np.array([5.0, 3.0, 2.0, 1.0])
+    Y = rng.standard_normal((20, 3))
+    rows = np.array([1, 4, 5, 11, 19])
+    W = least_norm(U, s, V, Y, rows=rows, shape=(20, 6))
+    want = V @ np.diag(1 / s) @ U[rows].T @ Y[rows]
+    assert np.allclose(W, want, rtol=0, atol=1e-13)
+
+
+def test_pinv_diag_cuts_numerical_zeros():
+    from oracle import pinv_diag
+
+    s = np.array([2.0, 1.0, 1e-20, 0.0])
+    assert np.array_equal(pinv_diag(s, 10, 4), [0.5, 1.0, 0.0, 0.0])
