@@ -215,6 +215,27 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* params, float* U, int64_
  * into device `omega` (this rank's c-rows x l, ld = round_up(l, 4)). */
 isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* omega, int64_t ldo);
 
+/* ---------------------------------------------------------- after the SVD
+ * Embeddings (Eq. 5): L = U S^1/2 (and R = V S^1/2 by a second call).
+ *   M: rows x k fp32 device, ld % 4 == 0; out may equal M (in place); S: host, k values >= 0.
+ *   Errors: ISVD_ERR_INVALID_ARG (null / bad ld), ISVD_ERR_NONFINITE (S < 0 or not finite). */
+isvd_status isvd_embeddings(isvd_ctx ctx, int64_t rows, int64_t k, const float* M, int64_t ldm, const double* S,
+                            float* out, int64_t ldo);
+
+/* Least-norm parameters (Eq. 7): W = V S^+ (U[rows]^T Y[rows]), multiplied right to
+ * left.  U^T Y is exact fp64 (FP64 tensor cores) over this rank's rows, all-reduced over
+ * the ranks in distributed mode; S^+ reciprocates S_i > max(r, c) eps_fp64 max(S) (reading O24);
+ * W = V (S^+ U^T Y) on the device.
+ *   U: r_local x k, Y: r_local x ny (labels, e.g. one-hot), V: v_rows x k (NE: this rank's rows,
+ *   NC: all c rows), W: v_rows x ny -- fp32 device, every ld % 4 == 0, 16-byte aligned.
+ *   rows: NULL (every row) or device int32[n_rows] of local row ids, the labelled rows
+ *   (semi-supervised option (i)).  S: host double[k].  (r, c): the shape of M.
+ *   Synchronises the ctx stream.  Errors: ISVD_ERR_INVALID_ARG, ISVD_ERR_NONFINITE. */
+isvd_status isvd_least_norm(isvd_ctx ctx, int64_t r_local, int64_t k, const float* U, int64_t ldu, const double* S,
+                            int64_t r, int64_t c, int64_t v_rows, const float* V, int64_t ldv, int64_t ny,
+                            const float* Y, int64_t ldy, const int32_t* rows, int64_t n_rows, float* W,
+                            int64_t ldw);
+
 #ifdef __cplusplus
 }
 #endif

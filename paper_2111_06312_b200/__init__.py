@@ -4,6 +4,19 @@ The product path is the CUDA library ``libisvd.so`` (sm_100a) behind the C ABI
 of ``include/isvd.h``; this package is its thin binding.  It never imports
 ``oracle/`` and has no CPU fallback.
 """
-from .api import NC, NE, Context, Graph, SvdResult, nccl_unique_id, padded, partition, round_up  # noqa: F401
+from .api import (  # noqa: F401
+    NC,
+    NE,
+    Context,
+    Graph,
+    SvdResult,
+    embeddings,
+    least_norm,
+    nccl_unique_id,
+    padded,
+    partition,
+    round_up,
+)
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "nccl_unique_id", "partition", "padded", "round_up"]
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "nccl_unique_id", "partition",
+           "padded", "round_up"]

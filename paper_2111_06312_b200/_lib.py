@@ -96,6 +96,11 @@ SIGNATURES = {
     "isvd_svd": (C.c_int, [C.c_void_p, C.POINTER(SvdParams), C.c_void_p, C.c_int64, C.POINTER(C.c_double),
                            C.c_void_p, C.c_int64, C.POINTER(SvdReport)]),
     "isvd_sample_omega": (C.c_int, [C.c_void_p, C.POINTER(SvdParams), C.c_void_p, C.c_int64]),
+    "isvd_embeddings": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                  C.POINTER(C.c_double), C.c_void_p, C.c_int64]),
+    "isvd_least_norm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_double),
+                                  C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                  C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
 }
 
 _lib = None

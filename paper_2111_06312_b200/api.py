@@ -20,7 +20,8 @@ import torch
 from . import _lib
 from ._lib import check
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "nccl_unique_id", "partition", "padded", "round_up"]
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "nccl_unique_id", "partition",
+           "padded", "round_up"]
 
 
 def round_up(x: int, m: int = 4) -> int:
@@ -308,3 +309,39 @@ class NC(_Operator):
 
     def c_rows(self) -> int:
         return self.d * (self.L + 1)
+
+
+# ------------------------------------------------------------------ after the SVD
+
+
+def embeddings(ctx: Context, M: torch.Tensor, S) -> torch.Tensor:
+    """L = U S^1/2 (or R = V S^1/2): Eq. 5, P:161-167 (isvd_embeddings)."""
+    M = _as_abi(M, ctx.device)
+    rows, k = M.shape
+    Sd = np.ascontiguousarray(S, dtype=np.float64)[:k]
+    out = padded(rows, k, ctx.device)
+    check(ctx.lib.isvd_embeddings(ctx.h, rows, k, C.c_void_p(M.data_ptr()), _ld(M),
+                                  Sd.ctypes.data_as(C.POINTER(C.c_double)), C.c_void_p(out.data_ptr()), _ld(out)),
+          "isvd_embeddings", ctx.h)
+    return out
+
+
+def least_norm(ctx: Context, U: torch.Tensor, S, V: torch.Tensor, Y: torch.Tensor, shape, rows=None) -> torch.Tensor:
+    """W* = V S^+ U^T Y (Eq. 7, P:196-206), right to left; `rows` = labelled local rows (P:209-210);
+    `shape` = (r, c) of M (isvd_least_norm)."""
+    U = _as_abi(U, ctx.device)
+    V = _as_abi(V, ctx.device)
+    Y = _as_abi(Y, ctx.device)
+    k, ny = U.shape[1], Y.shape[1]
+    Sd = np.ascontiguousarray(S, dtype=np.float64)[:k]
+    W = padded(V.shape[0], ny, ctx.device)
+    idx = None
+    if rows is not None:
+        idx = torch.as_tensor(rows, dtype=torch.int32, device=ctx.device).contiguous()
+    check(ctx.lib.isvd_least_norm(ctx.h, U.shape[0], k, C.c_void_p(U.data_ptr()), _ld(U),
+                                  Sd.ctypes.data_as(C.POINTER(C.c_double)), int(shape[0]), int(shape[1]),
+                                  V.shape[0], C.c_void_p(V.data_ptr()), _ld(V), ny, C.c_void_p(Y.data_ptr()), _ld(Y),
+                                  C.c_void_p(idx.data_ptr() if idx is not None else 0),
+                                  0 if idx is None else idx.numel(), C.c_void_p(W.data_ptr()), _ld(W)),
+          "isvd_least_norm", ctx.h)
+    return W

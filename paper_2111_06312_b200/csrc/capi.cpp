@@ -1261,6 +1261,98 @@ isvd_status isvd_sample_omega(isvd_op op, const isvd_svd_params* params, float* 
   });
 }
 
+isvd_status isvd_embeddings(isvd_ctx ctx, int64_t rows, int64_t k, const float* M, int64_t ldm, const double* S,
+                            float* out, int64_t ldo) {
+  if (!ctx) return ISVD_ERR_INVALID_ARG;
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    REQ(rows >= 0 && k >= 1 && M && out && S, ISVD_ERR_INVALID_ARG, "null argument or bad shape");
+    REQ(ldm >= round_up(k, 4) && ldo >= round_up(k, 4) && ldm % 4 == 0 && ldo % 4 == 0 && aligned16(M) &&
+            aligned16(out),
+        ISVD_ERR_INVALID_ARG, "ld must be a multiple of 4, >= round_up(k, 4), 16-byte aligned");
+    std::vector<float> r(round_up(k, 4), 0.f);
+    for (int64_t j = 0; j < k; ++j) {
+      REQ(std::isfinite(S[j]) && S[j] >= 0.0, ISVD_ERR_NONFINITE, "singular values must be finite and >= 0");
+      r[j] = (float)std::sqrt(S[j]);  // S^1/2 (Eq. 5), fp64 sqrt rounded once
+    }
+    std::vector<void*> tmp;
+    struct Tmp {
+      std::vector<void*>& v;
+      isvd_ctx c;
+      ~Tmp() { for (void* q : v) dfree(c, q); }
+    } tmp_free{tmp, ctx};
+    float* dr = (float*)dmalloc(ctx, sizeof(float) * r.size(), tmp);
+    CK(cudaMemcpyAsync(dr, r.data(), sizeof(float) * r.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(launch_scale_cols(M, ldm, out, ldo, rows, round_up(k, 4), dr, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+isvd_status isvd_least_norm(isvd_ctx ctx, int64_t r_local, int64_t k, const float* U, int64_t ldu, const double* S,
+                            int64_t r, int64_t c, int64_t v_rows, const float* V, int64_t ldv, int64_t ny,
+                            const float* Y, int64_t ldy, const int32_t* rows, int64_t n_rows, float* W,
+                            int64_t ldw) {
+  if (!ctx) return ISVD_ERR_INVALID_ARG;
+  return guarded(ctx, [&] {
+    DeviceGuard dg(ctx->device);
+    REQ(U && S && V && Y && W && k >= 1 && ny >= 1 && r_local >= 0 && v_rows >= 0 && r >= 1 && c >= 1,
+        ISVD_ERR_INVALID_ARG, "null argument or bad shape");
+    const int64_t kp = round_up(k, 4), nyp = round_up(ny, 4);
+    for (int64_t ld_ : {ldu, ldv})
+      REQ(ld_ >= kp && ld_ % 4 == 0, ISVD_ERR_INVALID_ARG, "ldu / ldv must be multiples of 4 >= round_up(k, 4)");
+    for (int64_t ld_ : {ldy, ldw})
+      REQ(ld_ >= nyp && ld_ % 4 == 0, ISVD_ERR_INVALID_ARG, "ldy / ldw must be multiples of 4 >= round_up(ny, 4)");
+    REQ(aligned16(U) && aligned16(V) && aligned16(Y) && aligned16(W), ISVD_ERR_INVALID_ARG,
+        "operands must be 16-byte aligned");
+    for (int64_t j = 0; j < k; ++j) REQ(std::isfinite(S[j]), ISVD_ERR_NONFINITE, "non-finite singular value");
+    REQ(!rows || (n_rows >= 0 && n_rows <= r_local), ISVD_ERR_INVALID_ARG, "bad row subset");
+    std::vector<void*> tmp;
+    struct Tmp {
+      std::vector<void*>& v;
+      isvd_ctx c;
+      ~Tmp() { for (void* q : v) dfree(c, q); }
+    } tmp_free{tmp, ctx};
+    // labelled rows of U and Y (option (i))
+    const float* Ua = U;
+    const float* Ya = Y;
+    int64_t nr = r_local, lda = ldu, ldb = ldy;
+    if (rows) {
+      nr = n_rows;
+      float* u2 = (float*)dmalloc(ctx, sizeof(float) * std::max<int64_t>(nr, 1) * kp, tmp);
+      float* y2 = (float*)dmalloc(ctx, sizeof(float) * std::max<int64_t>(nr, 1) * nyp, tmp);
+      if (nr > 0) {
+        CK(launch_scale_rows(U, ldu, u2, kp, nr, kp, nullptr, 1.f, nullptr, ctx->stream, rows));
+        CK(launch_scale_rows(Y, ldy, y2, nyp, nr, nyp, nullptr, 1.f, nullptr, ctx->stream, rows));
+      }
+      Ua = u2; Ya = y2; lda = kp; ldb = nyp;
+    }
+    // T = U^T Y, exact fp64, then the sum over ranks
+    double* ws = (double*)dmalloc(ctx, sizeof(double) * atb_ws_doubles(nr, k, ny, ctx->num_sms), tmp);
+    double* T = (double*)dmalloc(ctx, sizeof(double) * k * ny, tmp);
+    CK(launch_atb(Ua, lda, Ya, ldb, nr, k, ny, nullptr, false, ws, T, ny, nullptr, 0, ctx->num_sms, nullptr,
+                  ctx->stream, false));
+    if (ctx->dist) NK(ncclAllReduce(T, T, (size_t)k * ny, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    // S^+ T on the host (k x ny, small), reading O24's cut
+    std::vector<double> h((size_t)k * ny);
+    CK(cudaMemcpyAsync(h.data(), T, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double smax = 0.0;
+    for (int64_t j = 0; j < k; ++j) smax = std::max(smax, S[j]);
+    const double tol = (double)std::max(r, c) * 2.220446049250313e-16 * smax;
+    std::vector<float> t32((size_t)k * nyp, 0.f);
+    for (int64_t i = 0; i < k; ++i) {
+      const double inv = S[i] > tol ? 1.0 / S[i] : 0.0;
+      for (int64_t j = 0; j < ny; ++j) t32[(size_t)i * nyp + j] = (float)(inv * h[(size_t)i * ny + j]);
+    }
+    float* dT = (float*)dmalloc(ctx, sizeof(float) * t32.size(), tmp);
+    CK(cudaMemcpyAsync(dT, t32.data(), sizeof(float) * t32.size(), cudaMemcpyHostToDevice, ctx->stream));
+    // W = V (S^+ T)
+    if (v_rows > 0)
+      CK(launch_gemm_tn(V, ldv, dT, nyp, W, ldw, v_rows, nyp, k, nullptr, 1.f, false, nullptr, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ the solver body

@@ -65,6 +65,9 @@ cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ld
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows,
                               int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st,
                               const int32_t* in_map = nullptr);
+// out[i, j] = in[i, j] * colvec[j]  (i < rows, j < wpad, wpad % 4 == 0; out may equal in)
+cudaError_t launch_scale_cols(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
+                              const float* colvec, cudaStream_t st);
 
 // ------------------------------------------------------------------- SpMM
 // Fused CSR SpMM step (K1):  for each local row i (global id row_offset + i)

@@ -487,6 +487,17 @@ __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, flo
   }
 }
 
+__global__ void scale_cols_kernel(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t w4,
+                                  const float* __restrict__ colvec) {
+  const int64_t tot = rows * w4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / w4, c = (t - i * w4) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(in + i * ldi + c);
+    const float4 s = *reinterpret_cast<const float4*>(colvec + c);
+    *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s.x * v.x, s.y * v.y, s.z * v.z, s.w * v.w);
+  }
+}
+
 __global__ void f64_to_f32_kernel(const double* __restrict__ G, int64_t ldg, float* __restrict__ out, int64_t ldo,
                                   int64_t rows, int64_t cols) {
   int64_t tot = rows * cols;
@@ -844,6 +855,15 @@ cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t 
   ++g_launches;
   scale_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4,
                                                                                vec, coef, gate, in_map);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_cols(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
+                              const float* colvec, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  ++g_launches;
+  scale_cols_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4,
+                                                                               colvec);
   return cudaGetLastError();
 }
 

@@ -418,3 +418,35 @@ def test_ne_paper_exact_lambda_adj_and_fig1_weights(ctx, i):
     print(_check_isvd(res, isvd(ref, sp["k"], om, sp["q"]), sp["k"], f"cfg{i}/paper-exact"))
     op.close()
     graph.close()
+
+
+# --------------------------------------------- Eq. 5 embeddings and Eq. 7 W* on the device (f1)
+
+
+@pytest.mark.parametrize("i", [0, 2])
+def test_embeddings_and_least_norm_match_oracle(ctx, i):
+    """From the library's own SVD: L = U S^1/2 (Eq. 5) and W* = V S^+ U^T Y (Eq. 7) on one-hot
+    synthetic labels, all rows and a labelled subset, against the oracle formulas
+    applied to the same U, S, V (fp32 U/V promoted to fp64): W* within 1e-5 relative."""
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import embeddings as o_emb
+    from oracle import least_norm as o_ln
+
+    op, _, cfg, sp = _op(ctx, i)
+    p = -1 if cfg["p"] is None else cfg["p"]
+    res = op.svd(sp["k"], p, sp["q"], sp["seed"])
+    U, V, S = _to_np(res.U), _to_np(res.V), res.S
+    L = _to_np(isvd_mod.embeddings(ctx, res.U, S))
+    Lo, _ = o_emb(U, S, V)
+    assert rel_fro(L, Lo) <= 1e-6
+    rng = np.random.default_rng(21 + i)
+    n = U.shape[0]
+    ny = 7
+    Y = np.zeros((n, ny), dtype=np.float32)
+    Y[np.arange(n), rng.integers(0, ny, n)] = 1.0
+    shape = op.shape
+    W = _to_np(isvd_mod.least_norm(ctx, res.U, S, res.V, torch.from_numpy(Y).cuda(), shape))
+    assert rel_fro(W, o_ln(U, S, V, Y, shape=shape)) <= PROD_TOL
+    rows = np.sort(rng.choice(n, size=max(1, n // 10), replace=False)).astype(np.int32)
+    Wr = _to_np(isvd_mod.least_norm(ctx, res.U, S, res.V, torch.from_numpy(Y).cuda(), shape, rows=rows))
+    assert rel_fro(Wr, o_ln(U, S, V, Y, rows=rows, shape=shape)) <= PROD_TOL
