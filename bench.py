@@ -297,6 +297,34 @@ def main():
             del os.environ["ISVD_TC_PRODUCTS"]
         else:
             os.environ["ISVD_TC_PRODUCTS"] = prev
+    # ---- variant: NC with M materialised (M = M . I through the library, once),
+    # then the same isvd of the explicit n x c matrix (an NC operator with L = 0).  A measured
+    # comparison of what "never formed" costs; the matrix-free path stays the contract.
+    if not args.no_variants and cfg["op"] == "NC" and world == 1:
+        c = op.shape[1]
+        eye = torch.eye(c, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        e0.record(stream)
+        Mx = op.matmul(eye)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_mat = e0.elapsed_time(e1) / 1e3
+        del eye
+        opm = isvd.NC(graph, Mx, 0)
+        for _ in range(args.warmup):
+            opm.svd(sp["k"], p, sp["q"], sp["seed"])
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            opm.svd(sp["k"], p, sp["q"], sp["seed"])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        variants["materialised_M"] = {
+            "value": e0.elapsed_time(e1) / args.steps / 1e3, "unit": "s", "materialise_s": t_mat,
+            "what": "NC with M = [X|AX|A^2X|A^3X] formed once (M . I) and the isvd run on the explicit "
+                    "n x c matrix (SURVEY 8(f) f3, comparison only; north_star: M never materialised)"}
+        opm.close()
+        del Mx
     op.close()
     graph.close()
 

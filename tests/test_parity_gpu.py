@@ -450,3 +450,20 @@ def test_embeddings_and_least_norm_match_oracle(ctx, i):
     rows = np.sort(rng.choice(n, size=max(1, n // 10), replace=False)).astype(np.int32)
     Wr = _to_np(isvd_mod.least_norm(ctx, res.U, S, res.V, torch.from_numpy(Y).cuda(), shape, rows=rows))
     assert rel_fro(Wr, o_ln(U, S, V, Y, rows=rows, shape=shape)) <= PROD_TOL
+
+
+def test_materialised_nc_equals_implicit(ctx):
+    """SURVEY 8(f) f3 (comparison path): M formed through the library (M . I) and the isvd of the
+    explicit matrix (an NC operator with L = 0) meets the same parity bars against the oracle of
+    the implicit operator (implicit = explicit, oracle S3)."""
+    import paper_2111_06312_b200 as isvd_mod
+
+    op, _, cfg, sp = _op(ctx, 2)
+    c = op.shape[1]
+    Mx = op.matmul(torch.eye(c, dtype=torch.float32, device="cuda"))
+    opm = isvd_mod.NC(op.graph, Mx, 0)
+    assert opm.shape == op.shape
+    p = -1 if cfg["p"] is None else cfg["p"]
+    res = opm.svd(sp["k"], p, sp["q"], sp["seed"])
+    print(_check_isvd(res, _oracle_result(2), sp["k"], "cfg2/materialised"))
+    opm.close()
