@@ -24,6 +24,7 @@ from .isvd_oracle import (  # noqa: F401
     orthonorm_qr,
     pinv_diag,
     sign_fix,
+    spectral_kernel,
     sym_norm_adj,
     transition,
     uniform_weights,

@@ -345,3 +345,15 @@ def least_norm(U, s, V, Y, rows=None, shape=None):
     T = U.T @ Y
     T = pinv_diag(s, r, c)[:, None] * T
     return V @ T
+
+
+def spectral_kernel(s, mu: float, s_bar: float):
+    """Gaussian spectral reweighting of Eq. 9 by the discretisation of P:1057-1065:
+    E_x[S^x] ~ sum_{x in Omega} S^x softmax_x(-(x - mu)^2 exp(s_bar)), Omega = {0.5, 0.505, ..., 2.0}
+    (301 points), s_bar = log(1 / (2 s^2)).  Returns the reweighted diagonal (k-vector)."""
+    s = np.asarray(s, dtype=np.float64)
+    x = 0.5 + 0.005 * np.arange(301)
+    logits = -((x - mu) ** 2) * np.exp(s_bar)
+    w = np.exp(logits - logits.max())
+    w /= w.sum()
+    return np.array([np.sum(si ** x * w) for si in s])

@@ -498,3 +498,17 @@ def test_pinv_diag_cuts_numerical_zeros():
 
     s = np.array([2.0, 1.0, 1e-20, 0.0])
     assert np.array_equal(pinv_diag(s, 10, 4), [0.5, 1.0, 0.0, 0.0])
+
+
+def test_spectral_kernel_closed_forms():
+    """Eq. 9 discretised: mu = 1, s -> 0 is the identity (x concentrates at 1, on the
+    grid); S = 1 stays 1 for any (mu, s); S = (4, 1), mu = 2, s -> 0 gives (16, 1) (S:315-317);
+    a flat kernel (s -> inf) is the grid mean of S^x."""
+    from oracle import spectral_kernel
+
+    s = np.array([3.0, 1.5, 0.2])
+    assert np.allclose(spectral_kernel(s, 1.0, 40.0), s, rtol=1e-12)
+    assert np.allclose(spectral_kernel(np.ones(3), 0.7, 1.3), 1.0, rtol=1e-14)
+    assert np.allclose(spectral_kernel(np.array([4.0, 1.0]), 2.0, 40.0), [16.0, 1.0], rtol=1e-12)
+    x = 0.5 + 0.005 * np.arange(301)
+    assert np.isclose(spectral_kernel(np.array([2.0]), 1.0, -60.0)[0], np.mean(2.0 ** x), rtol=1e-12)
