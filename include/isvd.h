@@ -236,6 +236,13 @@ isvd_status isvd_least_norm(isvd_ctx ctx, int64_t r_local, int64_t k, const floa
                             const float* Y, int64_t ldy, const int32_t* rows, int64_t n_rows, float* W,
                             int64_t ldw);
 
+/* Gaussian spectral kernel (Eq. 9; discretisation P:1057-1065): out_i =
+ * sum_{x in Omega} S_i^x softmax_x(-(x - mu)^2 exp(s_bar)), Omega = {0.5, 0.505, ..., 2.0}
+ * (301 points), s_bar = log(1 / (2 s^2)); then f(i, j) = U_i^T diag(out) V_j.  Host arrays of k
+ * doubles (a k-vector epilogue; fp64 on the host side of the library).  S_i >= 0.
+ * Errors: ISVD_ERR_INVALID_ARG, ISVD_ERR_NONFINITE. */
+isvd_status isvd_spectral_kernel(const double* S, int64_t k, double mu, double s_bar, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,10 +13,11 @@ from .api import (  # noqa: F401
     embeddings,
     least_norm,
     nccl_unique_id,
+    spectral_kernel,
     padded,
     partition,
     round_up,
 )
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "nccl_unique_id", "partition",
-           "padded", "round_up"]
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
+           "nccl_unique_id", "partition", "padded", "round_up"]

@@ -98,6 +98,8 @@ SIGNATURES = {
     "isvd_sample_omega": (C.c_int, [C.c_void_p, C.POINTER(SvdParams), C.c_void_p, C.c_int64]),
     "isvd_embeddings": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
                                   C.POINTER(C.c_double), C.c_void_p, C.c_int64]),
+    "isvd_spectral_kernel": (C.c_int, [C.POINTER(C.c_double), C.c_int64, C.c_double, C.c_double,
+                                       C.POINTER(C.c_double)]),
     "isvd_least_norm": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_double),
                                   C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
                                   C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),

@@ -20,8 +20,8 @@ import torch
 from . import _lib
 from ._lib import check
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "nccl_unique_id", "partition",
-           "padded", "round_up"]
+__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
+           "nccl_unique_id", "partition", "padded", "round_up"]
 
 
 def round_up(x: int, m: int = 4) -> int:
@@ -345,3 +345,13 @@ def least_norm(ctx: Context, U: torch.Tensor, S, V: torch.Tensor, Y: torch.Tenso
                                   0 if idx is None else idx.numel(), C.c_void_p(W.data_ptr()), _ld(W)),
           "isvd_least_norm", ctx.h)
     return W
+
+
+def spectral_kernel(S, mu: float, s_bar: float) -> np.ndarray:
+    """Gaussian spectral reweighting of S (Eq. 9, discretised as P:1057-1065)."""
+    lib = _lib.load()
+    Sd = np.ascontiguousarray(S, dtype=np.float64)
+    out = np.zeros_like(Sd)
+    check(lib.isvd_spectral_kernel(Sd.ctypes.data_as(C.POINTER(C.c_double)), Sd.size, float(mu), float(s_bar),
+                                   out.ctypes.data_as(C.POINTER(C.c_double))), "isvd_spectral_kernel")
+    return out

@@ -1353,6 +1353,29 @@ isvd_status isvd_least_norm(isvd_ctx ctx, int64_t r_local, int64_t k, const floa
   });
 }
 
+isvd_status isvd_spectral_kernel(const double* S, int64_t k, double mu, double s_bar, double* out) {
+  if (!S || !out || k < 0) return ISVD_ERR_INVALID_ARG;
+  if (!std::isfinite(mu) || !std::isfinite(s_bar)) return ISVD_ERR_NONFINITE;
+  constexpr int kGrid = 301;  // Omega = {0.5, 0.505, ..., 2.0}
+  double w[kGrid], mx = -INFINITY;
+  const double sc = std::exp(s_bar);
+  for (int t = 0; t < kGrid; ++t) {
+    const double x = 0.5 + 0.005 * t;
+    w[t] = -(x - mu) * (x - mu) * sc;
+    mx = std::max(mx, w[t]);
+  }
+  double z = 0.0;
+  for (int t = 0; t < kGrid; ++t) z += (w[t] = std::exp(w[t] - mx));  // softmax, max-shifted
+  for (int t = 0; t < kGrid; ++t) w[t] /= z;
+  for (int64_t i = 0; i < k; ++i) {
+    if (!(S[i] >= 0.0) || !std::isfinite(S[i])) return ISVD_ERR_NONFINITE;
+    double acc = 0.0;
+    for (int t = 0; t < kGrid; ++t) acc += std::pow(S[i], 0.5 + 0.005 * t) * w[t];
+    out[i] = acc;
+  }
+  return ISVD_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ the solver body

@@ -78,3 +78,20 @@ def test_product_path_has_no_oracle_import():
             if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_spectral_kernel_host_logic_matches_oracle(lib):
+    """isvd_spectral_kernel (Eq. 9 discretised) is host-side library logic: it equals
+    the oracle's literal formula on random spectra and (mu, s_bar) pairs, and rejects bad input."""
+    import numpy as np
+
+    from oracle import spectral_kernel as o_sk
+    from paper_2111_06312_b200 import spectral_kernel
+
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        S = np.sort(rng.uniform(0.0, 5.0, 12))[::-1]
+        mu, sb = rng.uniform(0.5, 2.0), rng.uniform(-3.0, 8.0)
+        assert np.allclose(spectral_kernel(S, mu, sb), o_sk(S, mu, sb), rtol=1e-12, atol=0)
+    with pytest.raises(RuntimeError):
+        spectral_kernel(np.array([1.0, -1.0]), 1.0, 0.0)
