@@ -19,6 +19,7 @@ from .isvd_oracle import (  # noqa: F401
     embeddings,
     exact_svd,
     isvd,
+    label_reuse_adj,
     least_norm,
     orthonorm_cholesky,
     orthonorm_qr,

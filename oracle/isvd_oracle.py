@@ -128,10 +128,19 @@ class NEOperator:
         return self.matmul(np.eye(self.n))
 
 
-class NCOperator:
-    """M = [X | A_hat X | A_hat^2 X | ... | A_hat^L X]  in R^{n x d(L+1)}  (Eq. 6)."""
+def label_reuse_adj(A: sp.csr_matrix) -> sp.csr_matrix:
+    """A_hat - (D + I)^-1: the propagation of the label re-use blocks, i.e. A_hat with
+    its diagonal zeroed (no label leaks from row i to row i), built as written."""
+    d = degrees(A)
+    return sp.csr_matrix(sym_norm_adj(A) - sp.diags(1.0 / (d + 1.0)))
 
-    def __init__(self, A: sp.csr_matrix, X, L: int):
+
+class NCOperator:
+    """M = [X | A_hat X | A_hat^2 X | ... | A_hat^L X]  in R^{n x d(L+1)}  (Eq. 6),
+    optionally with the label re-use blocks:
+    M_LR = [M | B Y_train | B^2 Y_train | ... | B^P Y_train],  B = A_hat - (D + I)^-1."""
+
+    def __init__(self, A: sp.csr_matrix, X, L: int, Y_train=None, P: int = 0):
         self.A = sp.csr_matrix(A, dtype=np.float64)
         self.n = self.A.shape[0]
         self.X = np.asarray(X, dtype=np.float64)
@@ -141,13 +150,20 @@ class NCOperator:
         self.L = int(L)
         self.Ahat = sym_norm_adj(self.A)
         self.AhatT = sp.csr_matrix(self.Ahat.T)
+        self.P = int(P) if Y_train is not None else 0
+        self.Y = None if Y_train is None else np.asarray(Y_train, dtype=np.float64)
+        self.y = 0 if self.Y is None else self.Y.shape[1]
+        if self.P:
+            self.B = label_reuse_adj(self.A)
+            self.BT = sp.csr_matrix(self.B.T)
 
     @property
     def shape(self):
-        return (self.n, self.d * (self.L + 1))
+        return (self.n, self.d * (self.L + 1) + self.y * self.P)
 
     def matmul(self, G):
-        """M G = sum_j A_hat^j (X G_j), G_j = rows [jd, (j+1)d) of G (column concat)."""
+        """M G = sum_j A_hat^j (X G_j) + sum_p B^p (Y G'_p), G_j = rows [jd, (j+1)d) of G and G'_p
+        the following y-row blocks (column concat)."""
         G = np.asarray(G, dtype=np.float64)
         out = np.zeros((self.n, G.shape[1]))
         for j in range(self.L + 1):
@@ -155,10 +171,16 @@ class NCOperator:
             for _ in range(j):  # A_hat^j applied by j repeated products
                 P = self.Ahat @ P
             out += P
+        off = self.d * (self.L + 1)
+        for p in range(1, self.P + 1):
+            P = self.Y @ G[off + (p - 1) * self.y : off + p * self.y]
+            for _ in range(p):
+                P = self.B @ P
+            out += P
         return out
 
     def matmul_T(self, Q):
-        """M^T Q: block j = X^T (A_hat^T)^j Q."""
+        """M^T Q: block j = X^T (A_hat^T)^j Q, then Y^T (B^T)^p Q."""
         Q = np.asarray(Q, dtype=np.float64)
         blocks = []
         for j in range(self.L + 1):
@@ -166,14 +188,23 @@ class NCOperator:
             for _ in range(j):
                 P = self.AhatT @ P
             blocks.append(self.X.T @ P)
+        for p in range(1, self.P + 1):
+            P = Q
+            for _ in range(p):
+                P = self.BT @ P
+            blocks.append(self.Y.T @ P)
         return np.vstack(blocks)
 
     def dense(self) -> np.ndarray:
-        """Explicit n x d(L+1) M: the blocks A_hat^j X stacked side by side."""
+        """Explicit M: the blocks A_hat^j X (and B^p Y) stacked side by side."""
         blocks = [self.X]
         P = self.X
         for _ in range(self.L):
             P = self.Ahat @ P
+            blocks.append(P)
+        P = self.Y
+        for _ in range(self.P):
+            P = self.B @ P
             blocks.append(P)
         return np.hstack(blocks)
 

@@ -512,3 +512,61 @@ def test_spectral_kernel_closed_forms():
     assert np.allclose(spectral_kernel(np.array([4.0, 1.0]), 2.0, 40.0), [16.0, 1.0], rtol=1e-12)
     x = 0.5 + 0.005 * np.arange(301)
     assert np.isclose(spectral_kernel(np.array([2.0]), 1.0, -60.0)[0], np.mean(2.0 ** x), rtol=1e-12)
+
+
+# ---------------------------------------------------------- label re-use
+
+
+def test_label_reuse_edgeless_graph_gives_zero_blocks():
+    """No edges: A_hat = (D + I)^-1 = I, so B = A_hat - (D + I)^-1 = 0 and the label blocks vanish
+    (S:226)."""
+    import scipy.sparse as sps
+
+    from oracle import NCOperator
+
+    n = 5
+    A = sps.csr_matrix((n, n))
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((n, 2))
+    Y = np.eye(n)[:, :3]
+    op = NCOperator(A, X, 1, Y_train=Y, P=2)
+    M = op.dense()
+    assert M.shape == (n, 2 * 2 + 3 * 2)
+    assert np.array_equal(M[:, 4:], np.zeros((n, 6)))
+
+
+def test_label_reuse_has_no_self_leak_and_matches_s_a_s():
+    """Row i of B Y does not depend on Y_i: B = S A S with S = (D + I)^-1/2 has a zero
+    diagonal -- checked by perturbing one label row, and B against S A S built directly."""
+    from oracle import NCOperator, label_reuse_adj
+
+    rng = np.random.default_rng(9)
+    A = _random_connected(12, 20, rng)
+    d = np.asarray(A.sum(axis=1)).ravel()
+    S = np.diag(1.0 / np.sqrt(d + 1.0))
+    assert np.allclose(label_reuse_adj(A).toarray(), S @ A.toarray() @ S, rtol=0, atol=1e-15)
+    X = rng.standard_normal((12, 3))
+    Y = np.zeros((12, 4))
+    Y[np.arange(12), rng.integers(0, 4, 12)] = 1.0
+    Y2 = Y.copy()
+    Y2[5] = [7.0, -3.0, 2.0, 9.0]
+    M1 = NCOperator(A, X, 0, Y_train=Y, P=1).dense()
+    M2 = NCOperator(A, X, 0, Y_train=Y2, P=1).dense()
+    assert np.allclose(M1[5, 3:], M2[5, 3:], rtol=0, atol=1e-15)
+    assert not np.allclose(M1[:, 3:], M2[:, 3:])  # but the neighbours of node 5 do see it
+
+
+def test_label_reuse_implicit_equals_explicit():
+    """Implicit products of M_LR equal the explicit matrix's (P:328-337 with Eq. 6)."""
+    from oracle import NCOperator
+
+    rng = np.random.default_rng(4)
+    A = _random_connected(15, 25, rng)
+    X = rng.standard_normal((15, 3))
+    Y = rng.standard_normal((15, 2))
+    op = NCOperator(A, X, 2, Y_train=Y, P=2)
+    M = op.dense()
+    G = rng.standard_normal((op.shape[1], 5))
+    Q = rng.standard_normal((15, 5))
+    assert np.allclose(op.matmul(G), M @ G, rtol=0, atol=1e-12)
+    assert np.allclose(op.matmul_T(Q), M.T @ Q, rtol=0, atol=1e-12)
