@@ -142,12 +142,20 @@ typedef struct {
   const float* X;         /* NC: this rank's rows of X, n_local x d, row-major, leading dim ldx */
   int64_t d, ldx;         /* NC: feature width d (>= 1) and leading dimension (multiple of 4) */
   uint32_t x_flags;       /* NC: ISVD_PTR_DEVICE and/or ISVD_BORROW                           */
+  /* NC label re-use: M_LR = [M | B Y | B^2 Y | ... | B^P Y] with
+   * B = A_hat - (D + I)^-1 (A_hat without its diagonal: no label leaks to its own row).
+   * Y: this rank's rows of Y_train (n_local x y, one-hot on labelled rows, zero elsewhere),
+   * copied (host or device per y_flags & ISVD_PTR_DEVICE); ldy % 4 == 0.  P = 0: none.      */
+  const float* Y;
+  int64_t y, ldy;
+  int32_t lr_powers;
+  uint32_t y_flags;
 } isvd_op_desc;
 
 /* Define an implicit matrix over graph g.  No O(nnz) work; copies w (and X
  * unless borrowed).  The op holds a reference on g. */
 isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out);
-/* Global shape (r, c) of M (SymbolicPF.shape): NE (n, n); NC (n, d (L+1)). */
+/* Global shape (r, c) of M (SymbolicPF.shape): NE (n, n); NC (n, d (L+1) + y P). */
 isvd_status isvd_op_shape(isvd_op op, int64_t* rows, int64_t* cols);
 isvd_status isvd_op_destroy(isvd_op op);
 

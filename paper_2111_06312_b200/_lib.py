@@ -44,6 +44,11 @@ class OpDesc(C.Structure):
         ("d", C.c_int64),
         ("ldx", C.c_int64),
         ("x_flags", C.c_uint32),
+        ("Y", C.c_void_p),
+        ("y", C.c_int64),
+        ("ldy", C.c_int64),
+        ("lr_powers", C.c_int32),
+        ("y_flags", C.c_uint32),
     ]
 
 

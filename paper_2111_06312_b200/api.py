@@ -283,9 +283,10 @@ class NC(_Operator):
     """M = [X | A_hat X | ... | A_hat^L X],  A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2   (Eq. 6).
 
     X: this rank's rows (n_local x d), a CUDA tensor (borrowed when already in ABI layout)
-    or a host numpy array (copied)."""
+    or a host numpy array (copied).  Label re-use: Y_train (this rank's n_local x y
+    rows, copied) and P powers append the blocks B Y, ..., B^P Y, B = A_hat - (D+I)^-1."""
 
-    def __init__(self, graph: Graph, X, L: int):
+    def __init__(self, graph: Graph, X, L: int, Y_train=None, P: int = 0):
         d = _lib.OpDesc()
         d.kind = _lib.ISVD_OP_STACKED_PROPAGATION
         d.num_terms = int(L)
@@ -304,11 +305,24 @@ class NC(_Operator):
                 Xp[:, : Xn.shape[1]] = Xn
             d.X, d.d, d.ldx, d.x_flags = Xp.ctypes.data, Xn.shape[1], ldx, 0
             keep = (Xp,)
+        self.y, self.P = 0, 0
+        if Y_train is not None and P > 0:
+            if isinstance(Y_train, torch.Tensor):
+                Yt = _as_abi(Y_train, graph.ctx.device)
+                d.Y, d.y, d.ldy, d.y_flags = Yt.data_ptr(), Yt.shape[1], _ld(Yt), _lib.ISVD_PTR_DEVICE
+            else:
+                Yn = np.asarray(Y_train, dtype=np.float32)
+                Yt = np.zeros((Yn.shape[0], round_up(Yn.shape[1])), dtype=np.float32)
+                Yt[:, : Yn.shape[1]] = Yn
+                d.Y, d.y, d.ldy, d.y_flags = Yt.ctypes.data, Yn.shape[1], Yt.shape[1], 0
+            d.lr_powers = int(P)
+            keep = keep + (Yt,)
+            self.y, self.P = int(d.y), int(P)
         self.d, self.L = int(d.d), int(L)
         super().__init__(graph, d, keep=keep)
 
     def c_rows(self) -> int:
-        return self.d * (self.L + 1)
+        return self.d * (self.L + 1) + self.y * self.P
 
 
 # ------------------------------------------------------------------ after the SVD

@@ -121,11 +121,17 @@ struct isvd_op_s {
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
   float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
   float* adjbuf = nullptr;  // NE with lambda_adj != 0: lambda_adj A Q (internal row order)
+  // NC label re-use: Y_train (internal row order, owned), width, ld, powers
+  const float* Ylr = nullptr;
+  int64_t ylr = 0, ldylr = 0;
+  int lr_powers = 0;
+  float* lrbuf = nullptr;  // X G_0 + sum_p B^p Y G'_p (internal row order)
   SolverWs sws;
 };
 
 // ------------------------------------------------------------------ helpers
 namespace {
+int64_t c_rows_local(const isvd_op_s* op);
 
 struct Fail {
   isvd_status st;
@@ -278,14 +284,21 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
                          atb_ws_doubles(g->n_local, wpad, wpad, ctx->num_sms));
   atb = std::max(atb, (tc_atb_ws_floats(g->n_local, ka, wpad, false, ctx->num_sms) + 1) / 2);
   atb = std::max(atb, (tc_atb_ws_floats(g->n_local, wpad, wpad, true, ctx->num_sms) + 1) / 2);
+  if (op->lr_powers > 0) {
+    atb = std::max(atb, atb_ws_doubles(g->n_local, op->ylr, wpad, ctx->num_sms));
+    atb = std::max(atb, (tc_atb_ws_floats(g->n_local, op->ylr, wpad, false, ctx->num_sms) + 1) / 2);
+  }
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
   op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
                               op->ws_allocs);
   op->adjbuf = op->lambda_adj != 0.0
                    ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs)
                    : nullptr;
-  int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d * (op->terms + 1) : 1;
+  int64_t c = op->kind == ISVD_OP_STACKED_PROPAGATION ? c_rows_local(op) : 1;
   op->blk64 = (double*)dmalloc(ctx, sizeof(double) * c * wpad, op->ws_allocs);
+  op->lrbuf = op->lr_powers > 0
+                  ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs)
+                  : nullptr;
   op->ws_wpad = wpad;
 }
 
@@ -511,7 +524,8 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 // stretches from 26.4 to 32.5 ms (shared SMs / DRAM, lower clocks under the power cap), so it is
 // off by default (ISVD_OVERLAP=1 turns it on).
 bool nc_overlap(isvd_ctx ctx, isvd_op op) {
-  if (op->kind != ISVD_OP_STACKED_PROPAGATION || ctx->dist || !ctx->side || op->terms < 1) return false;
+  if (op->kind != ISVD_OP_STACKED_PROPAGATION || ctx->dist || !ctx->side || op->terms < 1 || op->lr_powers > 0)
+    return false;
   const char* v = getenv("ISVD_OVERLAP");
   return v && v[0] == '1';
 }
@@ -535,6 +549,42 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
   const int L = op->terms;
   const int64_t d = op->d;
   const int32_t* omap = (user_order && g->new2old) ? g->new2old : nullptr;
+  if (op->lr_powers > 0) {
+    // label re-use blocks first: lrbuf = X G_0 + sum_p B^p (Y G'_p), Horner over p on
+    // pre-scaled iterates, B Wt = s (A Wt) (no self term); L = 0: the sum goes straight to out
+    const int P = op->lr_powers;
+    const int64_t off = d * (L + 1), yw = op->ylr;
+    auto gp = [&](int p) { return G + (size_t)(off + (int64_t)(p - 1) * yw) * ldgm; };
+    float* wb[2] = {op->full_c, op->full_a};
+    float* wt = wb[P & 1];
+    gemm_fp32(op, op->Ylr, op->ldylr, gp(P), ldgm, slice(g, wt, wpad), wpad, g->n_local, wpad, yw, g->s, false,
+              nullptr);
+    allgather_rows(ctx, g, wt, wpad);
+    for (int p = P - 1; p >= 1; --p) {
+      gemm_fp32(op, op->Ylr, op->ldylr, gp(p), ldgm, op->ptmp, wpad, g->n_local, wpad, yw, nullptr, false, nullptr);
+      float* dst = wb[p & 1];
+      SpmmArgs a = spmm_base(g, wpad);
+      a.Y = wt; a.ldy = wpad;
+      a.post_vec = g->s2;
+      a.T = op->ptmp; a.ldt = wpad; a.term_vec = g->s;
+      a.out = slice(g, dst, wpad); a.ldo = wpad;
+      spmm(ctx, op, a);
+      allgather_rows(ctx, g, dst, wpad);
+      wt = dst;
+    }
+    gemm_fp32(op, op->X, op->ldx, G, ldgm, op->ptmp, wpad, g->n_local, wpad, d, nullptr, false, nullptr);
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = wt; a.ldy = wpad;
+    a.post_vec = g->s;
+    a.T = op->ptmp; a.ldt = wpad;
+    if (L == 0) {
+      a.out = out; a.ldo = ldo; a.out_map = omap;
+      spmm(ctx, op, a);
+      return;
+    }
+    a.out = op->lrbuf; a.ldo = wpad;
+    spmm(ctx, op, a);
+  }
   if (L == 0) {
     gemm_fp32(op, op->X, op->ldx, G, ldgm, out, ldo, g->n_local, wpad, d, nullptr, false, nullptr, omap);
     return;
@@ -597,10 +647,12 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
     cur = dst;
   }
   // X G_0 in internal row order; with a row map it goes through ptmp (the in-place
-  // accumulation into `out` needs identical read and write rows)
-  float* t0 = omap ? op->ptmp : out;
-  const int64_t ldt0 = omap ? wpad : ldo;
-  gemm_fp32(op, op->X, op->ldx, G, ldgm, t0, ldt0, g->n_local, wpad, d, nullptr, false, nullptr);
+  // accumulation into `out` needs identical read and write rows).  With label re-use, lrbuf
+  // already holds X G_0 plus the label blocks.
+  float* t0 = op->lr_powers > 0 ? op->lrbuf : (omap ? op->ptmp : out);
+  const int64_t ldt0 = (op->lr_powers > 0 || omap) ? wpad : ldo;
+  if (op->lr_powers == 0)
+    gemm_fp32(op, op->X, op->ldx, G, ldgm, t0, ldt0, g->n_local, wpad, d, nullptr, false, nullptr);
   SpmmArgs a = spmm_base(g, wpad);
   a.Y = cur; a.ldy = wpad; a.self_coef = 1.f;
   a.post_vec = g->s;
@@ -666,7 +718,25 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
     atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, slice(g, dst, wpad), wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
              wpad, nullptr);
   }
-  const int64_t c = d * (L + 1);
+  if (op->lr_powers > 0) {
+    // label re-use blocks: Zt_0 = s Q again; Zt_p = s^2 (A Zt_{p-1}) (B without the
+    // self term, B^T = B); block p = Y^T diag(1/s) Zt_p
+    float* zb[2] = {op->full_c, op->full_a};
+    CK(launch_scale_rows(Q, ldq, slice(g, zb[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream,
+                         imap));
+    allgather_rows(ctx, g, zb[0], wpad);
+    for (int p = 1; p <= op->lr_powers; ++p) {
+      SpmmArgs a = spmm_base(g, wpad);
+      a.Y = zb[(p - 1) & 1]; a.ldy = wpad;
+      a.post_vec = g->s2;
+      a.out = slice(g, zb[p & 1], wpad); a.ldo = wpad;
+      spmm(ctx, op, a);
+      if (p < op->lr_powers) allgather_rows(ctx, g, zb[p & 1], wpad);
+      atb_fp32(op, g->n_local, op->Ylr, op->ldylr, op->ylr, g->rs, slice(g, zb[p & 1], wpad), wpad, wpad, false,
+               op->blk64 + (size_t)(d * (L + 1) + (int64_t)(p - 1) * op->ylr) * wpad, wpad, nullptr);
+    }
+  }
+  const int64_t c = c_rows_local(op);
   allreduce_f64(ctx, op->blk64, (size_t)c * wpad);
   CK(launch_f64_to_f32(op->blk64, wpad, out, ldo, c, wpad, ctx->stream));
 }
@@ -687,12 +757,12 @@ void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ld
 
 void op_shape(const isvd_op_s* op, int64_t* r, int64_t* c) {
   *r = op->g->n;
-  *c = op->kind == ISVD_OP_POWER_SUM ? op->g->n : op->d * (op->terms + 1);
+  *c = op->kind == ISVD_OP_POWER_SUM ? op->g->n : op->d * (op->terms + 1) + op->ylr * op->lr_powers;
 }
 
 // rows of the c-side (columns of M) held by this rank
 int64_t c_rows_local(const isvd_op_s* op) {
-  return op->kind == ISVD_OP_POWER_SUM ? op->g->n_local : op->d * (op->terms + 1);
+  return op->kind == ISVD_OP_POWER_SUM ? op->g->n_local : op->d * (op->terms + 1) + op->ylr * op->lr_powers;
 }
 
 template <typename F>
@@ -998,6 +1068,34 @@ isvd_status isvd_graph_info(isvd_graph g, int64_t* n_global, int64_t* n_local, i
 }
 
 // ================================================================= operators
+namespace {
+// An owned device copy of a caller-ordered row block (n_local x ld fp32), rows in the graph's
+// internal order (relabelled graphs gather them through new2old).
+float* own_rows(isvd_ctx ctx, isvd_graph g, const float* src_in, int64_t ld, bool dev) {
+  std::vector<void*> tmp;
+  const size_t row_bytes = sizeof(float) * (size_t)ld;
+  float* x = (float*)dmalloc(ctx, row_bytes * (size_t)std::max<int64_t>(g->n_local, 1), tmp);
+  if (g->n_local > 0) {
+    if (!g->new2old) {
+      CK(cudaMemcpy(x, src_in, row_bytes * (size_t)g->n_local, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    } else {
+      const float* src = src_in;
+      std::vector<void*> stage;
+      if (!dev) {
+        float* d = (float*)dmalloc(ctx, row_bytes * (size_t)g->n_local, stage);
+        CK(cudaMemcpy(d, src_in, row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
+        src = d;
+      }
+      REQ(aligned16(src), ISVD_ERR_INVALID_ARG, "row blocks must be 16-byte aligned");
+      CK(launch_scale_rows(src, ld, x, ld, g->n_local, ld, nullptr, 1.f, nullptr, ctx->stream, g->new2old));
+      CK(cudaStreamSynchronize(ctx->stream));
+      for (void* q : stage) dfree(ctx, q);
+    }
+  }
+  return x;
+}
+}  // namespace
+
 isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out) {
   if (!g || !desc || !out) return ISVD_ERR_INVALID_ARG;
   isvd_ctx ctx = g->ctx;
@@ -1031,32 +1129,18 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
         REQ(aligned16(desc->X), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
         op->X = desc->X;
       } else {
-        // own copy (ldx kept); a relabelled graph stores X's rows in its internal order
-        std::vector<void*> tmp;
-        const size_t row_bytes = sizeof(float) * (size_t)desc->ldx;
-        float* x = (float*)dmalloc(ctx, row_bytes * (size_t)std::max<int64_t>(g->n_local, 1), tmp);
-        if (g->n_local > 0) {
-          if (!g->new2old) {
-            CK(cudaMemcpy(x, desc->X, row_bytes * (size_t)g->n_local,
-                          dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-          } else {
-            // caller-ordered X on the device (uploaded if needed), rows gathered to the internal order
-            const float* src = desc->X;
-            std::vector<void*> stage;
-            if (!dev) {
-              float* d = (float*)dmalloc(ctx, row_bytes * (size_t)g->n_local, stage);
-              CK(cudaMemcpy(d, desc->X, row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
-              src = d;
-            }
-            REQ(aligned16(src), ISVD_ERR_INVALID_ARG, "X must be 16-byte aligned");
-            CK(launch_scale_rows(src, desc->ldx, x, desc->ldx, g->n_local, desc->ldx, nullptr, 1.f, nullptr,
-                                 ctx->stream, g->new2old));
-            CK(cudaStreamSynchronize(ctx->stream));
-            for (void* q : stage) dfree(ctx, q);
-          }
-        }
-        op->X = x;
+        op->X = own_rows(ctx, g, desc->X, desc->ldx, dev);
         op->own_x = true;
+      }
+      if (desc->lr_powers > 0) {  // label re-use blocks
+        REQ(desc->y >= 1 && desc->ldy >= desc->y && desc->ldy % 4 == 0, ISVD_ERR_INVALID_ARG,
+            "label width y >= 1 and ldy >= y, a multiple of 4");
+        REQ(desc->Y != nullptr || g->n_local == 0, ISVD_ERR_INVALID_ARG, "Y is null");
+        REQ((desc->y_flags & ~(uint32_t)ISVD_PTR_DEVICE) == 0, ISVD_ERR_INVALID_ARG, "bad y_flags");
+        op->Ylr = own_rows(ctx, g, desc->Y, desc->ldy, desc->y_flags & ISVD_PTR_DEVICE);
+        op->ylr = desc->y;
+        op->ldylr = desc->ldy;
+        op->lr_powers = desc->lr_powers;
       }
     } else {
       REQ(false, ISVD_ERR_INVALID_ARG, "unknown op kind");
@@ -1092,6 +1176,7 @@ isvd_status isvd_op_destroy(isvd_op op) {
   for (void* p : op->ws_allocs) dfree(op->g->ctx, p);
   free_solver_ws(op->g->ctx, op->sws);
   if (op->own_x) dfree(op->g->ctx, (void*)op->X);
+  if (op->Ylr) dfree(op->g->ctx, (void*)op->Ylr);
   op->g->refs--;
   delete op;
   return ISVD_OK;

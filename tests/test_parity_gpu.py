@@ -467,3 +467,38 @@ def test_materialised_nc_equals_implicit(ctx):
     res = opm.svd(sp["k"], p, sp["q"], sp["seed"])
     print(_check_isvd(res, _oracle_result(2), sp["k"], "cfg2/materialised"))
     opm.close()
+
+
+# --------------------------------------------- label re-use NC operator
+
+
+@pytest.mark.parametrize("L,P", [(3, 2), (0, 2), (2, 1)])
+def test_label_reuse_products_and_isvd(ctx, L, P):
+    """M_LR = [X | ... | A_hat^L X | B Y_train | ... | B^P Y_train], B = A_hat - (D+I)^-1
+    on config 2's graph with synthetic one-hot labels on 30 % of the nodes: products within 1e-5 of
+    the oracle, and the isvd meets the parity bars."""
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import NCOperator, adjacency, isvd, philox_omega
+
+    cfg, g, X, sp = config_inputs(2)
+    rng = np.random.default_rng(40 + L + P)
+    ny = 8
+    Y = np.zeros((g.n, ny), dtype=np.float32)
+    lab = rng.random(g.n) < 0.3
+    Y[np.where(lab)[0], rng.integers(0, ny, lab.sum())] = 1.0
+    ref = NCOperator(adjacency(g.n, g.row_ptr, g.col_idx), X, L, Y_train=Y, P=P)
+    graph = isvd_mod.Graph(ctx, g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
+    op = isvd_mod.NC(graph, torch.from_numpy(np.ascontiguousarray(X)).cuda(), L, Y_train=Y, P=P)
+    assert op.shape == ref.shape
+    c = op.shape[1]
+    Gm = rng.standard_normal((c, 24)).astype(np.float32)
+    assert rel_fro(_to_np(op.matmul(torch.from_numpy(Gm).cuda())), ref.matmul(Gm.astype(np.float64))) <= PROD_TOL
+    Q = rng.standard_normal((g.n, 24)).astype(np.float32)
+    assert rel_fro(_to_np(op.matmul_T(torch.from_numpy(Q).cuda())), ref.matmul_T(Q.astype(np.float64))) <= PROD_TOL
+    if L == 3:
+        k = 64
+        res = op.svd(k, -1, sp["q"], sp["seed"])
+        om = philox_omega(sp["seed"], 0, c, res.l)
+        print(_check_isvd(res, isvd(ref, k, om, sp["q"]), k, f"LR L={L} P={P}"))
+    op.close()
+    graph.close()
