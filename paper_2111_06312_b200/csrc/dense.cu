@@ -47,8 +47,8 @@ ISVD_DEVICE void thread_xy(int tid, int* tx, int* ty) {
   }
 }
 
-template <int BM, int BN, int BK, int TM, int TN>
-__global__ void __launch_bounds__((BM / TM) * (BN / TN), 2)
+template <int BM, int BN, int BK, int TM, int TN, int MINB = 2>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
     gemm_tn_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                    float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                    const float* __restrict__ row_scale, float alpha, int upper_tri_b, const int* gate,
@@ -536,12 +536,14 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
     // for short K (X G_j, K = d = 100) the 8-deep ones waste less on the ragged last stage
     dim3 grid((unsigned)ceil_div(N, 80), (unsigned)ceil_div(M, 128));
     ++g_launches;
+    // 3 CTAs per SM (128 registers, a few bytes of spill) hide the per-tile prologue and the
+    // barriers better than 2: X G_j 5.47 -> 5.04 ms, Y R^-1 11.65 -> 11.34 ms at config 4
     if (K >= 256)
-      gemm_tn_kernel<128, 80, 16, 8, 8><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                             upper_tri_b ? 1 : 0, gate, out_map);
+      gemm_tn_kernel<128, 80, 16, 8, 8, 3><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                                upper_tri_b ? 1 : 0, gate, out_map);
     else
-      gemm_tn_kernel<128, 80, 8, 8, 8><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                            upper_tri_b ? 1 : 0, gate, out_map);
+      gemm_tn_kernel<128, 80, 8, 8, 8, 3><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
+                                                               upper_tri_b ? 1 : 0, gate, out_map);
   } else if (N > 64) {
     dim3 grid((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, 128));
     ++g_launches; gemm_tn_kernel<128, 128, 8, 8, 8><<<grid, 256, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
