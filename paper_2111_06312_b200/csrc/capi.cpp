@@ -1558,8 +1558,8 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
     NK(ncclAllGather(s.cand, s.cand_all, 3 * k, ncclDouble, ctx->comm, ctx->stream));
     cand = s.cand_all;
   }
-  CK(launch_sign_flip(cand, ctx->world, (int)k, s.sgn, U, ldu, rr, V, ldv, cr, ctx->stream));
-  CK(launch_check_finite(U, ldu, rr, k, ctx->status, ctx->stream));
+  // sign flip of U and V; the flip of U also flags non-finite output entries (one pass over U)
+  CK(launch_sign_flip(cand, ctx->world, (int)k, s.sgn, U, ldu, rr, V, ldv, cr, ctx->stream, ctx->status));
 }
 
 }  // namespace

@@ -206,7 +206,7 @@ cudaError_t launch_col_absmax(const float* U, int64_t ldu, int64_t rows, int k, 
 // Select over `world` candidate sets (cand: world x k x 3) and flip the columns of
 // U (rows x k) and V (vrows x k) whose selected entry is negative.
 cudaError_t launch_sign_flip(const double* cand, int world, int k, float* sgn_ws, float* U, int64_t ldu,
-                             int64_t rows, float* V, int64_t ldv, int64_t vrows, cudaStream_t st);
+                             int64_t rows, float* V, int64_t ldv, int64_t vrows, cudaStream_t st, DevStatus* status = nullptr);
 // status->nonfinite |= any(!isfinite(A[:rows, :cols])).
 cudaError_t launch_check_finite(const float* A, int64_t lda, int64_t rows, int64_t cols, DevStatus* status,
                                 cudaStream_t st);

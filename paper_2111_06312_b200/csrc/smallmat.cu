@@ -545,13 +545,34 @@ __global__ void sign_select_kernel(const double* __restrict__ cand, int world, i
   }
 }
 
-__global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int64_t ldu, int64_t rows) {
-  int64_t tot = rows * k;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / k;
-    int c = (int)(t - i * k);
-    U[i * ldu + c] *= sgn[c];
+// U[:, c] *= sgn[c]; with `status`, also flags a non-finite entry (the output check of isvd_svd,
+// fused here so U is read once).  k % 4 == 0 and ldu % 4 == 0: float4 path.
+__global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int64_t ldu, int64_t rows,
+                            DevStatus* status) {
+  int bad = 0;
+  if ((k & 3) == 0 && (ldu & 3) == 0) {
+    const int k4 = k >> 2;
+    const int64_t tot = rows * k4;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = t / k4;
+      const int c = (int)(t - i * k4) * 4;
+      float4* p = reinterpret_cast<float4*>(U + i * ldu + c);
+      float4 v = *p;
+      v.x *= sgn[c]; v.y *= sgn[c + 1]; v.z *= sgn[c + 2]; v.w *= sgn[c + 3];
+      bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+      *p = v;
+    }
+  } else {
+    const int64_t tot = rows * k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = t / k;
+      const int c = (int)(t - i * k);
+      const float v = U[i * ldu + c] * sgn[c];
+      bad |= !isfinite(v);
+      U[i * ldu + c] = v;
+    }
   }
+  if (status && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status->nonfinite, 1);
 }
 
 int grid_for(int64_t work, int threads, int cap) {
@@ -936,10 +957,14 @@ cudaError_t launch_col_absmax(const float* U, int64_t ldu, int64_t rows, int k, 
 }
 
 cudaError_t launch_sign_flip(const double* cand, int world, int k, float* sgn_ws, float* U, int64_t ldu, int64_t rows,
-                             float* V, int64_t ldv, int64_t vrows, cudaStream_t st) {
+                             float* V, int64_t ldv, int64_t vrows, cudaStream_t st, DevStatus* status) {
   ++g_launches; sign_select_kernel<<<grid_for(k, 256, 16), 256, 0, st>>>(cand, world, k, sgn_ws);
-  if (rows > 0) { ++g_launches; flip_kernel<<<grid_for(rows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, U, ldu, rows); }
-  if (vrows > 0) { ++g_launches; flip_kernel<<<grid_for(vrows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, V, ldv, vrows); }
+  if (rows > 0) {
+    ++g_launches; flip_kernel<<<grid_for(rows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, U, ldu, rows, status);
+  }
+  if (vrows > 0) {
+    ++g_launches; flip_kernel<<<grid_for(vrows * k, 256, 148 * 8), 256, 0, st>>>(sgn_ws, k, V, ldv, vrows, nullptr);
+  }
   return cudaGetLastError();
 }
 

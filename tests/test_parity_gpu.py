@@ -502,3 +502,22 @@ def test_label_reuse_products_and_isvd(ctx, L, P):
         print(_check_isvd(res, isvd(ref, k, om, sp["q"]), k, f"LR L={L} P={P}"))
     op.close()
     graph.close()
+
+
+def test_non_finite_input_is_reported_not_returned(ctx):
+    """A NaN in X propagates through every product; the solver must report it instead of returning
+    garbage: the Cholesky breakdown check fires first (ISVD_ERR_NOT_PD after the shifted
+    retries), and the output check fused into the sign flip of U (ISVD_ERR_NONFINITE) backs it up."""
+    import paper_2111_06312_b200 as isvd_mod
+
+    cfg, g, X, sp = config_inputs(2)
+    Xn = np.ascontiguousarray(X).copy()
+    Xn[17, 3] = np.nan
+    graph = isvd_mod.Graph(ctx, g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
+    op = isvd_mod.NC(graph, torch.from_numpy(Xn).cuda(), sp["L"])
+    with pytest.raises(RuntimeError) as e:
+        op.svd(sp["k"], -1 if cfg["p"] is None else cfg["p"], sp["q"], sp["seed"])
+    msg = str(e.value)
+    assert "ISVD_ERR_NOT_PD" in msg or "ISVD_ERR_NONFINITE" in msg, msg
+    op.close()
+    graph.close()
