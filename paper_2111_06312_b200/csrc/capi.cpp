@@ -328,12 +328,15 @@ void atb_fp32(isvd_op op, int64_t rows, const float* A, int64_t lda, int64_t Ka,
               const float* B, int64_t ldb, int64_t Kb, bool symmetric, double* G, int64_t ldg, const int* gate) {
   isvd_ctx ctx = op->g->ctx;
   if (use_tensor_cores(rows, Ka, Kb, lda, ldb, symmetric && A == B)) {
-    int64_t ws_lda = 0, ws_ld = 0, parts = 0;
+    int64_t ws_lda = 0, ws_ld = 0, parts = 0, diag0 = -1;
     float* ws32 = reinterpret_cast<float*>(op->atb_ws);
     CK(launch_tc_atb(A, lda, Ka, row_scale, B, ldb, Kb, rows, symmetric, ws32, &ws_lda, &ws_ld, &parts,
-                     ctx->num_sms, gate, ctx->stream));
+                     ctx->num_sms, gate, ctx->stream, symmetric ? &diag0 : nullptr));
     CK(launch_atb_f32_reduce(ws32, ws_lda, ws_ld, parts, Ka, Kb, symmetric, G, ldg, nullptr, 0, ctx->num_sms, gate,
                              ctx->stream));
+    if (diag0 >= 0)  // the few trailing rows' diagonal block, SIMT fp32-chunk class (overwrites it)
+      CK(launch_atb(A + diag0, lda, B + diag0, ldb, rows, Ka - diag0, Kb - diag0, row_scale, true, op->atb_ws,
+                    G + diag0 * ldg + diag0, ldg, nullptr, 0, ctx->num_sms, gate, ctx->stream, true));
     return;
   }
   CK(launch_atb(A, lda, B, ldb, rows, Ka, Kb, row_scale, symmetric, op->atb_ws, G, ldg, nullptr, 0, ctx->num_sms,

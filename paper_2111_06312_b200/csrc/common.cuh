@@ -166,9 +166,12 @@ cudaError_t launch_atb_f32_reduce(const float* ws32, int64_t ws_lda, int64_t ws_
 // only the tiles holding some i <= j are computed (the reduce mirrors).
 bool tc_atb_supported(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t ldb);
 int64_t tc_atb_ws_floats(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num_sms);
+// diag0 (symmetric only): if non-null, the launch may leave a trailing diagonal block [*diag0, Ka)^2
+// (when the last 128-row tile holds <= 64 valid rows) for the caller to compute; *diag0 = -1 if not.
 cudaError_t launch_tc_atb(const float* A, int64_t lda, int64_t Ka, const float* row_scale, const float* B,
                           int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws32, int64_t* ws_lda,
-                          int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st);
+                          int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st,
+                          int64_t* diag0 = nullptr);
 // out = *flag ? I : Rinv  (l x l, ld x ld fp32; the deferred CholeskyQR2 factor)
 cudaError_t launch_select_rfold(const float* Rinv, float* out, int l, int64_t ld, const int* flag, cudaStream_t st);
 // out32[i, j] = (float) G[i, j]

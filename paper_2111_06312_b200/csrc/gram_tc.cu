@@ -306,10 +306,15 @@ constexpr int kTcNs[] = {128, 160, 208, 256};  // instantiated tile widths
 
 struct TcTiling {
   int n, ta, tb, tiles;
+  int ta_run;            // M-tiles computed (symmetric: the last one may be left to a small kernel)
+  int64_t diag0;         // >= 0: the diagonal block [diag0, Ka)^2 is computed by the caller instead
   int64_t parts, rows_per_cta;
 };
 
-TcTiling tc_tiling(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num_sms) {
+// skip_diag: for a symmetric product whose last 128-row M-tile holds only a few valid rows, that
+// tile contributes only the diagonal block [a0, Ka)^2 to the upper triangle (every other entry of
+// those rows is mirrored from a column tile): leave it to the caller's small kernel.
+TcTiling tc_tiling(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num_sms, bool skip_diag = false) {
   TcTiling t{};
   t.ta = (int)ceil_div(Ka, kTcM);
   const int64_t tb = ceil_div(Kb, 256);
@@ -318,8 +323,14 @@ TcTiling tc_tiling(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num
   for (int n : kTcNs)
     if (n >= need) { t.n = n; break; }
   t.tb = (int)ceil_div(Kb, t.n);
+  t.ta_run = t.ta;
+  t.diag0 = -1;
+  if (skip_diag && symmetric && t.ta > 1 && Ka - (int64_t)(t.ta - 1) * kTcM <= 64) {
+    t.ta_run = t.ta - 1;
+    t.diag0 = (int64_t)(t.ta - 1) * kTcM;
+  }
   t.tiles = 0;
-  for (int i = 0; i < t.ta; ++i)
+  for (int i = 0; i < t.ta_run; ++i)
     for (int j = 0; j < t.tb; ++j)
       if (!(symmetric && (int64_t)i * kTcM > (int64_t)j * t.n + t.n - 1)) ++t.tiles;
   // one wave of CTAs (1 per SM), row ranges a multiple of the chunk
@@ -345,7 +356,7 @@ cudaError_t tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t 
   }
   dim3 grid((unsigned)t.tiles, (unsigned)t.parts);
   ++g_launches;
-  tc_atb_kernel<N><<<grid, kTcWsThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta, t.tb, symmetric ? 1 : 0,
+  tc_atb_kernel<N><<<grid, kTcWsThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta_run, t.tb, symmetric ? 1 : 0,
                                                    t.rows_per_cta, ws, ws_lda, ws_ld, gate);
   return cudaGetLastError();
 }
@@ -358,13 +369,16 @@ bool tc_atb_supported(int64_t rows, int64_t Ka, int64_t Kb, int64_t lda, int64_t
 
 int64_t tc_atb_ws_floats(int64_t rows, int64_t Ka, int64_t Kb, bool symmetric, int num_sms) {
   TcTiling t = tc_tiling(rows, Ka, Kb, symmetric, num_sms);
-  return t.parts * ((int64_t)t.ta * kTcM) * ((int64_t)t.tb * t.n);
+  TcTiling u = tc_tiling(rows, Ka, Kb, symmetric, num_sms, true);  // fewer tiles -> possibly more parts
+  return std::max(t.parts, u.parts) * ((int64_t)t.ta * kTcM) * ((int64_t)t.tb * t.n);
 }
 
 cudaError_t launch_tc_atb(const float* A, int64_t lda, int64_t Ka, const float* row_scale, const float* B,
                           int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws32, int64_t* ws_lda,
-                          int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st) {
-  TcTiling t = tc_tiling(rows, Ka, Kb, symmetric, num_sms);
+                          int64_t* ws_ld, int64_t* parts, int num_sms, const int* gate, cudaStream_t st,
+                          int64_t* diag0) {
+  TcTiling t = tc_tiling(rows, Ka, Kb, symmetric, num_sms, diag0 != nullptr);
+  if (diag0) *diag0 = t.diag0;
   *ws_lda = (int64_t)t.ta * kTcM;
   *ws_ld = (int64_t)t.tb * t.n;
   *parts = t.parts;
