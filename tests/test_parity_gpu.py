@@ -521,3 +521,17 @@ def test_non_finite_input_is_reported_not_returned(ctx):
     assert "ISVD_ERR_NOT_PD" in msg or "ISVD_ERR_NONFINITE" in msg, msg
     op.close()
     graph.close()
+
+
+@pytest.mark.parametrize("k,p", [(64, 100), (96, 96), (96, 98)])
+def test_tc_gram_partial_last_tile(ctx, k, p):
+    """Config 2 (n = 169,343, tcgen05 Gram engaged) at l = 164 and l = 192, where the symmetric
+    Gram leaves the last 128-row tile's diagonal block ([128, l)^2, 36 and 64 rows) to the SIMT
+    kernel, and at l = 194 (66 rows), where the tensor-core kernel computes that tile itself."""
+    from oracle import isvd, philox_omega
+
+    op, ref, cfg, sp = _op(ctx, 2)
+    res = op.svd(k, p, sp["q"], sp["seed"])
+    assert res.l == k + p
+    om = philox_omega(sp["seed"], 0, ref.shape[1], k + p)
+    print(_check_isvd(res, isvd(ref, k, om, sp["q"]), k, f"cfg2 l={k + p}"))
