@@ -114,6 +114,8 @@ struct isvd_op_s {
   const float* X = nullptr;
   int64_t d = 0, ldx = 0;
   bool own_x = false;
+  float* Xrs = nullptr;  // NC: diag(1/s) X = diag((d+1)^1/2) X, the left operand of every X^T Zt_j
+                         // (the same fp32 products the kernel would form; refreshed per call if X is borrowed)
   // product workspace (sized for the widest request so far)
   int64_t ws_wpad = 0;
   std::vector<void*> ws_allocs;
@@ -664,6 +666,13 @@ void nc_matmul(isvd_ctx ctx, isvd_op op, const float* G, int64_t ldgm, float* ou
   spmm(ctx, op, a);
 }
 
+// Xrs = diag(1/s) X (P:182-193 with A_hat = S (A+I) S; 1/s = (d+1)^1/2 = g->rs)
+void refresh_xrs(isvd_ctx ctx, isvd_op op) {
+  isvd_graph g = op->g;
+  CK(launch_scale_rows(op->X, op->ldx, op->Xrs, op->ldx, g->n_local, op->ldx, g->rs, 1.f, nullptr, ctx->stream,
+                       nullptr));
+}
+
 // M^T Q: block j = X^T A_hat^j Q.  Zt_0 = s Q; Zt_{j+1} = s^2 ((A+I) Zt_j); block j = X^T diag(1/s) Zt_j.
 // Q rows are in the caller's order when user_order (mapped by the first scaling pass).
 void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
@@ -673,7 +682,9 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   const int64_t d = op->d;
   const int32_t* imap = (user_order && g->new2old) ? g->new2old : nullptr;
   float* bufs[2] = {op->full_a, op->full_b};
-  // Zt_0 = s Q (internal row order), block 0 = X^T diag(1/s) Zt_0
+  if (!op->own_x) refresh_xrs(ctx, op);  // a borrowed X may have changed since the last call
+  const float* Xrs = op->Xrs;
+  // Zt_0 = s Q (internal row order), block 0 = X^T diag(1/s) Zt_0 = Xrs^T Zt_0
   CK(launch_scale_rows(Q, ldq, slice(g, bufs[0], wpad), wpad, g->n_local, wpad, g->s, 1.f, nullptr, ctx->stream,
                        imap));
   if (nc_overlap(ctx, op)) {
@@ -685,7 +696,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
       ev_wait(ctx, 2 * j, ctx->side);
       {
         OnStream on(ctx, ctx->side);
-        atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, zt, wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
+        atb_fp32(op, g->n_local, Xrs, op->ldx, d, nullptr, zt, wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
                  wpad, nullptr);
       }
       ev_record(ctx, 2 * j + 1, ctx->side);
@@ -707,7 +718,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
     CK(launch_f64_to_f32(op->blk64, wpad, out, ldo, c, wpad, ctx->stream));
     return;
   }
-  atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, slice(g, bufs[0], wpad), wpad, wpad, false, op->blk64, wpad, nullptr);
+  atb_fp32(op, g->n_local, Xrs, op->ldx, d, nullptr, slice(g, bufs[0], wpad), wpad, wpad, false, op->blk64, wpad, nullptr);
   if (L > 0) allgather_rows(ctx, g, bufs[0], wpad);
   for (int j = 1; j <= L; ++j) {
     float* src = bufs[(j - 1) & 1];
@@ -718,7 +729,7 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
     a.out = slice(g, dst, wpad); a.ldo = wpad;
     spmm(ctx, op, a);
     if (j < L) allgather_rows(ctx, g, dst, wpad);
-    atb_fp32(op, g->n_local, op->X, op->ldx, d, g->rs, slice(g, dst, wpad), wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
+    atb_fp32(op, g->n_local, Xrs, op->ldx, d, nullptr, slice(g, dst, wpad), wpad, wpad, false, op->blk64 + (size_t)j * d * wpad,
              wpad, nullptr);
   }
   if (op->lr_powers > 0) {
@@ -1135,6 +1146,11 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
         op->X = own_rows(ctx, g, desc->X, desc->ldx, dev);
         op->own_x = true;
       }
+      {
+        std::vector<void*> tmp;
+        op->Xrs = (float*)dmalloc(ctx, sizeof(float) * (size_t)desc->ldx * (size_t)std::max<int64_t>(g->n_local, 1), tmp);
+        if (op->own_x) refresh_xrs(ctx, op);
+      }
       if (desc->lr_powers > 0) {  // label re-use blocks
         REQ(desc->y >= 1 && desc->ldy >= desc->y && desc->ldy % 4 == 0, ISVD_ERR_INVALID_ARG,
             "label width y >= 1 and ldy >= y, a multiple of 4");
@@ -1179,6 +1195,7 @@ isvd_status isvd_op_destroy(isvd_op op) {
   for (void* p : op->ws_allocs) dfree(op->g->ctx, p);
   free_solver_ws(op->g->ctx, op->sws);
   if (op->own_x) dfree(op->g->ctx, (void*)op->X);
+  if (op->Xrs) dfree(op->g->ctx, op->Xrs);
   if (op->Ylr) dfree(op->g->ctx, (void*)op->Ylr);
   op->g->refs--;
   delete op;
