@@ -721,7 +721,9 @@ F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   // on B200 (128 FP32 lanes, 128 B/clk of shared memory per SM) small register tiles are
   // shared-memory-bound.  (8 x 16 tiles need 255 registers; at 2 CTAs per SM they measured
   // slower than 8 x 8 -- 0.95 vs 0.88 s per config-4 isvd -- and are not offered.)
-  const int cand[5][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8}};
+  // (32 x 32: the symmetric Gram's small trailing diagonal block, e.g. 16 x 16 at l = 400)
+  const int cand[6][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8},
+                          {32, 32, 4, 8}};
   F32Tiling t{64, 64, 4, 8, 0, 0, 0, 0};
   double best = -1;
   for (auto& c : cand) {
@@ -803,6 +805,7 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     atb_f32_kernel<BM_, BN_, TM_, TN_><<<grid, (BM_ / TM_) * (BN_ / TN_), 0, st>>>(                       \
         A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows, ws32, ws_lda, ws_ld, gate);
       ISVD_ATB_F32(64, 64, 4, 8)
+      else ISVD_ATB_F32(32, 32, 4, 8)
       else ISVD_ATB_F32(100, 80, 4, 8)
       else ISVD_ATB_F32(128, 128, 4, 8)
       else if (t.bm == 104 && t.bn == 80 && t.tm == 8 && row_scale)  // 4 CTAs per SM (96 registers): 8.2 -> 7.4 ms at config 4
