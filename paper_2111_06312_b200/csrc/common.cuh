@@ -33,6 +33,11 @@ ISVD_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
   return *reinterpret_cast<float2*>(&d);
 }
+// flat index t -> (row, column) of a width-w grid-stride loop: a 32-bit division whenever t fits
+// (a 64-bit division is a ~70-instruction subroutine call per element)
+ISVD_DEVICE int64_t row_of(int64_t t, int64_t w) {
+  return (uint64_t)t <= 0xFFFFFFFFull ? (int64_t)((uint32_t)t / (uint32_t)w) : t / w;
+}
 #endif
 
 // Kernels enqueued by this host thread (each launcher adds the number it launched);

@@ -479,7 +479,7 @@ __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, flo
   if (gate && *((volatile const int*)gate) == 0) return;
   int64_t tot = rows * w4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / w4, c = (t - i * w4) * 4;
+    int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
     float s = coef * (vec ? vec[i] : 1.f);
     const int64_t src = in_map ? (int64_t)in_map[i] : i;
     float4 v = *reinterpret_cast<const float4*>(in + src * ldi + c);
@@ -491,7 +491,7 @@ __global__ void scale_cols_kernel(const float* in, int64_t ldi, float* out, int6
                                   const float* __restrict__ colvec) {
   const int64_t tot = rows * w4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / w4, c = (t - i * w4) * 4;
+    const int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
     const float4 v = *reinterpret_cast<const float4*>(in + i * ldi + c);
     const float4 s = *reinterpret_cast<const float4*>(colvec + c);
     *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s.x * v.x, s.y * v.y, s.z * v.z, s.w * v.w);
@@ -502,7 +502,7 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ G, int64_t ldg, flo
                                   int64_t rows, int64_t cols) {
   int64_t tot = rows * cols;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / cols, j = t - i * cols;
+    int64_t i = row_of(t, cols), j = t - i * cols;
     out[i * ldo + j] = (float)G[i * ldg + j];
   }
 }
@@ -512,7 +512,7 @@ __global__ void check_finite_kernel(const float* __restrict__ A, int64_t lda, in
   int64_t tot = rows * cols;
   int bad = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / cols, j = t - i * cols;
+    int64_t i = row_of(t, cols), j = t - i * cols;
     if (!isfinite(A[i * lda + j])) bad = 1;
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status->nonfinite, 1);

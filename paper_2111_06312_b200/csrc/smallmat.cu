@@ -554,7 +554,7 @@ __global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int6
     const int k4 = k >> 2;
     const int64_t tot = rows * k4;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = t / k4;
+      const int64_t i = row_of(t, k4);
       const int c = (int)(t - i * k4) * 4;
       float4* p = reinterpret_cast<float4*>(U + i * ldu + c);
       float4 v = *p;
@@ -565,7 +565,7 @@ __global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int6
   } else {
     const int64_t tot = rows * k;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = t / k;
+      const int64_t i = row_of(t, k);
       const int c = (int)(t - i * k);
       const float v = U[i * ldu + c] * sgn[c];
       bad |= !isfinite(v);
