@@ -19,11 +19,15 @@ import scipy.sparse as sp
 # ---------------------------------------------------------------------------
 
 
-def adjacency(n: int, row_ptr, col_idx) -> sp.csr_matrix:
-    """A in R^{n x n}: A_ij = edge weight, 1 for the unweighted configs."""
+def adjacency(n: int, row_ptr, col_idx, values=None) -> sp.csr_matrix:
+    """A in R^{n x n}: A_ij = edge weight ("A_ij is set to their edge weight"); every
+    stored A_ij = 1 when `values` is None (the unweighted configs, reading O12)."""
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
     col_idx = np.asarray(col_idx, dtype=np.int64)
-    vals = np.ones(col_idx.size, dtype=np.float64)
+    if values is None:
+        vals = np.ones(col_idx.size, dtype=np.float64)
+    else:
+        vals = np.asarray(values, dtype=np.float64)
     return sp.csr_matrix((vals, col_idx, row_ptr), shape=(n, n))
 
 

@@ -570,3 +570,82 @@ def test_label_reuse_implicit_equals_explicit():
     Q = rng.standard_normal((15, 5))
     assert np.allclose(op.matmul(G), M @ G, rtol=0, atol=1e-12)
     assert np.allclose(op.matmul_T(Q), M.T @ Q, rtol=0, atol=1e-12)
+
+
+# --------------------------------------------- weighted graphs and the A_hat NE basis
+
+
+def _Aw(n, wedges):
+    """Symmetric weighted A from (i, j, w) triples."""
+    import scipy.sparse as sps
+
+    r = [i for i, j, _ in wedges] + [j for i, j, _ in wedges]
+    c = [j for i, j, _ in wedges] + [i for i, j, _ in wedges]
+    v = [w for _, _, w in wedges] * 2
+    A = sps.csr_matrix((v, (r, c)), shape=(n, n))
+    A.sort_indices()
+    return adjacency(n, A.indptr, A.indices, A.data)
+
+
+def test_weighted_path_hand_values():
+    """Path 0-1-2 with A_01 = 2, A_12 = 1 ("A_ij is set to their edge weight").  By hand:
+    d = (2, 3, 1) -> T = D^-1 A = [[0, 1, 0], [2/3, 0, 1/3], [0, 1, 0]] (P:67);
+    s = (d+1)^-1/2 = (1/sqrt3, 1/2, 1/sqrt2) -> A_hat = S (A+I) S (P:68) has
+    A_hat_00 = 1/3, A_hat_01 = 2 (1/sqrt3)(1/2) = 1/sqrt3, A_hat_11 = 1/4, A_hat_12 = 1/(2 sqrt2),
+    A_hat_22 = 1/2."""
+    A = _Aw(3, [(0, 1, 2.0), (1, 2, 1.0)])
+    assert np.allclose(transition(A).toarray(), [[0, 1, 0], [2 / 3, 0, 1 / 3], [0, 1, 0]], rtol=0, atol=1e-15)
+    Ah = sym_norm_adj(A).toarray()
+    want = np.array([[1 / 3, 1 / np.sqrt(3), 0], [1 / np.sqrt(3), 1 / 4, 1 / (2 * np.sqrt(2))],
+                     [0, 1 / (2 * np.sqrt(2)), 1 / 2]])
+    assert np.allclose(Ah, want, rtol=0, atol=1e-15)
+
+
+def test_weighted_ne_null_vector_and_unit_weights():
+    """Weighted T is still row-stochastic, so M 1 = 0 for sum w = 1, lambda = 1/n; unit
+    weights reproduce the unweighted operator exactly."""
+    rng = np.random.default_rng(8)
+    n = 40
+    A0 = _random_connected(n, 30, rng)
+    Aw = adjacency(n, A0.indptr, A0.indices, 0.5 + rng.random(A0.nnz))
+    Aw = sp_sym(Aw)
+    op = NEOperator(Aw, uniform_weights(5), 1.0 / n)
+    assert np.abs(op.matmul(np.ones((n, 1)))).max() < 1e-14
+    A1 = adjacency(n, A0.indptr, A0.indices, np.ones(A0.nnz))
+    G = rng.standard_normal((n, 3))
+    assert np.array_equal(NEOperator(A1, uniform_weights(3), 1 / n).matmul(G),
+                          NEOperator(A0, uniform_weights(3), 1 / n).matmul(G))
+
+
+def sp_sym(A):
+    """(A + A^T) / 2 as a CSR adjacency with sorted indices (symmetric weights)."""
+    import scipy.sparse as sps
+
+    S = sps.csr_matrix((A + A.T) / 2.0)
+    S.sort_indices()
+    return adjacency(S.shape[0], S.indptr, S.indices, S.data)
+
+
+@pytest.mark.parametrize("C", [1, 3, 5])
+def test_ne_ahat_basis_cycle_spectrum(C):
+    """NE over A_hat on the cycle C_n: d = 2, A_hat = (A + I)/3 with eigenvalues
+    (1 + 2 cos(2 pi j/n))/3; the j = 0 direction (eigenvalue 1, vector 1) is cancelled by the
+    rank-1 term when sum w = 1, lambda = 1/n.  So sigma(M) = {|sum_c w_c ((1 + 2 cos(2 pi j / n))/3)^c|:
+    j = 1..n-1} plus 0, and M = M^T."""
+    w = uniform_weights(C)
+    for n in range(6, 15):
+        op = NEOperator(_cycle(n), w, 1.0 / n, basis="Ahat")
+        Md = op.dense()
+        assert np.allclose(Md, Md.T, rtol=0, atol=1e-15)
+        lam = (1 + 2 * np.cos(2 * np.pi * np.arange(1, n) / n)) / 3
+        want = np.sort(np.abs([sum(w[c - 1] * x ** c for c in range(1, C + 1)) for x in lam]))[::-1]
+        _, _, _, s_all = isvd(op, n - 1, philox_omega(300 + n, 0, n, n), iterations=2)
+        assert np.allclose(s_all[: n - 1], want, rtol=0, atol=1e-13)
+
+
+def test_ne_ahat_basis_complete_graph_is_zero():
+    """K_n: A_hat = (J - I + I)/n = J/n, so every power is J/n and sum_c w_c J/n - (1/n) J = 0 when
+    sum w = 1 (P:158 with the configs' lambda = 1/n)."""
+    for n in range(4, 10):
+        op = NEOperator(_complete(n), context_weights(4), 1.0 / n, basis="Ahat")
+        assert np.abs(op.dense()).max() < 1e-15
