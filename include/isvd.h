@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define ISVD_ABI_VERSION 1
+#define ISVD_ABI_VERSION 2
 
 typedef enum {
   ISVD_OK = 0,
@@ -62,11 +62,30 @@ typedef enum {
 typedef struct isvd_ctx_s* isvd_ctx;
 typedef struct isvd_graph_s* isvd_graph;
 typedef struct isvd_op_s* isvd_op;
+typedef struct isvd_sim_group_s* isvd_sim_group;
+
+/* Device memory supplier (north_star: "PyTorch is used only for device memory, streams and
+ * process groups").  alloc(bytes, stream, user) returns a 16-byte aligned device pointer on the
+ * ctx's device, usable on `stream` (a cudaStream_t as void*), or NULL on failure
+ * (-> ISVD_ERR_OOM); free(ptr, stream, user) gives it back.  The library calls free only after
+ * the work that used the block has completed on the host-visible timeline (it synchronises its
+ * stream first), so a stream-ordered caching allocator may reuse the block at once.  With an
+ * allocator the library keeps no cache of its own. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* user);
+  void (*free)(void* ptr, void* stream, void* user);
+  void* user;
+} isvd_allocator;
 
 /* ------------------------------------------------------------------ context */
 
 /* Create a context on CUDA device `device`, enqueuing on `stream`
  * (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ * alloc == NULL: device workspace comes from cudaMalloc, cached by the context (buffers of
+ *             destroyed graphs / operators are reused by later objects of the same sizes, trimmed
+ *             when an allocation fails, released by isvd_ctx_destroy; ISVD_NO_POOL=1 disables
+ *             the cache).  alloc != NULL: every device buffer comes from the caller's allocator
+ *             (copied struct; the Python binding wires PyTorch's caching allocator).
  * nccl_unique_id == NULL: single GPU (world must be 1).  Large graphs are then
  *             relabelled internally by degree (hub rows contiguous and kept
  *             L2-persisting; every caller-ordered input and output is mapped at
@@ -75,16 +94,30 @@ typedef struct isvd_op_s* isvd_op;
  *             the 128-byte ncclUniqueId that rank 0 created (isvd_nccl_unique_id)
  *             and every rank received out of band; the call is collective.  The
  *             row-partitioned schedule (all-gather of every SpMM gather source,
- *             fp64 all-reduce of Gram / column sums / X^T Z) runs even for world 1.
- * Device workspace is allocated with cudaMalloc when an op first needs it. */
-isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world,
-                            isvd_ctx* out);
+ *             fp64 all-reduce of Gram / column sums / X^T Z) runs even for world 1. */
+isvd_status isvd_ctx_create(int device, void* stream, const isvd_allocator* alloc, const void* nccl_unique_id,
+                            int rank, int world, isvd_ctx* out);
 isvd_status isvd_ctx_destroy(isvd_ctx ctx);
 /* Fill the 128-byte buffer `id_out` with a fresh ncclUniqueId (rank 0 only). */
 isvd_status isvd_nccl_unique_id(void* id_out, size_t id_bytes);
 const char* isvd_status_string(isvd_status s);
 const char* isvd_last_error(isvd_ctx ctx); /* never NULL; "" when no error */
 int isvd_abi_version(void);
+
+/* Simulated ranks (a TEST backend of the distributed layout, SURVEY 8(c) "simulation mode"):
+ * `world` (1..16) logical ranks on ONE device, one context per rank, each driven by its own
+ * host thread.  The contexts run the same row-partitioned schedule as the NCCL path (padded
+ * all-gathers of every SpMM gather source, fp64 all-reduces, the sign-rule candidate gather);
+ * the collectives move data with one cudaMemcpyAsync per peer slice (all-gather) or one
+ * rank-ordered sum kernel (all-reduce), ordered across the ranks' streams by events and host
+ * barriers only (no kernel waits on another rank).  Every collective call (graph/op creation
+ * do none; isvd_matmul, isvd_matmul_T, isvd_svd and isvd_least_norm do) must be made by all
+ * ranks of the group, in the same order.  The solver is not captured as a CUDA graph in this
+ * mode.  isvd_sim_group_destroy returns ISVD_ERR_BUSY while contexts of the group live. */
+isvd_status isvd_sim_group_create(int world, isvd_sim_group* out);
+isvd_status isvd_sim_group_destroy(isvd_sim_group group);
+isvd_status isvd_ctx_create_sim(int device, void* stream, const isvd_allocator* alloc, isvd_sim_group group,
+                                int rank, isvd_ctx* out);
 
 /* Row partition used by the distributed layout: rows [*row_begin, *row_begin + *n_local). */
 isvd_status isvd_partition(int64_t n, int world, int rank, int64_t* row_begin, int64_t* n_local);
@@ -98,21 +131,23 @@ enum {
   ISVD_BORROW = 8u             /* op keeps the caller's device X instead of copying it            */
 };
 
-/* Unweighted graph A (A_ij = 1 for every stored (i, j), reading O12)
- * given as this rank's rows in CSR: row_ptr int64[n_local + 1] (row_ptr[0] may
- * be nonzero: it is subtracted), col_idx int32[nnz] holding GLOBAL node ids.
- * Rows must hold no self-loop and no duplicate (reading O16; A + I adds the
- * diagonal itself).  The graph copies both arrays into device memory it owns
- * (the caller may free its inputs on return) and computes, once, in fp64:
+/* Graph A given as this rank's rows in CSR: row_ptr int64[n_local + 1] (row_ptr[0] may be
+ * nonzero: it is subtracted), col_idx int32[nnz] holding GLOBAL node ids, and
+ * values: NULL (unweighted, A_ij = 1 for every stored (i, j); reading O12) or fp32[nnz] edge
+ * weights A_ij ("A_ij is set to their edge weight"; finite, >= 0; same host/device
+ * kind as col_idx).  Rows must hold no self-loop and no duplicate (reading O16; A + I adds the
+ * diagonal itself).  The graph copies every array into device memory it owns (the caller may
+ * free its inputs on return) and computes, once, in fp64 from the degrees d_i = sum_j A_ij
+ * (integer for unweighted graphs):
  *   inv_deg_i = 1 / d_i      (T = D^-1 A; d_i = 0 -> 0, reading O3)
  *   s_i = (d_i + 1)^-1/2     (A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2)
  * stored in fp32.  Transposes are never built: this build requires
  * ISVD_GRAPH_SYMMETRIC (all configs are undirected), so T^T = A D^-1 and
  * A_hat^T = A_hat are the same CSR with the scale moved; without the flag
- * the call returns ISVD_ERR_UNSUPPORTED.
+ * the call returns ISVD_ERR_UNSUPPORTED.  ISVD_GRAPH_VALIDATE also checks every weight.
  * Row partition: (row_begin, n_local) must equal isvd_partition(n_global, world, rank). */
 isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
-                              const int64_t* row_ptr, const int32_t* col_idx, uint32_t flags,
+                              const int64_t* row_ptr, const int32_t* col_idx, const float* values, uint32_t flags,
                               isvd_graph* out);
 /* ISVD_ERR_BUSY while ops reference it.  Device memory of destroyed graphs / operators goes
  * back to the context's cache (reused by later graphs / operators of the same sizes, trimmed
@@ -128,6 +163,13 @@ typedef enum {
   ISVD_OP_POWER_SUM = 1,           /* NE, Eq. 3: M = sum_c w_c T^c - lambda_ones 1 1^T          */
   ISVD_OP_STACKED_PROPAGATION = 2  /* NC, Eq. 6: M = [X | A_hat X | ... | A_hat^L X]            */
 } isvd_op_kind;
+
+/* NE basis (Section 2.1: "replace T by A_hat, recovering a basis where L = R"). */
+typedef enum {
+  ISVD_BASIS_DEFAULT = 0,  /* = ISVD_BASIS_T_ROW                                                 */
+  ISVD_BASIS_T_ROW = 1,    /* T = D^-1 A (Eq. 3 as printed)                           */
+  ISVD_BASIS_AHAT_SYM = 2  /* A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2: M is symmetric  */
+} isvd_basis;
 
 typedef struct {
   isvd_op_kind kind;
@@ -150,6 +192,8 @@ typedef struct {
   int64_t y, ldy;
   int32_t lr_powers;
   uint32_t y_flags;
+  int32_t basis;          /* NE: isvd_basis (0 = T).  NC: must be 0 (its basis is A_hat)  */
+  int32_t pad0;
 } isvd_op_desc;
 
 /* Define an implicit matrix over graph g.  No O(nnz) work; copies w (and X
@@ -202,6 +246,12 @@ typedef struct {
   double ms_spmm;         /* ISVD_SVD_PROFILE: summed CUDA-event time of those steps, else 0 */
   double spmm_alg_bytes;  /* algorithmic bytes of those steps (CSR + scales + gather source
                              read once + epilogue operand + output)           */
+  /* ISVD_SVD_PROFILE: CUDA-event time by phase (the solver's stream, so the phases sum to about
+   * ms_total); 0 otherwise.  products = every M Q / M^T Q (SpMM chains, NC dense terms, their
+   * all-gathers); orth = the CholeskyQR passes (Grams, Cholesky, applies, their all-reduces);
+   * small = Omega, the final SVD of R^T, U / V and the sign rule; comm = the collectives alone
+   * (a subset of the other three). */
+  double ms_products, ms_orth, ms_small, ms_comm;
 } isvd_svd_report;
 
 /* Rank-k randomized SVD of M (Alg. 1) with CholeskyQR2

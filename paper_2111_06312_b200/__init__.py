@@ -9,6 +9,7 @@ from .api import (  # noqa: F401
     NE,
     Context,
     Graph,
+    SimGroup,
     SvdResult,
     embeddings,
     least_norm,
@@ -19,5 +20,5 @@ from .api import (  # noqa: F401
     round_up,
 )
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
+__all__ = ["Context", "SimGroup", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
            "nccl_unique_id", "partition", "padded", "round_up"]

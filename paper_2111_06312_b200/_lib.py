@@ -26,6 +26,17 @@ ISVD_BORROW = 8
 ISVD_OP_POWER_SUM = 1
 ISVD_OP_STACKED_PROPAGATION = 2
 
+ISVD_BASIS_DEFAULT = 0
+ISVD_BASIS_T_ROW = 1
+ISVD_BASIS_AHAT_SYM = 2
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
 ISVD_SVD_OMEGA_PROVIDED = 1
 ISVD_SVD_HOST_OUTPUT = 2
 ISVD_SVD_NO_GRAPH = 4
@@ -49,6 +60,8 @@ class OpDesc(C.Structure):
         ("ldy", C.c_int64),
         ("lr_powers", C.c_int32),
         ("y_flags", C.c_uint32),
+        ("basis", C.c_int32),
+        ("pad0", C.c_int32),
     ]
 
 
@@ -76,6 +89,10 @@ class SvdReport(C.Structure):
         ("pad0", C.c_int32),
         ("ms_spmm", C.c_double),
         ("spmm_alg_bytes", C.c_double),
+        ("ms_products", C.c_double),
+        ("ms_orth", C.c_double),
+        ("ms_small", C.c_double),
+        ("ms_comm", C.c_double),
     ]
 
 
@@ -86,10 +103,15 @@ SIGNATURES = {
     "isvd_last_error": (C.c_char_p, [C.c_void_p]),
     "isvd_partition": (C.c_int, [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "isvd_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_size_t]),
-    "isvd_ctx_create": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "isvd_ctx_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(Allocator), C.c_void_p, C.c_int, C.c_int,
+                                  C.POINTER(C.c_void_p)]),
+    "isvd_sim_group_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "isvd_sim_group_destroy": (C.c_int, [C.c_void_p]),
+    "isvd_ctx_create_sim": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(Allocator), C.c_void_p, C.c_int,
+                                      C.POINTER(C.c_void_p)]),
     "isvd_ctx_destroy": (C.c_int, [C.c_void_p]),
     "isvd_graph_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
-                                    C.c_uint32, C.POINTER(C.c_void_p)]),
+                                    C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
     "isvd_graph_destroy": (C.c_int, [C.c_void_p]),
     "isvd_graph_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                   C.POINTER(C.c_int64)]),

@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from ._lib import check
 
-__all__ = ["Context", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
+__all__ = ["Context", "SimGroup", "Graph", "NE", "NC", "SvdResult", "embeddings", "least_norm", "spectral_kernel",
            "nccl_unique_id", "partition", "padded", "round_up"]
 
 
@@ -64,19 +64,68 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _torch_allocator(device_index: int) -> "_lib.Allocator":
+    """isvd_allocator over PyTorch's caching allocator (north_star: PyTorch supplies device memory).
+    A failed allocation returns NULL, which the library reports as ISVD_ERR_OOM."""
+
+    def alloc(nbytes, stream, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device_index, int(stream or 0))
+        except Exception:  # out of memory (or any failure) -> NULL, never an exception across the ABI
+            return None
+
+    def free(ptr, stream, user):
+        if ptr:
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+    a = _lib.Allocator()
+    a.alloc = _lib.ALLOC_FN(alloc)
+    a.free = _lib.FREE_FN(free)
+    a.user = None
+    return a
+
+
+class SimGroup:
+    """isvd_sim_group: `world` logical ranks of the row-partitioned schedule on ONE device (a test
+    backend).  Each rank needs its own Context(sim_group=..., rank=r) driven by its own thread."""
+
+    def __init__(self, world: int):
+        self.lib = _lib.load()
+        self.world = int(world)
+        h = C.c_void_p()
+        check(self.lib.isvd_sim_group_create(self.world, C.byref(h)), "isvd_sim_group_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(self.lib.isvd_sim_group_destroy(self.h), "isvd_sim_group_destroy")
+            self.h = None
+
+
 class Context:
-    """isvd_ctx: device, stream and (world > 1) the NCCL communicator."""
+    """isvd_ctx: device, stream, device memory and (world > 1) the rank group.
+
+    allocator: "torch" (default: every device buffer from PyTorch's caching allocator) or None
+    (the library's own cudaMalloc cache).  nccl_id: NCCL distributed mode; sim_group: simulated
+    ranks on one device (test backend of the same schedule)."""
 
     def __init__(self, device: int = 0, stream: "torch.cuda.Stream | None" = None, rank: int = 0, world: int = 1,
-                 nccl_id: "bytes | None" = None):
+                 nccl_id: "bytes | None" = None, sim_group: "SimGroup | None" = None, allocator="torch"):
         self.lib = _lib.load()
         self.device = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.rank, self.world = rank, world
+        self._alloc = _torch_allocator(device) if allocator == "torch" else None
+        ap = C.byref(self._alloc) if self._alloc is not None else None
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        check(self.lib.isvd_ctx_create(device, C.c_void_p(self.stream.cuda_stream), idbuf, rank, world, C.byref(h)),
-              "isvd_ctx_create")
+        if sim_group is not None:
+            self.world = sim_group.world
+            check(self.lib.isvd_ctx_create_sim(device, C.c_void_p(self.stream.cuda_stream), ap, sim_group.h, rank,
+                                               C.byref(h)), "isvd_ctx_create_sim")
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            check(self.lib.isvd_ctx_create(device, C.c_void_p(self.stream.cuda_stream), ap, idbuf, rank, world,
+                                           C.byref(h)), "isvd_ctx_create")
         self.h = h
 
     def close(self):
@@ -92,9 +141,10 @@ class Context:
 
 
 class Graph:
-    """isvd_graph: this rank's rows of the symmetric, unweighted adjacency A in CSR."""
+    """isvd_graph: this rank's rows of the symmetric adjacency A in CSR; `values` are the
+    edge weights A_ij (None: unweighted, every A_ij = 1)."""
 
-    def __init__(self, ctx: Context, n: int, row_ptr, col_idx, validate: bool = False):
+    def __init__(self, ctx: Context, n: int, row_ptr, col_idx, values=None, validate: bool = False):
         self.ctx = ctx
         lib = ctx.lib
         self.n = int(n)
@@ -103,19 +153,23 @@ class Graph:
         if isinstance(row_ptr, torch.Tensor) and row_ptr.is_cuda:
             rp = row_ptr.to(torch.int64).contiguous()
             ci = col_idx.to(torch.int32).contiguous()
+            vv = None if values is None else torch.as_tensor(values, device=rp.device).to(torch.float32).contiguous()
             flags |= _lib.ISVD_PTR_DEVICE
-            keep = (rp, ci)
+            keep = (rp, ci, vv)
             prp, pci = rp.data_ptr(), ci.data_ptr()
+            pv = 0 if vv is None else vv.data_ptr()
         else:
             rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
             ci = np.ascontiguousarray(col_idx, dtype=np.int32)
-            keep = (rp, ci)
+            vv = None if values is None else np.ascontiguousarray(values, dtype=np.float32)
+            keep = (rp, ci, vv)
             prp, pci = rp.ctypes.data, ci.ctypes.data
+            pv = 0 if vv is None else vv.ctypes.data
         if len(keep[0]) != self.n_local + 1:
             raise ValueError(f"row_ptr must have n_local + 1 = {self.n_local + 1} entries for rank {ctx.rank}")
         h = C.c_void_p()
         check(lib.isvd_graph_create(ctx.h, self.n, self.row_begin, self.n_local, C.c_void_p(prp), C.c_void_p(pci),
-                                    flags, C.byref(h)), "isvd_graph_create", ctx.h)
+                                    C.c_void_p(pv or None), flags, C.byref(h)), "isvd_graph_create", ctx.h)
         self.h = h
 
     def info(self):
@@ -142,6 +196,7 @@ class SvdResult:
     spmm_steps: int = 0
     ms_spmm: float = 0.0
     spmm_alg_bytes: float = 0.0
+    phases: "dict | None" = None  # profile=True: ms by phase (products / orth / small / comm)
 
 
 class _Operator:
@@ -258,14 +313,18 @@ class _Operator:
         U = U[: self.graph.n_local, :k]
         V = V[: self.c_rows(), :k]
         S = S[:k]
+        phases = None
+        if profile:
+            phases = dict(products=rep.ms_products, orth=rep.ms_orth, small=rep.ms_small, comm=rep.ms_comm)
         return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
-                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes)
+                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases)
 
 
 class NE(_Operator):
-    """M = sum_{c=1..C} w_c T^c - lambda_ones 1 1^T, T = D^-1 A   (Eq. 3)."""
+    """M = sum_{c=1..C} w_c B^c - lambda_ones 1 1^T + lambda_adj A   (Eq. 3),
+    B = T = D^-1 A (basis "T") or B = A_hat (basis "Ahat", the symmetric variant of P:158)."""
 
-    def __init__(self, graph: Graph, weights, lambda_ones: float, lambda_adj: float = 0.0):
+    def __init__(self, graph: Graph, weights, lambda_ones: float, lambda_adj: float = 0.0, basis: str = "T"):
         w = np.ascontiguousarray(weights, dtype=np.float64)
         d = _lib.OpDesc()
         d.kind = _lib.ISVD_OP_POWER_SUM
@@ -273,6 +332,9 @@ class NE(_Operator):
         d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
         d.lambda_ones = float(lambda_ones)
         d.lambda_adj = float(lambda_adj)
+        if basis not in ("T", "Ahat"):
+            raise ValueError("basis must be 'T' or 'Ahat'")
+        d.basis = _lib.ISVD_BASIS_T_ROW if basis == "T" else _lib.ISVD_BASIS_AHAT_SYM
         super().__init__(graph, d, keep=(w,))
 
     def c_rows(self) -> int:

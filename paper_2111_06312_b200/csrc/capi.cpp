@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -39,12 +40,59 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// P logical ranks of the row-partitioned schedule on ONE device (a test backend, SURVEY 8(c)
+// "simulation mode"): one context and one host thread per rank.  The collectives keep the real
+// partitioned schedule (padded all-gathers, fp64 all-reduces, the sign-rule candidate gather)
+// and move the data with one cudaMemcpyAsync per peer slice (all-gather) or one rank-ordered
+// sum kernel (all-reduce).  Ordering across the ranks' streams uses events only -- no kernel
+// ever waits on another rank's kernel: each collective is two host barriers, a cross-stream
+// event wait on every peer's "ready" event, the copies / sum on the rank's own stream, and a
+// wait on every peer's "done" event before the rank may overwrite what peers read.
+struct isvd_sim_group_s {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<const void*> ptr;        // per rank: the buffer published for this collective
+  std::vector<cudaEvent_t> ready, done;
+  std::atomic<int> members{0};
+  bool broken = false;  // a rank timed out: every later collective of the group fails
+  // false on timeout (ISVD_SIM_TIMEOUT_S, default 120 s): a peer never reached this collective
+  bool barrier() {
+    static const double timeout_s = getenv("ISVD_SIM_TIMEOUT_S") ? atof(getenv("ISVD_SIM_TIMEOUT_S")) : 120.0;
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const uint64_t gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return true;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
+                                [&] { return generation != gen || broken; });
+    if (!ok || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
 struct isvd_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
-  bool dist = false;  // NCCL collectives on (nccl id given); the row partition follows `world`
+  bool dist = false;  // row-partitioned schedule on (NCCL id or simulated group given); partition follows `world`
   ncclComm_t comm = nullptr;
+  isvd_sim_group_s* sim = nullptr;  // simulated ranks on one device (test backend), else null
+  double* sim_tmp = nullptr;        // all-reduce staging of the simulated backend
+  size_t sim_tmp_count = 0;
+  std::vector<void*> sim_allocs;
+  isvd_allocator alloc{};           // caller's device allocator (e.g. PyTorch's caching allocator)
+  bool has_alloc = false;
   int num_sms = 148;
   std::string last_error;
   DevStatus* status = nullptr;  // device
@@ -59,6 +107,9 @@ struct isvd_ctx_s {
   int spmm_steps = 0;
   double spmm_alg_bytes = 0.0;
   std::vector<cudaEvent_t> prof_events;  // pairs
+  // ISVD_SVD_PROFILE phase brackets: (phase, start event index, end event index) into phase_ev
+  std::vector<cudaEvent_t> phase_ev;
+  std::vector<int> phase_tag;  // per pair: 0 products, 1 orth, 2 small, 3 comm
   // caching device allocator: buffers released by destroyed graphs / ops / workspaces are kept
   // (by exact rounded size) and handed out again, so rebuilding a graph + operator of the same
   // shape pays no cudaMalloc/cudaFree (they cost ~ms per GB-sized buffer); trimmed on OOM and
@@ -73,6 +124,7 @@ struct isvd_graph_s {
   int64_t n = 0, row_begin = 0, n_local = 0, n_pad = 0, nnz = 0, max_deg = 0;
   int64_t* row_ptr = nullptr;  // device, rebased to 0
   int32_t* col_idx = nullptr;  // device
+  float* val = nullptr;        // device edge weights (null: unweighted)
   float* inv_deg = nullptr;    // 1/d (0 for d = 0)
   float* s = nullptr;          // (d+1)^-1/2
   float* s2 = nullptr;         // (d+1)^-1
@@ -107,6 +159,7 @@ struct SolverWs {
 struct isvd_op_s {
   isvd_graph g = nullptr;
   isvd_op_kind kind = ISVD_OP_POWER_SUM;
+  bool ahat_basis = false;  // NE over A_hat instead of T
   int terms = 0;
   std::vector<double> w;
   double lambda_ones = 0.0;
@@ -169,6 +222,8 @@ void set_err(isvd_ctx ctx, const std::string& m) {
     }                                                                                                         \
   } while (0)
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 void pool_trim(isvd_ctx ctx) {
   std::lock_guard<std::mutex> lk(ctx->pool_mu);
   for (auto& kv : ctx->pool_free) {
@@ -182,6 +237,14 @@ void* dmalloc(isvd_ctx ctx, size_t bytes, std::vector<void*>& list) {
   void* p = nullptr;
   bytes = (bytes + 511) / 512 * 512;
   if (bytes == 0) bytes = 512;
+  if (ctx->has_alloc) {  // the caller's allocator (it caches; the library keeps no pool then)
+    p = ctx->alloc.alloc(bytes, ctx->stream, ctx->alloc.user);
+    REQ(p != nullptr, ISVD_ERR_OOM, "the caller's allocator returned null");
+    REQ(aligned16(p), ISVD_ERR_INVALID_ARG, "the caller's allocator returned a pointer that is not 16-byte aligned");
+    list.push_back(p);
+    CK(cudaMemsetAsync(p, 0, bytes, ctx->stream));
+    return p;
+  }
   {
     std::lock_guard<std::mutex> lk(ctx->pool_mu);
     auto it = ctx->pool_free.find(bytes);
@@ -200,8 +263,9 @@ void* dmalloc(isvd_ctx ctx, size_t bytes, std::vector<void*>& list) {
     ctx->pool_size[p] = bytes;
   }
   list.push_back(p);
-  // padding columns of every iterate must read as zero: workspaces start cleared
-  CK(cudaMemset(p, 0, bytes));
+  // padding columns of every iterate must read as zero: workspaces start cleared (on the ctx
+  // stream, so the clearing is ordered before every later use whatever stream kind it is)
+  CK(cudaMemsetAsync(p, 0, bytes, ctx->stream));
   return p;
 }
 
@@ -209,6 +273,10 @@ void* dmalloc(isvd_ctx ctx, size_t bytes, std::vector<void*>& list) {
 // synchronise the stream before releasing, as they did before cudaFree)
 void dfree(isvd_ctx ctx, void* p) {
   if (!p) return;
+  if (ctx->has_alloc) {
+    ctx->alloc.free(p, ctx->stream, ctx->alloc.user);
+    return;
+  }
   static const bool no_pool = getenv("ISVD_NO_POOL") && getenv("ISVD_NO_POOL")[0] == '1';
   std::lock_guard<std::mutex> lk(ctx->pool_mu);
   if (no_pool) {
@@ -235,8 +303,6 @@ struct DeviceGuard {
   }
 };
 
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
 void partition(int64_t n, int world, int rank, int64_t* rb, int64_t* nl) {
   int64_t chunk = (n + world - 1) / world;
   int64_t b = std::min<int64_t>(n, chunk * rank);
@@ -245,16 +311,97 @@ void partition(int64_t n, int world, int rank, int64_t* rb, int64_t* nl) {
   *nl = e - b;
 }
 
+// ------------------------------------------------------------ phase profiling
+// ISVD_SVD_PROFILE: CUDA events bracket every phase of the solver on its stream
+// (isvd_svd_report ms_products / ms_orth / ms_small / ms_comm).
+enum PhaseTag { kPhProducts = 0, kPhOrth = 1, kPhSmall = 2, kPhComm = 3 };
+struct Phase {
+  isvd_ctx ctx;
+  size_t i = (size_t)-1;
+  Phase(isvd_ctx c, PhaseTag tag) : ctx(c) {
+    if (!ctx->profiling) return;
+    i = ctx->phase_tag.size();
+    while (ctx->phase_ev.size() < 2 * i + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) { i = (size_t)-1; return; }
+      ctx->phase_ev.push_back(e);
+    }
+    ctx->phase_tag.push_back((int)tag);
+    cudaEventRecord(ctx->phase_ev[2 * i], ctx->stream);
+  }
+  ~Phase() {
+    if (i != (size_t)-1) cudaEventRecord(ctx->phase_ev[2 * i + 1], ctx->stream);
+  }
+};
+
 // --------------------------------------------------------------- collectives
+// In-place all-gather: rank p's `bytes_per_rank` bytes sit at recv + p * bytes_per_rank.
+void coll_allgather(isvd_ctx ctx, void* recv, size_t bytes_per_rank) {
+  if (!ctx->dist || bytes_per_rank == 0) return;
+  Phase ph(ctx, kPhComm);
+  char* r = static_cast<char*>(recv);
+  if (ctx->comm) {
+    NK(ncclAllGather(r + (size_t)ctx->rank * bytes_per_rank, r, bytes_per_rank, ncclChar, ctx->comm, ctx->stream));
+    return;
+  }
+  isvd_sim_group_s* g = ctx->sim;
+  const int me = ctx->rank;
+  g->ptr[me] = recv;
+  CK(cudaEventRecord(g->ready[me], ctx->stream));
+  REQ(g->barrier(), ISVD_ERR_BUSY, "simulated ranks: a peer did not reach the collective (timeout)");
+  for (int q = 0; q < g->world; ++q) {
+    if (q == me) continue;
+    CK(cudaStreamWaitEvent(ctx->stream, g->ready[q], 0));
+    const char* src = static_cast<const char*>(g->ptr[q]) + (size_t)q * bytes_per_rank;
+    CK(cudaMemcpyAsync(r + (size_t)q * bytes_per_rank, src, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CK(cudaEventRecord(g->done[me], ctx->stream));
+  REQ(g->barrier(), ISVD_ERR_BUSY, "simulated ranks: a peer did not reach the collective (timeout)");
+  for (int q = 0; q < g->world; ++q)
+    if (q != me) CK(cudaStreamWaitEvent(ctx->stream, g->done[q], 0));  // peers finished reading my buffer
+}
+
 void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld) {
-  if (!ctx->dist) return;
-  size_t count = (size_t)g->n_pad * ld;
-  NK(ncclAllGather(full + (size_t)ctx->rank * count, full, count, ncclFloat, ctx->comm, ctx->stream));
+  coll_allgather(ctx, full, sizeof(float) * (size_t)g->n_pad * ld);
 }
 
 void allreduce_f64(isvd_ctx ctx, double* buf, size_t count) {
-  if (!ctx->dist) return;
-  NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  if (!ctx->dist || count == 0) return;
+  Phase ph(ctx, kPhComm);
+  if (ctx->comm) {
+    NK(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return;
+  }
+  isvd_sim_group_s* g = ctx->sim;
+  const int me = ctx->rank;
+  if (count > ctx->sim_tmp_count) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (void* p : ctx->sim_allocs) dfree(ctx, p);
+    ctx->sim_allocs.clear();
+    ctx->sim_tmp = (double*)dmalloc(ctx, sizeof(double) * count, ctx->sim_allocs);
+    ctx->sim_tmp_count = count;
+  }
+  g->ptr[me] = buf;
+  CK(cudaEventRecord(g->ready[me], ctx->stream));
+  REQ(g->barrier(), ISVD_ERR_BUSY, "simulated ranks: a peer did not reach the collective (timeout)");
+  RankPtrs rp{};
+  for (int q = 0; q < g->world; ++q) {
+    rp.p[q] = static_cast<const double*>(g->ptr[q]);
+    if (q != me) CK(cudaStreamWaitEvent(ctx->stream, g->ready[q], 0));
+  }
+  CK(launch_sum_ranks(rp, g->world, (int64_t)count, ctx->sim_tmp, ctx->stream));
+  CK(cudaEventRecord(g->done[me], ctx->stream));
+  REQ(g->barrier(), ISVD_ERR_BUSY, "simulated ranks: a peer did not reach the collective (timeout)");
+  for (int q = 0; q < g->world; ++q)
+    if (q != me) CK(cudaStreamWaitEvent(ctx->stream, g->done[q], 0));
+  CK(cudaMemcpyAsync(buf, ctx->sim_tmp, sizeof(double) * count, cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// recv (world x count doubles) <- every rank's send (count doubles), in rank order
+void allgather_f64(isvd_ctx ctx, const double* send, double* recv, size_t count) {
+  CK(cudaMemcpyAsync(recv + (size_t)ctx->rank * count, send, sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  coll_allgather(ctx, recv, sizeof(double) * count);
 }
 
 // ------------------------------------------------------------------ op workspace
@@ -363,6 +510,7 @@ void gemm_fp32(isvd_op op, const float* A, int64_t lda, const float* B, int64_t 
 SpmmArgs spmm_base(const isvd_graph_s* g, int64_t wpad) {
   SpmmArgs a{};
   a.col_idx = g->col_idx;
+  a.val = g->val;
   a.row_offset = g->row_begin;
   a.post_coef = 1.f;
   a.term_coef = 1.f;
@@ -397,6 +545,7 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
   // once (all n rows), the epilogue operand T, the output
   double nl = (double)g->n_local, w = (double)a.wpad;
   double b = 8.0 * (nl + 1) + 4.0 * (double)g->nnz + 4.0 * (double)g->n * w + 4.0 * nl * w;
+  if (a.val) b += 4.0 * (double)g->nnz;  // edge weights
   if (a.post_vec) b += 4.0 * nl;
   if (a.term_vec) b += 4.0 * nl;
   if (a.T) b += 4.0 * nl * w;
@@ -515,6 +664,60 @@ void ne_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
   }
   SpmmArgs a = spmm_base(g, wpad);
   a.Y = src; a.ldy = wpad;
+  a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
+  if (op->adjbuf) { a.T = op->adjbuf; a.ldt = wpad; }
+  a.out = out; a.ldo = ldo; a.out_map = omap;
+  spmm(ctx, op, a);
+}
+
+// NE over the symmetric basis A_hat ("replace T by A_hat, recovering a basis where L = R"):
+// M = sum_c w_c A_hat^c - lambda_ones 1 1^T + lambda_adj A is symmetric, so M^T Q = M Q.
+// Horner on pre-scaled iterates Ht = s H (A_hat H = s (A+I) Ht, as for NC):
+//   Ht_C = s w_C Q;  Ht_c = w_c s Q + s^2 ((A+I) Ht_{c+1});  M Q = s ((A+I) Ht_1) - lambda 1 cs^T (+ lambda_adj A Q).
+void ne_ahat_matmul(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad,
+                    bool user_order) {
+  isvd_graph g = op->g;
+  const int C = op->terms;
+  const int32_t* omap = nullptr;
+  CK(launch_colsum(Q, g->n_local, wpad, ldq, op->colsum_ws, op->colsum, ctx->stream));
+  allreduce_f64(ctx, op->colsum, wpad);
+  if (user_order && g->new2old) {
+    CK(launch_scale_rows(Q, ldq, op->ptmp, wpad, g->n_local, wpad, nullptr, 1.f, nullptr, ctx->stream, g->new2old));
+    Q = op->ptmp;
+    ldq = wpad;
+    omap = g->new2old;
+  }
+  if (op->adjbuf) {  // lambda_adj A Q from Q's full rows (A symmetric)
+    const float* qf = Q;
+    int64_t ldqf = ldq;
+    if (ctx->dist) {
+      CK(launch_scale_rows(Q, ldq, slice(g, op->full_b, wpad), wpad, g->n_local, wpad, nullptr, 1.f, nullptr,
+                           ctx->stream));
+      allgather_rows(ctx, g, op->full_b, wpad);
+      qf = op->full_b;
+      ldqf = wpad;
+    }
+    ne_adj_term(ctx, op, qf, ldqf, wpad);
+  }
+  CK(launch_scale_rows(Q, ldq, slice(g, op->full_a, wpad), wpad, g->n_local, wpad, g->s, (float)op->w[C - 1], nullptr,
+                       ctx->stream));
+  allgather_rows(ctx, g, op->full_a, wpad);
+  const float* src = op->full_a;
+  float* bufs[2] = {op->full_b, op->full_c};
+  for (int c = C - 1; c >= 1; --c) {
+    float* dst_full = bufs[c & 1];
+    SpmmArgs a = spmm_base(g, wpad);
+    a.Y = src; a.ldy = wpad; a.self_coef = 1.f;
+    a.post_vec = g->s2;
+    a.T = Q; a.ldt = ldq; a.term_vec = g->s; a.term_coef = (float)op->w[c - 1];
+    a.out = slice(g, dst_full, wpad); a.ldo = wpad;
+    spmm(ctx, op, a);
+    allgather_rows(ctx, g, dst_full, wpad);
+    src = dst_full;
+  }
+  SpmmArgs a = spmm_base(g, wpad);
+  a.Y = src; a.ldy = wpad; a.self_coef = 1.f;
+  a.post_vec = g->s;
   a.colsum = op->colsum; a.rank1_coef = op->lambda_ones;
   if (op->adjbuf) { a.T = op->adjbuf; a.ldt = wpad; }
   a.out = out; a.ldo = ldo; a.out_map = omap;
@@ -758,14 +961,18 @@ void nc_matmul_T(isvd_ctx ctx, isvd_op op, const float* Q, int64_t ldq, float* o
 void op_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool user_order) {
   isvd_ctx ctx = op->g->ctx;
   ensure_op_ws(op, wpad);
-  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  Phase ph(ctx, kPhProducts);
+  if (op->kind == ISVD_OP_POWER_SUM && op->ahat_basis) ne_ahat_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  else if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else nc_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
 }
 
 void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool user_order) {
   isvd_ctx ctx = op->g->ctx;
   ensure_op_ws(op, wpad);
-  if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  Phase ph(ctx, kPhProducts);
+  if (op->kind == ISVD_OP_POWER_SUM && op->ahat_basis) ne_ahat_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  else if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
 }
 
@@ -836,42 +1043,57 @@ isvd_status isvd_nccl_unique_id(void* id_out, size_t id_bytes) {
   return ISVD_OK;
 }
 
-isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id, int rank, int world, isvd_ctx* out) {
-  if (!out || world < 1 || rank < 0 || rank >= world) return ISVD_ERR_INVALID_ARG;
-  if (world > 1 && nccl_unique_id == nullptr) return ISVD_ERR_INVALID_ARG;
+namespace {
+// Device, streams, events and status word of a new context (shared by both creation paths).
+void ctx_init(isvd_ctx ctx, int device, void* stream, const isvd_allocator* alloc, int rank, int world) {
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  REQ(device >= 0 && device < ndev, ISVD_ERR_INVALID_ARG, "device out of range");
+  if (alloc) {
+    REQ(alloc->alloc && alloc->free, ISVD_ERR_INVALID_ARG, "allocator needs both alloc and free");
+    ctx->alloc = *alloc;
+    ctx->has_alloc = true;
+  }
+  ctx->device = device;
+  DeviceGuard dg(device);
+  ctx->stream = (cudaStream_t)stream;
+  ctx->rank = rank;
+  ctx->world = world;
+  CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  int major = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  REQ(major == 10, ISVD_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
+  CK(cudaMalloc(&ctx->status, sizeof(DevStatus)));
+  CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventCreate(&ctx->ev0));
+  CK(cudaEventCreate(&ctx->ev1));
+  CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  ctx->ov_ev.resize(16);
+  for (auto& e : ctx->ov_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int persist = 0;
+  CK(cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+  ctx->max_persist_l2 = (size_t)persist;
+}
+
+isvd_status ctx_create_common(int device, void* stream, const isvd_allocator* alloc, const void* nccl_unique_id,
+                              isvd_sim_group_s* sim, int rank, int world, isvd_ctx* out) {
   *out = nullptr;
   isvd_ctx ctx = new (std::nothrow) isvd_ctx_s();
   if (!ctx) return ISVD_ERR_OOM;
   isvd_status st = guarded(ctx, [&] {
-    int ndev = 0;
-    CK(cudaGetDeviceCount(&ndev));
-    REQ(device >= 0 && device < ndev, ISVD_ERR_INVALID_ARG, "device out of range");
-    ctx->device = device;
+    ctx_init(ctx, device, stream, alloc, rank, world);
     DeviceGuard dg(device);
-    ctx->stream = (cudaStream_t)stream;
-    ctx->rank = rank;
-    ctx->world = world;
-    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
-    int major = 0;
-    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
-    REQ(major == 10, ISVD_ERR_UNSUPPORTED, "this library is built for sm_100a (B200) only");
-    CK(cudaMalloc(&ctx->status, sizeof(DevStatus)));
-    CK(cudaMemset(ctx->status, 0, sizeof(DevStatus)));
-    CK(cudaEventCreate(&ctx->ev0));
-    CK(cudaEventCreate(&ctx->ev1));
-    CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
-    CK(cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-    ctx->ov_ev.resize(16);
-    for (auto& e : ctx->ov_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    int persist = 0;
-    CK(cudaDeviceGetAttribute(&persist, cudaDevAttrMaxPersistingL2CacheSize, device));
-    ctx->max_persist_l2 = (size_t)persist;
     if (nccl_unique_id) {  // distributed mode (also world == 1: NCCL path with a 1-rank communicator)
       ctx->dist = true;
       ncclUniqueId id;
       memcpy(&id, nccl_unique_id, sizeof(id));
       NK(ncclCommInitRank(&ctx->comm, world, id, rank));
+    } else if (sim) {
+      ctx->dist = true;
+      ctx->sim = sim;
     }
   });
   if (st != ISVD_OK) {
@@ -880,8 +1102,59 @@ isvd_status isvd_ctx_create(int device, void* stream, const void* nccl_unique_id
     delete ctx;
     return st;
   }
+  if (sim) sim->members++;
   *out = ctx;
   return ISVD_OK;
+}
+}  // namespace
+
+isvd_status isvd_ctx_create(int device, void* stream, const isvd_allocator* alloc, const void* nccl_unique_id,
+                            int rank, int world, isvd_ctx* out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return ISVD_ERR_INVALID_ARG;
+  if (world > 1 && nccl_unique_id == nullptr) return ISVD_ERR_INVALID_ARG;
+  return ctx_create_common(device, stream, alloc, nccl_unique_id, nullptr, rank, world, out);
+}
+
+isvd_status isvd_sim_group_create(int world, isvd_sim_group* out) {
+  if (!out || world < 1 || world > kMaxSimRanks) return ISVD_ERR_INVALID_ARG;
+  *out = nullptr;
+  isvd_sim_group_s* g = new (std::nothrow) isvd_sim_group_s();
+  if (!g) return ISVD_ERR_OOM;
+  g->world = world;
+  g->ptr.assign(world, nullptr);
+  g->ready.assign(world, nullptr);
+  g->done.assign(world, nullptr);
+  for (int q = 0; q < world; ++q) {
+    if (cudaEventCreateWithFlags(&g->ready[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->done[q], cudaEventDisableTiming) != cudaSuccess) {
+      (void)cudaGetLastError();
+      for (int r = 0; r < world; ++r) {
+        if (g->ready[r]) cudaEventDestroy(g->ready[r]);
+        if (g->done[r]) cudaEventDestroy(g->done[r]);
+      }
+      delete g;
+      return ISVD_ERR_CUDA;
+    }
+  }
+  *out = g;
+  return ISVD_OK;
+}
+
+isvd_status isvd_sim_group_destroy(isvd_sim_group g) {
+  if (!g) return ISVD_ERR_INVALID_ARG;
+  if (g->members.load() > 0) return ISVD_ERR_BUSY;
+  for (int q = 0; q < g->world; ++q) {
+    cudaEventDestroy(g->ready[q]);
+    cudaEventDestroy(g->done[q]);
+  }
+  delete g;
+  return ISVD_OK;
+}
+
+isvd_status isvd_ctx_create_sim(int device, void* stream, const isvd_allocator* alloc, isvd_sim_group group, int rank,
+                                isvd_ctx* out) {
+  if (!out || !group || rank < 0 || rank >= group->world) return ISVD_ERR_INVALID_ARG;
+  return ctx_create_common(device, stream, alloc, nullptr, group, rank, group->world, out);
 }
 
 isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
@@ -890,6 +1163,8 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
   DeviceGuard dg(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (void* p : ctx->sim_allocs) dfree(ctx, p);
+  if (ctx->sim) ctx->sim->members--;
   pool_trim(ctx);
   if (ctx->status) cudaFree(ctx->status);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
@@ -911,7 +1186,8 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
 
 // ===================================================================== graph
 isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
-                              const int64_t* row_ptr, const int32_t* col_idx, uint32_t flags, isvd_graph* out) {
+                              const int64_t* row_ptr, const int32_t* col_idx, const float* values, uint32_t flags,
+                              isvd_graph* out) {
   if (!ctx || !out) return ISVD_ERR_INVALID_ARG;
   *out = nullptr;
   isvd_graph g = new (std::nothrow) isvd_graph_s();
@@ -940,8 +1216,12 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       t_last = t;
     };
     std::vector<int64_t> rp(n_local + 1);
-    if (dev) CK(cudaMemcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
-    else memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1));
+    if (dev) {  // on the ctx stream: ordered after the caller's producer on that stream
+      CK(cudaMemcpyAsync(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+      memcpy(rp.data(), row_ptr, sizeof(int64_t) * (n_local + 1));
+    }
     const int64_t base = rp[0];
     for (auto& v : rp) v -= base;
     for (int64_t i = 0; i < n_local; ++i)
@@ -966,14 +1246,25 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->row_ptr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
     g->col_idx = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nnz + kIdxPad), g->allocs);
     int32_t* ci_in = relabel ? (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(nnz, 1), tmp) : g->col_idx;
-    if (nnz > 0)
-      CK(cudaMemcpy(ci_in, col_idx + base, sizeof(int32_t) * nnz,
-                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (nnz > 0) CK(cudaMemcpyAsync(ci_in, col_idx + base, sizeof(int32_t) * nnz, kind, ctx->stream));
+    // edge weights: moved with their edges
+    float* val_in = nullptr;
+    if (values) {
+      g->val = (float*)dmalloc(ctx, sizeof(float) * (nnz + kIdxPad), g->allocs);
+      val_in = relabel ? (float*)dmalloc(ctx, sizeof(float) * std::max<int64_t>(nnz, 1), tmp) : g->val;
+      if (nnz > 0) CK(cudaMemcpyAsync(val_in, values + base, sizeof(float) * nnz, kind, ctx->stream));
+    }
     if (flags & ISVD_GRAPH_VALIDATE) {
       std::vector<int32_t> ci(nnz);
-      if (nnz) CK(cudaMemcpy(ci.data(), ci_in, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost));
+      if (nnz) CK(cudaMemcpyAsync(ci.data(), ci_in, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+      std::vector<float> vv(values ? nnz : 0);
+      if (values && nnz)
+        CK(cudaMemcpyAsync(vv.data(), val_in, sizeof(float) * nnz, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
       for (int64_t e = 0; e < nnz; ++e)
         REQ(ci[e] >= 0 && ci[e] < n_global, ISVD_ERR_INDEX, "col_idx outside [0, n)");
+      for (float v : vv) REQ(std::isfinite(v) && v >= 0.f, ISVD_ERR_NONFINITE, "edge weights must be finite and >= 0");
     }
     phase("csr_upload");
     // Degree relabelling (single rank, large graphs; SURVEY 8(d2) "allowed optimisation"):
@@ -999,8 +1290,8 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
       g->new2old = (int32_t*)dmalloc(ctx, sizeof(int32_t) * n_local, g->allocs);
       CK(launch_degree_order(d_rp_in, n_local, keys2, idx, g->new2old, d_new_of_old, deg_tmp, g->row_ptr, temp,
                              temp_bytes, ctx->stream));
-      CK(launch_relabel_csr(d_rp_in, ci_in, g->new2old, d_new_of_old, g->row_ptr, g->col_idx, n_local,
-                            ctx->stream));
+      CK(launch_relabel_csr(d_rp_in, ci_in, val_in, g->new2old, d_new_of_old, g->row_ptr, g->col_idx, g->val,
+                            n_local, ctx->stream));
       if (ctx->max_persist_l2 > 0) {
         static bool limit_set = false;  // process-wide L2 set-aside for persisting accesses
         if (!limit_set) {
@@ -1016,7 +1307,7 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->s = (float*)dmalloc(ctx, nb, g->allocs);
     g->s2 = (float*)dmalloc(ctx, nb, g->allocs);
     g->rs = (float*)dmalloc(ctx, nb, g->allocs);
-    CK(launch_scales(g->row_ptr, n_local, g->inv_deg, g->s, g->s2, g->rs, ctx->stream));
+    CK(launch_scales(g->row_ptr, g->val, n_local, g->inv_deg, g->s, g->s2, g->rs, ctx->stream));
     phase("scales");
     // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
     // split, their partial sums combined by the fixup pass in segment order (graph_build.cu)
@@ -1089,15 +1380,22 @@ float* own_rows(isvd_ctx ctx, isvd_graph g, const float* src_in, int64_t ld, boo
   std::vector<void*> tmp;
   const size_t row_bytes = sizeof(float) * (size_t)ld;
   float* x = (float*)dmalloc(ctx, row_bytes * (size_t)std::max<int64_t>(g->n_local, 1), tmp);
+  struct FreeOnThrow {  // the copy below may fail (bad pointer / alignment): do not leak x
+    isvd_ctx c;
+    float* p;
+    ~FreeOnThrow() { if (p) dfree(c, p); }
+  } guard{ctx, x};
   if (g->n_local > 0) {
     if (!g->new2old) {
-      CK(cudaMemcpy(x, src_in, row_bytes * (size_t)g->n_local, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(x, src_in, row_bytes * (size_t)g->n_local, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
     } else {
       const float* src = src_in;
       std::vector<void*> stage;
       if (!dev) {
         float* d = (float*)dmalloc(ctx, row_bytes * (size_t)g->n_local, stage);
-        CK(cudaMemcpy(d, src_in, row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(d, src_in, row_bytes * (size_t)g->n_local, cudaMemcpyHostToDevice, ctx->stream));
         src = d;
       }
       REQ(aligned16(src), ISVD_ERR_INVALID_ARG, "row blocks must be 16-byte aligned");
@@ -1106,6 +1404,7 @@ float* own_rows(isvd_ctx ctx, isvd_graph g, const float* src_in, int64_t ld, boo
       for (void* q : stage) dfree(ctx, q);
     }
   }
+  guard.p = nullptr;
   return x;
 }
 }  // namespace
@@ -1121,7 +1420,10 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
     op->g = g;
     op->kind = desc->kind;
     op->terms = desc->num_terms;
+    REQ(desc->basis == ISVD_BASIS_DEFAULT || desc->basis == ISVD_BASIS_T_ROW || desc->basis == ISVD_BASIS_AHAT_SYM,
+        ISVD_ERR_INVALID_ARG, "unknown basis");
     if (desc->kind == ISVD_OP_POWER_SUM) {
+      op->ahat_basis = desc->basis == ISVD_BASIS_AHAT_SYM;
       REQ(desc->num_terms >= 1, ISVD_ERR_INVALID_ARG, "NE needs C >= 1 powers");
       REQ(desc->weights != nullptr, ISVD_ERR_INVALID_ARG, "NE weights are null");
       op->w.assign(desc->weights, desc->weights + desc->num_terms);
@@ -1132,6 +1434,7 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
       op->lambda_adj = desc->lambda_adj;
     } else if (desc->kind == ISVD_OP_STACKED_PROPAGATION) {
       REQ(desc->num_terms >= 0, ISVD_ERR_INVALID_ARG, "NC needs L >= 0");
+      REQ(desc->basis != ISVD_BASIS_T_ROW, ISVD_ERR_UNSUPPORTED, "NC propagates with A_hat (Eq. 6, P:68) only");
       REQ(desc->d >= 1, ISVD_ERR_INVALID_ARG, "NC feature width d must be >= 1");
       REQ(desc->ldx >= desc->d && desc->ldx % 4 == 0, ISVD_ERR_INVALID_ARG, "ldx must be >= d and a multiple of 4");
       REQ(desc->X != nullptr || g->n_local == 0, ISVD_ERR_INVALID_ARG, "X is null");
@@ -1165,7 +1468,10 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
       REQ(false, ISVD_ERR_INVALID_ARG, "unknown op kind");
     }
   });
-  if (st != ISVD_OK) {
+  if (st != ISVD_OK) {  // give back whatever the op had already taken
+    if (op->own_x) dfree(ctx, (void*)op->X);
+    dfree(ctx, op->Xrs);
+    dfree(ctx, (void*)op->Ylr);
     delete op;
     return st;
   }
@@ -1242,8 +1548,10 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
 // ==================================================================== solver
 namespace {
 
-// Everything a captured solver graph bakes in (FNV-1a over the argument values).
-uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t ldu, const float* V, int64_t ldv) {
+// Everything a captured solver graph bakes in (FNV-1a over the argument values).  The graph writes
+// U and V into the op's own buffers (copied out after each replay), so the caller's output
+// pointers are not part of the key: a new pair of output tensors per call still replays.
+uint64_t graph_key(const isvd_svd_params* p, int64_t l, int64_t ldk) {
   uint64_t h = 0xCBF29CE484222325ULL;
   auto mix = [&](uint64_t v) {
     for (int b = 0; b < 8; ++b) {
@@ -1252,8 +1560,7 @@ uint64_t graph_key(const isvd_svd_params* p, int64_t l, const float* U, int64_t 
     }
   };
   mix((uint64_t)p->k); mix((uint64_t)(uint32_t)p->oversampling); mix((uint64_t)p->power_iters); mix(p->seed);
-  mix(p->flags); mix((uint64_t)(uintptr_t)p->omega); mix((uint64_t)l); mix((uint64_t)(uintptr_t)U);
-  mix((uint64_t)ldu); mix((uint64_t)(uintptr_t)V); mix((uint64_t)ldv);
+  mix(p->flags); mix((uint64_t)(uintptr_t)p->omega); mix((uint64_t)l); mix((uint64_t)ldk);
   mix((uint64_t)tc_for_grams() | (uint64_t)tc_for_products() << 1);
   return h;
 }
@@ -1436,7 +1743,7 @@ isvd_status isvd_least_norm(isvd_ctx ctx, int64_t r_local, int64_t k, const floa
     double* T = (double*)dmalloc(ctx, sizeof(double) * k * ny, tmp);
     CK(launch_atb(Ua, lda, Ya, ldb, nr, k, ny, nullptr, false, ws, T, ny, nullptr, 0, ctx->num_sms, nullptr,
                   ctx->stream, false));
-    if (ctx->dist) NK(ncclAllReduce(T, T, (size_t)k * ny, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    allreduce_f64(ctx, T, (size_t)k * ny);
     // S^+ T on the host (k x ny, small), reading O24's cut
     std::vector<double> h((size_t)k * ny);
     CK(cudaMemcpyAsync(h.data(), T, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1520,16 +1827,20 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   // Alg. 1 line 4: Q ~ N(0,1)^{c x l}
   // (NE on a relabelled graph: Omega's rows are node ids, mapped to the internal order)
   const int32_t* omap = ne ? g->new2old : nullptr;
-  if (p->flags & ISVD_SVD_OMEGA_PROVIDED) {
-    CK(launch_scale_rows(p->omega, ld, s.Qc, ld, cr, ld, nullptr, 1.f, nullptr, ctx->stream, omap));
-  } else {
-    CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, omap, ctx->stream));
+  {
+    Phase ph(ctx, kPhSmall);
+    if (p->flags & ISVD_SVD_OMEGA_PROVIDED) {
+      CK(launch_scale_rows(p->omega, ld, s.Qc, ld, cr, ld, nullptr, 1.f, nullptr, ctx->stream, omap));
+    } else {
+      CK(launch_omega(p->seed, ne ? g->row_begin : 0, cr, (int)l, ld, s.Qc, omap, ctx->stream));
+    }
   }
   // r-side orthonormalisation: with a small c side (NC) the second CholeskyQR update is folded
   // into the small products (cqr2_deferred); otherwise the plain CholeskyQR2
   const bool fold = !ne && 4 * cr <= g->n;  // NC: c = d (L + 1) rows, replicated on every rank
   float* q_r = s.Yr;  // buffer holding the r-side orthonormal factor (times Rfold when folding)
   auto orth_r = [&](bool exact) {
+    Phase ph(ctx, kPhOrth);
     if (fold) {
       q_r = cqr2_deferred(op, s.Yr, s.Yr2, rr, l, force, exact);
     } else {
@@ -1541,6 +1852,7 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   auto mt_q = [&]() {
     if (fold) {
       op_matmul_T(op, q_r, ld, s.Qc2, ld, ld, false);
+      Phase ph(ctx, kPhProducts);
       gemm_fp32(op, s.Qc2, ld, s.Rfold, ld, s.Qc, ld, cr, ld, l, nullptr, false, nullptr);
     } else {
       op_matmul_T(op, q_r, ld, s.Qc, ld, ld, false);
@@ -1551,6 +1863,7 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
     op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);            // M Q       (r x l)
     orth_r(it == 0);                                         // orthonorm
     mt_q();                                                  // M^T Q     (c x l)
+    Phase ph(ctx, kPhOrth);
     cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr, true);  // orthonorm
   }
   // Alg. 1 line 9: Q <- orthonorm(M Q)
@@ -1558,7 +1871,11 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   orth_r(p->power_iters == 0);
   // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
   mt_q();
-  cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin, true);
+  {
+    Phase ph(ctx, kPhOrth);
+    cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, s.Rfin, true);
+  }
+  Phase ph(ctx, kPhSmall);
   // Alg. 1 line 11: svd(B) with B = R^T Q_W^T -> one-sided Jacobi on R^T
   CK(launch_jacobi_svd(s.Rfin, (int)l, (int)k, ldk, s.sigma, s.Ub, s.Vb, s.jac_ws, ctx->status, ctx->num_sms,
                        ctx->stream));
@@ -1575,7 +1892,7 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
   const double* cand = s.cand;
   if (ctx->dist) {
-    NK(ncclAllGather(s.cand, s.cand_all, 3 * k, ncclDouble, ctx->comm, ctx->stream));
+    allgather_f64(ctx, s.cand, s.cand_all, 3 * k);
     cand = s.cand_all;
   }
   // sign flip of U and V; the flip of U also flags non-finite output entries (one pass over U)
@@ -1604,6 +1921,8 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
                                 ISVD_SVD_FORCE_CHOL_FAIL | ISVD_SVD_PROFILE)) == 0,
         ISVD_ERR_INVALID_ARG, "unknown svd flag");
     REQ(!(p->flags & ISVD_SVD_OMEGA_PROVIDED) || p->omega, ISVD_ERR_INVALID_ARG, "omega is null");
+    REQ(!(p->flags & ISVD_SVD_OMEGA_PROVIDED) || aligned16(p->omega), ISVD_ERR_INVALID_ARG,
+        "omega must be 16-byte aligned (its rows are read as float4, ld = round_up(l, 4))");
     const int64_t l = working_l(op, p);
     REQ(l <= 1024, ISVD_ERR_UNSUPPORTED, "working width l > 1024 is not supported by the small-matrix kernels");
     const int64_t k = p->k, ldk = round_up(k, 4);
@@ -1614,12 +1933,15 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     ensure_op_ws(op, round_up(l, 4));
     ensure_solver_ws(op, l, k);
     SolverWs& s = op->sws;
-    float* Ud = host_out ? s.Utmp : U;
-    float* Vd = host_out ? s.Vtmp : V;
-    const int64_t lduu = host_out ? ldk : ldu, ldvv = host_out ? ldk : ldv;
     // The solver runs on the context's private stream, joined to the caller's stream by
-    // events; without ISVD_SVD_NO_GRAPH / ISVD_SVD_PROFILE the whole enqueue sequence is
-    // captured once per argument set into a CUDA graph and replayed (one launch per isvd).
+    // events; without ISVD_SVD_NO_GRAPH / ISVD_SVD_PROFILE (and outside the simulated-rank
+    // backend) the whole enqueue sequence is captured once per argument set into a CUDA graph
+    // and replayed (one launch per isvd), writing U / V into the op's buffers.
+    const bool use_graph = !(p->flags & (ISVD_SVD_NO_GRAPH | ISVD_SVD_PROFILE)) && !s.graph_broken && !ctx->sim;
+    const bool staged = host_out || use_graph;
+    float* Ud = staged ? s.Utmp : U;
+    float* Vd = staged ? s.Vtmp : V;
+    const int64_t lduu = staged ? ldk : ldu, ldvv = staged ? ldk : ldv;
     cudaStream_t user = ctx->stream;
     CK(cudaEventRecord(ctx->ev_join, user));
     CK(cudaStreamWaitEvent(ctx->work, ctx->ev_join, 0));
@@ -1630,8 +1952,8 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     } swap_back{ctx, user};
     ctx->stream = ctx->work;
     ctx->profiling = p->flags & ISVD_SVD_PROFILE;
-    const uint64_t key = graph_key(p, l, Ud, lduu, Vd, ldvv);
-    const bool use_graph = !(p->flags & (ISVD_SVD_NO_GRAPH | ISVD_SVD_PROFILE)) && !s.graph_broken;
+    ctx->phase_tag.clear();
+    const uint64_t key = graph_key(p, l, ldk);
     int64_t launches = 0;
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_graph && (s.graph_exec == nullptr || s.graph_key != key)) {
@@ -1653,7 +1975,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
              cudaGraphInstantiate(&s.graph_exec, graph, 0) == cudaSuccess;
         if (graph) cudaGraphDestroy(graph);
       }
-      if (!ok) {  // some launch could not be captured: fall back to eager enqueue for this op
+      if (!ok) {  // some launch could not be captured: run eagerly for this op from now on
         (void)cudaGetLastError();
         if (s.graph_exec) cudaGraphExecDestroy(s.graph_exec);
         s.graph_exec = nullptr;
@@ -1678,12 +2000,19 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
       solver_body(op, p, l, Ud, lduu, Vd, ldvv);
       launches = g_launches - l0;
     }
+    const int64_t rr = op->g->n_local, cr = c_rows_local(op);
+    if (staged && !host_out) {  // the op's U / V buffers -> the caller's device outputs
+      if (rr > 0)
+        CK(cudaMemcpy2DAsync(U, ldu * sizeof(float), Ud, lduu * sizeof(float), ldk * sizeof(float), rr,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+      CK(cudaMemcpy2DAsync(V, ldv * sizeof(float), Vd, ldvv * sizeof(float), ldk * sizeof(float), cr,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     CK(cudaEventRecord(ctx->ev1, ctx->stream));
     DevStatus st;
     std::vector<double> sig(k);
     CK(cudaMemcpyAsync(sig.data(), s.sigma, sizeof(double) * k, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&st, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
-    const int64_t rr = op->g->n_local, cr = c_rows_local(op);
     if (host_out) {
       if (rr > 0)
         CK(cudaMemcpy2DAsync(U, ldu * sizeof(float), Ud, lduu * sizeof(float), k * sizeof(float), rr,
@@ -1707,11 +2036,18 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
       rep->spmm_steps = ctx->spmm_steps;
       rep->spmm_alg_bytes = ctx->spmm_alg_bytes;
       rep->ms_spmm = 0.0;
+      rep->ms_products = rep->ms_orth = rep->ms_small = rep->ms_comm = 0.0;
       if (p->flags & ISVD_SVD_PROFILE) {
         for (int i = 0; i < ctx->spmm_steps; ++i) {
           float t = 0.f;
           CK(cudaEventElapsedTime(&t, ctx->prof_events[2 * i], ctx->prof_events[2 * i + 1]));
           rep->ms_spmm += t;
+        }
+        double* acc[4] = {&rep->ms_products, &rep->ms_orth, &rep->ms_small, &rep->ms_comm};
+        for (size_t i = 0; i < ctx->phase_tag.size(); ++i) {
+          float t = 0.f;
+          CK(cudaEventElapsedTime(&t, ctx->phase_ev[2 * i], ctx->phase_ev[2 * i + 1]));
+          *acc[ctx->phase_tag[i]] += t;
         }
       }
     }

@@ -76,7 +76,7 @@ cudaError_t launch_scale_cols(const float* in, int64_t ldi, float* out, int64_t 
 
 // ------------------------------------------------------------------- SpMM
 // Fused CSR SpMM step (K1):  for each local row i (global id row_offset + i)
-//   acc_i = self_coef * Y[row_offset + i] + sum_{j in N(i)} Y[j]          (fp32 blocks of 8, fp64 across)
+//   acc_i = self_coef * Y[row_offset + i] + sum_{j in N(i)} A_ij Y[j]     (fp32 blocks of 8, fp64 across)
 //   out_i = post_coef * post_vec[i] * acc_i
 //         + term_coef * term_vec[i] * T[i]
 //         - rank1_coef * colsum                                          (all in fp64, one rounding)
@@ -102,6 +102,7 @@ constexpr int kIdxPad = 16;  // readable zero entries after col_idx[nnz - 1] (in
 
 struct SpmmArgs {
   const int32_t* col_idx;
+  const float* val;        // edge weights A_ij (nullable: unweighted, every A_ij = 1)
   int64_t row_offset;
   const float* Y; int64_t ldy;
   float self_coef;
@@ -113,10 +114,11 @@ struct SpmmArgs {
   int64_t wpad;            // columns processed (multiple of 4)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
-// Graph relabelling on the device: new row t = old row order[t], neighbour ids renamed by new_of_old.
-cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const int32_t* order,
-                               const int32_t* new_of_old, const int64_t* rp_new, int32_t* ci_new, int64_t n,
-                               cudaStream_t st);
+// Graph relabelling on the device: new row t = old row order[t], neighbour ids renamed by new_of_old
+// (edge weights, if any, move with their edges; the order inside a row is kept).
+cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const float* val_old,
+                               const int32_t* order, const int32_t* new_of_old, const int64_t* rp_new,
+                               int32_t* ci_new, float* val_new, int64_t n, cudaStream_t st);
 // Device-side graph build (graph_build.cu): degree order (stable, decreasing degree) with its
 // maps and the relabelled row_ptr; fp64-derived scale vectors; SpMM segment plan (count + scan,
 // then fill once the host has read the totals).  temp: graph_build_temp_bytes(n) bytes.
@@ -124,7 +126,9 @@ size_t graph_build_temp_bytes(int64_t n);
 cudaError_t launch_degree_order(const int64_t* rp, int64_t n, uint32_t* keys2, int32_t* idx, int32_t* order,
                                 int32_t* new_of_old, int64_t* deg_tmp, int64_t* rp_new, void* temp, size_t temp_bytes,
                                 cudaStream_t st);
-cudaError_t launch_scales(const int64_t* rp, int64_t n, float* inv, float* s, float* s2, float* rs, cudaStream_t st);
+// val: null (unweighted: d_i = edge count) or fp32 edge weights (d_i = sum_j A_ij in fp64).
+cudaError_t launch_scales(const int64_t* rp, const float* val, int64_t n, float* inv, float* s, float* s2, float* rs,
+                          cudaStream_t st);
 cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32_t* nsplit, int32_t* nslot,
                               int64_t* seg_off, int32_t* split_off, int32_t* slot_off, void* temp, size_t temp_bytes,
                               cudaStream_t st);
@@ -218,5 +222,13 @@ cudaError_t launch_sign_flip(const double* cand, int world, int k, float* sgn_ws
 // status->nonfinite |= any(!isfinite(A[:rows, :cols])).
 cudaError_t launch_check_finite(const float* A, int64_t lda, int64_t rows, int64_t cols, DevStatus* status,
                                 cudaStream_t st);
+
+// Simulated ranks (capi.cpp SimGroup, a test backend): out[i] = sum over q < world of p.p[q][i],
+// summed in rank order (bitwise identical on every logical rank).
+constexpr int kMaxSimRanks = 16;
+struct RankPtrs {
+  const double* p[kMaxSimRanks];
+};
+cudaError_t launch_sum_ranks(const RankPtrs& p, int world, int64_t count, double* out, cudaStream_t st);
 
 }  // namespace isvd

@@ -898,4 +898,23 @@ cudaError_t launch_check_finite(const float* A, int64_t lda, int64_t rows, int64
   return cudaGetLastError();
 }
 
+// ---- simulated ranks (test backend of the row-partitioned schedule, capi.cpp SimGroup) ----
+// out[i] = sum_{q = 0..world-1} in_q[i], always in rank order: every logical rank runs this same
+// kernel on the same inputs, so the all-reduced values are bitwise identical across ranks.
+namespace {
+__global__ void sum_ranks_kernel(RankPtrs p, int world, int64_t count, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < world; ++q) s += p.p[q][i];
+    out[i] = s;
+  }
+}
+}  // namespace
+
+cudaError_t launch_sum_ranks(const RankPtrs& p, int world, int64_t count, double* out, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  ++g_launches; sum_ranks_kernel<<<grid_for(count, 256, 148 * 4), 256, 0, st>>>(p, world, count, out);
+  return cudaGetLastError();
+}
+
 }  // namespace isvd

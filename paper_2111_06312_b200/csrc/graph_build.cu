@@ -35,14 +35,33 @@ __global__ void relabel_maps_kernel(const int64_t* __restrict__ rp, const int32_
   }
 }
 
+ISVD_DEVICE void write_scales(int64_t i, double d, float* inv, float* s, float* s2, float* rs) {
+  inv[i] = d > 0.0 ? (float)(1.0 / d) : 0.f;
+  s[i] = (float)(1.0 / sqrt(d + 1.0));
+  s2[i] = (float)(1.0 / (d + 1.0));
+  rs[i] = (float)sqrt(d + 1.0);
+}
+
+// unweighted: d_i = number of stored edges (exact integer)
 __global__ void scales_kernel(const int64_t* __restrict__ rp, int64_t n, float* __restrict__ inv,
                               float* __restrict__ s, float* __restrict__ s2, float* __restrict__ rs) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double d = (double)(rp[i + 1] - rp[i]);
-    inv[i] = d > 0.0 ? (float)(1.0 / d) : 0.f;
-    s[i] = (float)(1.0 / sqrt(d + 1.0));
-    s2[i] = (float)(1.0 / (d + 1.0));
-    rs[i] = (float)sqrt(d + 1.0);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    write_scales(i, (double)(rp[i + 1] - rp[i]), inv, s, s2, rs);
+}
+
+// weighted: d_i = sum_j A_ij in fp64, one warp per row (lane-strided sums, then a fixed
+// xor tree: deterministic)
+__global__ void scales_weighted_kernel(const int64_t* __restrict__ rp, const float* __restrict__ val, int64_t n,
+                                       float* __restrict__ inv, float* __restrict__ s, float* __restrict__ s2,
+                                       float* __restrict__ rs) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double d = 0.0;
+    for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) d += (double)val[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if (lane == 0) write_scales(i, d, inv, s, s2, rs);
   }
 }
 
@@ -116,9 +135,16 @@ cudaError_t launch_degree_order(const int64_t* rp, int64_t n, uint32_t* keys2, i
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t launch_scales(const int64_t* rp, int64_t n, float* inv, float* s, float* s2, float* rs, cudaStream_t st) {
+cudaError_t launch_scales(const int64_t* rp, const float* val, int64_t n, float* inv, float* s, float* s2, float* rs,
+                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  ++g_launches; scales_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, inv, s, s2, rs);
+  ++g_launches;
+  if (val) {
+    const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 16);
+    scales_weighted_kernel<<<(unsigned)blocks, 256, 0, st>>>(rp, val, n, inv, s, s2, rs);
+  } else {
+    scales_kernel<<<grid_n(n), 256, 0, st>>>(rp, n, inv, s, s2, rs);
+  }
   return cudaGetLastError();
 }
 

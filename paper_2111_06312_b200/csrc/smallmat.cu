@@ -87,10 +87,10 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
   extern __shared__ double smem[];
   __shared__ double s_scal[4];
   __shared__ int s_flag;
-  __shared__ double s_tmp[512];
+  __shared__ double s_tmp[1024];  // l <= 1024 (isvd_svd rejects wider working widths)
   double* A = (l <= kCholSmemMax) ? smem : ws;
   const int tid = threadIdx.x, nt = blockDim.x;
-  // trace and max diagonal (thread 0, l <= 512)
+  // trace and max diagonal (thread 0)
   if (tid == 0) {
     double tr = 0.0, mx = 0.0;
     for (int i = 0; i < l; ++i) {

@@ -60,41 +60,70 @@ ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4
 // Software-pipelined: the eight row loads of batch b+1 are issued before batch b is summed,
 // so 8-16 independent 16-byte loads per thread are in flight (measured: letting the
 // compiler interleave loads and adds left ~2 in flight and cost 20 % at config 4).
-ISVD_DEVICE void load_batch(const int32_t* __restrict__ idx, const float* __restrict__ y, int64_t ld, float4 v[8]) {
+// kW: weighted graph, each row scaled by its edge weight A_ij inside the fp32 batch.
+template <bool kW>
+ISVD_DEVICE void load_batch(const int32_t* __restrict__ idx, const float* __restrict__ val,
+                            const float* __restrict__ y, int64_t ld, float4 v[8], float wv[8]) {
   int j[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) j[u] = __ldg(idx + u);
+  if constexpr (kW) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) wv[u] = __ldg(val + u);
+  }
 #pragma unroll
   for (int u = 0; u < 8; ++u) v[u] = ldg4(y + (int64_t)j[u] * ld);
 }
 
-ISVD_DEVICE float4 sum_batch(const float4 v[8]) {
-  float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
-  return f4add(f4add(s01, s23), f4add(s45, s67));
+ISVD_DEVICE float4 f4fma(float a, float4 x, float4 c) {
+  return make_float4(fmaf(a, x.x, c.x), fmaf(a, x.y, c.y), fmaf(a, x.z, c.z), fmaf(a, x.w, c.w));
+}
+ISVD_DEVICE float4 f4mul(float a, float4 x) { return make_float4(a * x.x, a * x.y, a * x.z, a * x.w); }
+
+template <bool kW>
+ISVD_DEVICE float4 sum_batch(const float4 v[8], const float wv[8]) {
+  if constexpr (kW) {
+    float4 s01 = f4fma(wv[1], v[1], f4mul(wv[0], v[0])), s23 = f4fma(wv[3], v[3], f4mul(wv[2], v[2]));
+    float4 s45 = f4fma(wv[5], v[5], f4mul(wv[4], v[4])), s67 = f4fma(wv[7], v[7], f4mul(wv[6], v[6]));
+    return f4add(f4add(s01, s23), f4add(s45, s67));
+  } else {
+    float4 s01 = f4add(v[0], v[1]), s23 = f4add(v[2], v[3]), s45 = f4add(v[4], v[5]), s67 = f4add(v[6], v[7]);
+    return f4add(f4add(s01, s23), f4add(s45, s67));
+  }
 }
 
-ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, int len, const float* __restrict__ y, int64_t ld) {
+template <bool kW>
+ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __restrict__ val, int len,
+                                const float* __restrict__ y, int64_t ld) {
   Acc4 acc{0.0, 0.0, 0.0, 0.0};
   int e = 0;
   if (len >= 8) {
     float4 cur[8], nxt[8];
-    load_batch(idx, y, ld, cur);
+    float wc[8], wn[8];
+    load_batch<kW>(idx, val, y, ld, cur, wc);
     for (e = 8; e + 8 <= len; e += 8) {
-      load_batch(idx + e, y, ld, nxt);
-      acc_add(acc, sum_batch(cur));
+      load_batch<kW>(idx + e, kW ? val + e : val, y, ld, nxt, wn);
+      acc_add(acc, sum_batch<kW>(cur, wc));
 #pragma unroll
-      for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < 8; ++u) {
+        cur[u] = nxt[u];
+        if constexpr (kW) wc[u] = wn[u];
+      }
     }
-    acc_add(acc, sum_batch(cur));
+    acc_add(acc, sum_batch<kW>(cur, wc));
   }
   if (e < len) {
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (; e < len; ++e) t = f4add(t, ldg4(y + (int64_t)__ldg(idx + e) * ld));
+    for (; e < len; ++e) {
+      const float4 r = ldg4(y + (int64_t)__ldg(idx + e) * ld);
+      t = kW ? f4fma(__ldg(val + e), r, t) : f4add(t, r);
+    }
     acc_add(acc, t);
   }
   return acc;
 }
 
+template <bool kW>
 __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
                                                     const int64_t* __restrict__ seg_beg,
                                                     const int32_t* __restrict__ seg_len,
@@ -107,7 +136,8 @@ __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* _
   const float* __restrict__ Yc = a.Y + 4 * (int64_t)c4;
   for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
     const int64_t row = seg_row[s];
-    Acc4 acc = gather_segment(a.col_idx + seg_beg[s], seg_len[s], Yc, a.ldy);
+    const int64_t b = seg_beg[s];
+    Acc4 acc = gather_segment<kW>(a.col_idx + b, kW ? a.val + b : nullptr, seg_len[s], Yc, a.ldy);
     const int slot = seg_slot[s];
     if (slot < 0) {
       spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
@@ -161,26 +191,31 @@ int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad) { return plan.n_slots
 namespace {
 // One warp per new row t: copy old row order[t]'s neighbours, renamed through new_of_old.
 __global__ void relabel_csr_kernel(const int64_t* __restrict__ rp_old, const int32_t* __restrict__ ci_old,
-                                   const int32_t* __restrict__ order, const int32_t* __restrict__ new_of_old,
-                                   const int64_t* __restrict__ rp_new, int32_t* __restrict__ ci_new, int64_t n) {
+                                   const float* __restrict__ v_old, const int32_t* __restrict__ order,
+                                   const int32_t* __restrict__ new_of_old, const int64_t* __restrict__ rp_new,
+                                   int32_t* __restrict__ ci_new, float* __restrict__ v_new, int64_t n) {
   const int lane = threadIdx.x & 31;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n;
        t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t o = order[t];
     const int64_t b = rp_old[o], d = rp_old[o + 1] - b, dst = rp_new[t];
-    for (int64_t e = lane; e < d; e += 32) ci_new[dst + e] = new_of_old[ci_old[b + e]];
+    for (int64_t e = lane; e < d; e += 32) {
+      ci_new[dst + e] = new_of_old[ci_old[b + e]];
+      if (v_old) v_new[dst + e] = v_old[b + e];
+    }
   }
 }
 }  // namespace
 
-cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const int32_t* order,
-                               const int32_t* new_of_old, const int64_t* rp_new, int32_t* ci_new, int64_t n,
-                               cudaStream_t st) {
+cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, const float* val_old,
+                               const int32_t* order, const int32_t* new_of_old, const int64_t* rp_new,
+                               int32_t* ci_new, float* val_new, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = ceil_div(n * 32, 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   ++g_launches;
-  relabel_csr_kernel<<<(int)blocks, 256, 0, st>>>(rp_old, ci_old, order, new_of_old, rp_new, ci_new, n);
+  relabel_csr_kernel<<<(int)blocks, 256, 0, st>>>(rp_old, ci_old, val_old, order, new_of_old, rp_new, ci_new,
+                                                  val_new, n);
   return cudaGetLastError();
 }
 
@@ -220,8 +255,12 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ++g_launches;
-    spmm_kernel<<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len, plan.seg_slot,
-                                                 plan.n_seg, teams, ws_partial);
+    if (a.val)
+      spmm_kernel<true><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len,
+                                                         plan.seg_slot, plan.n_seg, teams, ws_partial);
+    else
+      spmm_kernel<false><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len,
+                                                          plan.seg_slot, plan.n_seg, teams, ws_partial);
     if (plan.n_split_rows > 0) {
       int64_t fb = ceil_div(plan.n_split_rows, teams);
       if (fb > cap) fb = cap;

@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.isvd_abi_version() == 1
+    assert lib.isvd_abi_version() == 2
     assert lib.isvd_status_string(0) == b"ok"
     assert lib.isvd_status_string(3) == b"rank out of range"
     assert lib.isvd_last_error(None) == b""
@@ -66,8 +66,25 @@ def test_ctx_create_fails_cleanly_without_gpu(lib):
     if torch.cuda.is_available():
         pytest.skip("GPU present")
     h = C.c_void_p()
-    st = lib.isvd_ctx_create(0, None, None, 0, 1, C.byref(h))
+    st = lib.isvd_ctx_create(0, None, None, None, 0, 1, C.byref(h))
     assert st != 0 and not h.value
+
+
+def test_sim_group_host_logic(lib):
+    """The simulated-rank group (test backend of the distributed schedule) validates its size and
+    refuses to be destroyed while contexts use it; creating a context on it needs a GPU."""
+    import torch
+
+    g = C.c_void_p()
+    assert lib.isvd_sim_group_create(0, C.byref(g)) == 1
+    assert lib.isvd_sim_group_create(17, C.byref(g)) == 1
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the -m gpu multi-rank tests")
+    # without a device the group's events cannot be created: a clean CUDA error, no handle
+    st = lib.isvd_sim_group_create(2, C.byref(g))
+    assert st in (0, 7)
+    if st == 0:
+        assert lib.isvd_sim_group_destroy(g) == 0
 
 
 def test_product_path_has_no_oracle_import():
