@@ -8,6 +8,7 @@
 // Gram / column-sum / X^T Z partials.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: phase ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <atomic>
@@ -312,13 +313,17 @@ void partition(int64_t n, int world, int rank, int64_t* rb, int64_t* nl) {
 }
 
 // ------------------------------------------------------------ phase profiling
-// ISVD_SVD_PROFILE: CUDA events bracket every phase of the solver on its stream
+// Every phase of the solver is an NVTX range ("isvd:products" / "isvd:orth" / "isvd:small" /
+// "isvd:comm"; host-side enqueue ranges, visible to nsys and `ncu --nvtx`).  With
+// ISVD_SVD_PROFILE, CUDA events also bracket each phase on the solver's stream
 // (isvd_svd_report ms_products / ms_orth / ms_small / ms_comm).
 enum PhaseTag { kPhProducts = 0, kPhOrth = 1, kPhSmall = 2, kPhComm = 3 };
 struct Phase {
   isvd_ctx ctx;
   size_t i = (size_t)-1;
   Phase(isvd_ctx c, PhaseTag tag) : ctx(c) {
+    static const char* names[4] = {"isvd:products", "isvd:orth", "isvd:small", "isvd:comm"};
+    nvtxRangePushA(names[tag]);
     if (!ctx->profiling) return;
     i = ctx->phase_tag.size();
     while (ctx->phase_ev.size() < 2 * i + 2) {
@@ -331,6 +336,7 @@ struct Phase {
   }
   ~Phase() {
     if (i != (size_t)-1) cudaEventRecord(ctx->phase_ev[2 * i + 1], ctx->stream);
+    nvtxRangePop();
   }
 };
 
@@ -2021,6 +2027,11 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
                            cudaMemcpyDeviceToHost, ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->comm) {  // a failed peer / network error surfaces here instead of as a hang later
+      ncclResult_t aerr = ncclSuccess;
+      NK(ncclCommGetAsyncError(ctx->comm, &aerr));
+      REQ(aerr == ncclSuccess, ISVD_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(aerr));
+    }
     CK(cudaEventRecord(ctx->ev_join, ctx->stream));
     CK(cudaStreamWaitEvent(user, ctx->ev_join, 0));
     float ms = 0.f;

@@ -51,7 +51,7 @@ def gpu_op(ctx, cfg, g, X, sp, device_inputs=True):
 
 PROD_TOL = 1e-5   # north_star: single products within 1e-5 relative (Frobenius)
 COL_TOL = 1e-5    # ... and every output column (SURVEY 8(c) "worst per-column relative error")
-ROW_TOL = 1e-4    # every output row (floor: 1e-3 of the rms row norm, see worst_row_rel)
+ROW_TOL = 1e-5    # every output row (floor: 1e-3 of the rms row norm, see worst_row_rel)
 SIG_TOL = 1e-4
 ANGLE_TOL = 1e-3
 
@@ -73,8 +73,9 @@ def worst_row_rel(Y, Yref, floor=1e-3) -> float:
     wrong rows (hub / split-fixup / ragged tail) cannot hide inside a Frobenius ratio.  Rows whose
     reference is numerically ~0 (a cancellation, e.g. the NE rank-1 term) are judged against the
     floor instead of their own tiny norm.  Per-row errors of fp32 storage with fp64 row
-    accumulation are ~1e-7 relative; the 1e-4 bar (ROW_TOL) leaves room for rows whose
-    reference is a partial cancellation of larger terms."""
+    accumulation are ~1e-7 relative (one fp32 rounding of the output plus fp32 sums of 8
+    neighbours); the bar (ROW_TOL) is north_star's 1e-5, as for the Frobenius ratio.  Measured
+    (round 2, all configs, P = 1..8): worst row 1.0e-6 (config 4 M^T Q)."""
     Y = np.asarray(Y, dtype=np.float64)
     num = np.linalg.norm(Y - Yref, axis=1)
     den = np.linalg.norm(Yref, axis=1)
