@@ -192,26 +192,37 @@ typedef struct {
   int64_t y, ldy;
   int32_t lr_powers;
   uint32_t y_flags;
-  int32_t basis;          /* NE: isvd_basis (0 = T).  NC: must be 0 (its basis is A_hat)  */
+  int32_t basis;          /* NE: isvd_basis (0 = T).  NC: 0 or ISVD_BASIS_AHAT_SYM (its basis is
+                             A_hat)                                                      */
   int32_t pad0;
+  /* Implicit row gather (semi-supervised option (ii): "SVD of submatrix of M without
+   * explicitly computing M nor the submatrix"): the op is M_S = M[S, :] for the n_rows sorted,
+   * distinct GLOBAL row ids in `rows` (host array, the same full list on every rank; copied).
+   * Shape (|S|, c).  The r-side (isvd_matmul output, isvd_matmul_T input, U) then has this
+   * rank's subset rows -- those of S inside its row block, in S order.  Products are
+   * M_S G = (M G)[S] and M_S^T H = M^T (H scattered to the rows S, zero elsewhere).
+   * n_rows = 0: the whole M. */
+  const int64_t* rows;
+  int64_t n_rows;
 } isvd_op_desc;
 
 /* Define an implicit matrix over graph g.  No O(nnz) work; copies w (and X
  * unless borrowed).  The op holds a reference on g. */
 isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out);
-/* Global shape (r, c) of M (SymbolicPF.shape): NE (n, n); NC (n, d (L+1) + y P). */
+/* Global shape (r, c) of M (SymbolicPF.shape): NE (n, n); NC (n, d (L+1) + y P); with a row
+ * subset S, r = |S|. */
 isvd_status isvd_op_shape(isvd_op op, int64_t* rows, int64_t* cols);
 isvd_status isvd_op_destroy(isvd_op op);
 
 /* out = M . Q   (SymbolicPF.dot; Alg. 1 lines 5/7).
  *   Q   : device, rows = this rank's share of c (NE: n_local; NC: all c, replicated), w columns.
- *   out : device, n_local x w.  Must not alias Q.
+ *   out : device, this rank's r-side rows (n_local, or its subset rows) x w.  Must not alias Q.
  * Accumulation: fp32 products summed in fp64 per row (blocks of 8 neighbours in
  * fp32, then fp64); the rank-1 term is applied in fp64 before the single
  * rounding to fp32 (reading O15).  Asynchronous on the ctx stream. */
 isvd_status isvd_matmul(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo);
 /* out = M^T . Q (SymbolicPF.T().dot; Alg. 1 lines 6/9).
- *   Q   : device, n_local x w.   out : device, NE: n_local x w; NC: c x w (replicated). */
+ *   Q   : device, this rank's r-side rows x w.   out : device, NE: n_local x w; NC: c x w (replicated). */
 isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, float* out, int64_t ldo);
 
 /* -------------------------------------------------------------------- solver */
@@ -258,7 +269,7 @@ typedef struct {
  * orthonormalisation (Alg. 2 right, applied twice) and the final
  * SVD of B = (M^T Q)^T computed as CQR2(M^T Q) = Q_W R followed
  * by a one-sided Jacobi SVD of R^T (B = R^T Q_W^T).
- *   U : n_local x k (ldu), the left singular vectors (this rank's rows).
+ *   U : r-side rows x k (ldu): this rank's rows (n_local, or its subset rows), left singular vectors.
  *   S : HOST double[k], non-increasing (reading O9).
  *   V : NE: n_local x k (this rank's rows); NC: c x k replicated (ldv).
  *   Sign rule (reading O9): each (U_j, V_j) is flipped so that the largest-

@@ -14,6 +14,7 @@ and ``tests/golden/``.  Parity status per function is listed in DESIGN.md
 from .isvd_oracle import (  # noqa: F401
     NCOperator,
     NEOperator,
+    RowSubsetOperator,
     adjacency,
     context_weights,
     embeddings,

@@ -213,6 +213,32 @@ class NCOperator:
         return np.hstack(blocks)
 
 
+class RowSubsetOperator:
+    """M_S = M[S, :] for sorted row ids S (semi-supervised option (ii): "SVD of submatrix
+    of M without explicitly computing M nor the submatrix"), by definition of the submatrix:
+    M_S G = (M G)[S] and M_S^T H = M^T H_full, H_full = H on the rows S and zero elsewhere."""
+
+    def __init__(self, op, rows):
+        self.op = op
+        self.rows = np.asarray(rows, dtype=np.int64)
+
+    @property
+    def shape(self):
+        return (self.rows.size, self.op.shape[1])
+
+    def matmul(self, G):
+        return self.op.matmul(G)[self.rows]
+
+    def matmul_T(self, H):
+        H = np.asarray(H, dtype=np.float64)
+        full = np.zeros((self.op.shape[0], H.shape[1]))
+        full[self.rows] = H
+        return self.op.matmul_T(full)
+
+    def dense(self):
+        return self.op.dense()[self.rows]
+
+
 class DenseOperator:
     """An explicit matrix behind the same product contract (leaf node)."""
 

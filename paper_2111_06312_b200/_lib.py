@@ -62,6 +62,8 @@ class OpDesc(C.Structure):
         ("y_flags", C.c_uint32),
         ("basis", C.c_int32),
         ("pad0", C.c_int32),
+        ("rows", C.POINTER(C.c_int64)),
+        ("n_rows", C.c_int64),
     ]
 
 

@@ -200,9 +200,17 @@ class SvdResult:
 
 
 class _Operator:
-    def __init__(self, graph: Graph, desc: _lib.OpDesc, keep=()):
+    def __init__(self, graph: Graph, desc: _lib.OpDesc, keep=(), rows=None):
         self.graph = graph
         self.ctx = graph.ctx
+        self._r_local = graph.n_local
+        if rows is not None:  # implicit row gather M[S, :] (option (ii))
+            S = np.ascontiguousarray(rows, dtype=np.int64)
+            desc.rows = S.ctypes.data_as(C.POINTER(C.c_int64))
+            desc.n_rows = S.size
+            keep = tuple(keep) + (S,)
+            lo, hi = graph.row_begin, graph.row_begin + graph.n_local
+            self._r_local = int(np.count_nonzero((S >= lo) & (S < hi)))
         self._keep = keep
         h = C.c_void_p()
         check(self.ctx.lib.isvd_op_define(graph.h, C.byref(desc), C.byref(h)), "isvd_op_define", self.ctx.h)
@@ -215,6 +223,10 @@ class _Operator:
     def c_rows(self) -> int:
         raise NotImplementedError
 
+    # r-side rows held by this rank (rows of M . Q, of U): n_local, or this rank's subset rows
+    def r_rows(self) -> int:
+        return self._r_local
+
     def close(self):
         if self.h:
             check(self.ctx.lib.isvd_op_destroy(self.h), "isvd_op_destroy", self.ctx.h)
@@ -226,7 +238,7 @@ class _Operator:
         Q = _as_abi(Q, dev)
         w = Q.shape[1]
         if out is None:
-            out = padded(self.graph.n_local, w, dev)
+            out = padded(self.r_rows(), w, dev)
         check(self.ctx.lib.isvd_matmul(self.h, C.c_void_p(Q.data_ptr()), w, _ld(Q), C.c_void_p(out.data_ptr()),
                                        _ld(out)), "isvd_matmul", self.ctx.h)
         return out
@@ -266,7 +278,7 @@ class _Operator:
         """Page-locked host arrays (U, V) for svd(host_output=True, out=...): the library's device-to-host copies
         run at full DMA speed and a repeated call pays no allocation."""
         kk = max(round_up(k), 4)
-        U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, pin_memory=True).numpy()
+        U = torch.zeros(max(self.r_rows(), 1), kk, dtype=torch.float32, pin_memory=True).numpy()
         V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, pin_memory=True).numpy()
         return U, V
 
@@ -281,7 +293,7 @@ class _Operator:
             flags |= _lib.ISVD_SVD_HOST_OUTPUT
             if out is not None:  # caller-owned host arrays (ideally page-locked, see host_buffers())
                 U, V = out
-                for a, rows in ((U, self.graph.n_local), (V, self.c_rows())):
+                for a, rows in ((U, self.r_rows()), (V, self.c_rows())):
                     if (not isinstance(a, np.ndarray) or a.dtype != np.float32 or a.ndim != 2
                             or a.shape[0] < rows or a.shape[1] < k or a.strides[1] != 4
                             or not a.flags.writeable):
@@ -294,7 +306,7 @@ class _Operator:
             if out is not None:
                 U, V = out
             else:
-                U = torch.zeros(max(self.graph.n_local, 1), kk, dtype=torch.float32, device=dev)
+                U = torch.zeros(max(self.r_rows(), 1), kk, dtype=torch.float32, device=dev)
                 V = torch.zeros(max(self.c_rows(), 1), kk, dtype=torch.float32, device=dev)
             pu, pv, ldu, ldv = U.data_ptr(), V.data_ptr(), U.stride(0), V.stride(0)
         if omega is not None:
@@ -310,7 +322,7 @@ class _Operator:
         check(self.ctx.lib.isvd_svd(self.h, C.byref(p), C.c_void_p(pu), ldu,
                                     S.ctypes.data_as(C.POINTER(C.c_double)), C.c_void_p(pv), ldv, C.byref(rep)),
               "isvd_svd", self.ctx.h)
-        U = U[: self.graph.n_local, :k]
+        U = U[: self.r_rows(), :k]
         V = V[: self.c_rows(), :k]
         S = S[:k]
         phases = None
@@ -324,7 +336,8 @@ class NE(_Operator):
     """M = sum_{c=1..C} w_c B^c - lambda_ones 1 1^T + lambda_adj A   (Eq. 3),
     B = T = D^-1 A (basis "T") or B = A_hat (basis "Ahat", the symmetric variant of P:158)."""
 
-    def __init__(self, graph: Graph, weights, lambda_ones: float, lambda_adj: float = 0.0, basis: str = "T"):
+    def __init__(self, graph: Graph, weights, lambda_ones: float, lambda_adj: float = 0.0, basis: str = "T",
+                 rows=None):
         w = np.ascontiguousarray(weights, dtype=np.float64)
         d = _lib.OpDesc()
         d.kind = _lib.ISVD_OP_POWER_SUM
@@ -335,7 +348,7 @@ class NE(_Operator):
         if basis not in ("T", "Ahat"):
             raise ValueError("basis must be 'T' or 'Ahat'")
         d.basis = _lib.ISVD_BASIS_T_ROW if basis == "T" else _lib.ISVD_BASIS_AHAT_SYM
-        super().__init__(graph, d, keep=(w,))
+        super().__init__(graph, d, keep=(w,), rows=rows)
 
     def c_rows(self) -> int:
         return self.graph.n_local
@@ -344,11 +357,13 @@ class NE(_Operator):
 class NC(_Operator):
     """M = [X | A_hat X | ... | A_hat^L X],  A_hat = (D+I)^-1/2 (A+I) (D+I)^-1/2   (Eq. 6).
 
+    rows (NE and NC): sorted global row ids S -> the op is M[S, :] (implicit row gather).
+
     X: this rank's rows (n_local x d), a CUDA tensor (borrowed when already in ABI layout)
     or a host numpy array (copied).  Label re-use: Y_train (this rank's n_local x y
     rows, copied) and P powers append the blocks B Y, ..., B^P Y, B = A_hat - (D+I)^-1."""
 
-    def __init__(self, graph: Graph, X, L: int, Y_train=None, P: int = 0):
+    def __init__(self, graph: Graph, X, L: int, Y_train=None, P: int = 0, rows=None):
         d = _lib.OpDesc()
         d.kind = _lib.ISVD_OP_STACKED_PROPAGATION
         d.num_terms = int(L)
@@ -381,7 +396,7 @@ class NC(_Operator):
             keep = keep + (Yt,)
             self.y, self.P = int(d.y), int(P)
         self.d, self.L = int(d.d), int(L)
-        super().__init__(graph, d, keep=keep)
+        super().__init__(graph, d, keep=keep, rows=rows)
 
     def c_rows(self) -> int:
         return self.d * (self.L + 1) + self.y * self.P

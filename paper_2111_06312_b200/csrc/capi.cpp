@@ -182,12 +182,22 @@ struct isvd_op_s {
   int64_t ylr = 0, ldylr = 0;
   int lr_powers = 0;
   float* lrbuf = nullptr;  // X G_0 + sum_p B^p Y G'_p (internal row order)
+  // implicit row gather (option (ii)): M_S = M[S, :] for sorted global rows S
+  bool has_sub = false;
+  int64_t sub_n = 0;       // |S| (global)
+  int64_t sub_local = 0;   // rows of S in this rank's block
+  int64_t sub_offset = 0;  // rows of S on lower ranks (global index of this rank's first subset row)
+  int32_t* sub_caller = nullptr;  // device: caller-order local row of subset row i
+  int32_t* sub_int = nullptr;     // device: internal (relabelled) local row of subset row i
+  std::vector<void*> sub_allocs;
+  float* sub_buf = nullptr;  // n_local x wpad: full-row product before the gather / after the scatter
   SolverWs sws;
 };
 
 // ------------------------------------------------------------------ helpers
 namespace {
 int64_t c_rows_local(const isvd_op_s* op);
+int64_t r_rows_local(const isvd_op_s* op);
 
 struct Fail {
   isvd_status st;
@@ -454,6 +464,9 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   op->lrbuf = op->lr_powers > 0
                   ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs)
                   : nullptr;
+  op->sub_buf = op->has_sub
+                    ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad, op->ws_allocs)
+                    : nullptr;
   op->ws_wpad = wpad;
 }
 
@@ -982,10 +995,35 @@ void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ld
   else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
 }
 
+// Implicit row gather (option (ii): "SVD of submatrix of M without explicitly
+// computing M nor the submatrix"): M_S G = (M G)[S] and M_S^T H = M^T (scatter_S H), with the
+// full-row product / scattered operand in sub_buf (zero outside S).  `caller_order`: the r-side
+// rows of out / H are in the caller's order (API calls) or the solver's internal order.
+void r_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool caller_order) {
+  if (!op->has_sub) return op_matmul(op, Q, ldq, out, ldo, wpad, caller_order);
+  isvd_ctx ctx = op->g->ctx;
+  ensure_op_ws(op, wpad);
+  op_matmul(op, Q, ldq, op->sub_buf, wpad, wpad, caller_order);
+  CK(launch_scale_rows(op->sub_buf, wpad, out, ldo, op->sub_local, wpad, nullptr, 1.f, nullptr, ctx->stream,
+                       caller_order ? op->sub_caller : op->sub_int));
+}
+void r_matmul_T(isvd_op op, const float* H, int64_t ldh, float* out, int64_t ldo, int64_t wpad, bool caller_order) {
+  if (!op->has_sub) return op_matmul_T(op, H, ldh, out, ldo, wpad, caller_order);
+  isvd_ctx ctx = op->g->ctx;
+  ensure_op_ws(op, wpad);
+  CK(cudaMemsetAsync(op->sub_buf, 0, sizeof(float) * (size_t)std::max<int64_t>(op->g->n_local, 1) * wpad, ctx->stream));
+  CK(launch_scatter_rows(H, ldh, op->sub_buf, wpad, op->sub_local, wpad, caller_order ? op->sub_caller : op->sub_int,
+                         ctx->stream));
+  op_matmul_T(op, op->sub_buf, wpad, out, ldo, wpad, caller_order);
+}
+
 void op_shape(const isvd_op_s* op, int64_t* r, int64_t* c) {
-  *r = op->g->n;
+  *r = op->has_sub ? op->sub_n : op->g->n;
   *c = op->kind == ISVD_OP_POWER_SUM ? op->g->n : op->d * (op->terms + 1) + op->ylr * op->lr_powers;
 }
+
+// rows of the r-side (rows of M) held by this rank
+int64_t r_rows_local(const isvd_op_s* op) { return op->has_sub ? op->sub_local : op->g->n_local; }
 
 // rows of the c-side (columns of M) held by this rank
 int64_t c_rows_local(const isvd_op_s* op) {
@@ -1473,8 +1511,42 @@ isvd_status isvd_op_define(isvd_graph g, const isvd_op_desc* desc, isvd_op* out)
     } else {
       REQ(false, ISVD_ERR_INVALID_ARG, "unknown op kind");
     }
+    // implicit row gather (option (ii)): M_S = M[S, :], S sorted global row ids
+    REQ(desc->n_rows >= 0 && (desc->n_rows == 0 || desc->rows != nullptr), ISVD_ERR_INVALID_ARG,
+        "rows is null while n_rows > 0");
+    if (desc->n_rows > 0) {
+      const int64_t* S = desc->rows;
+      for (int64_t i = 0; i < desc->n_rows; ++i) {
+        REQ(S[i] >= 0 && S[i] < g->n, ISVD_ERR_INDEX, "row subset entry outside [0, n)");
+        REQ(i == 0 || S[i] > S[i - 1], ISVD_ERR_INVALID_ARG, "row subset must be strictly increasing");
+      }
+      const int64_t* lo = std::lower_bound(S, S + desc->n_rows, g->row_begin);
+      const int64_t* hi = std::lower_bound(S, S + desc->n_rows, g->row_begin + g->n_local);
+      op->has_sub = true;
+      op->sub_n = desc->n_rows;
+      op->sub_offset = lo - S;
+      op->sub_local = hi - lo;
+      std::vector<int32_t> loc(std::max<int64_t>(op->sub_local, 1), 0);
+      for (int64_t i = 0; i < op->sub_local; ++i) loc[i] = (int32_t)(lo[i] - g->row_begin);
+      op->sub_caller = (int32_t*)dmalloc(ctx, sizeof(int32_t) * loc.size(), op->sub_allocs);
+      CK(cudaMemcpyAsync(op->sub_caller, loc.data(), sizeof(int32_t) * loc.size(), cudaMemcpyHostToDevice,
+                         ctx->stream));
+      if (g->new2old) {  // internal row of each subset row: (new2old)^-1 composed with the caller rows
+        op->sub_int = (int32_t*)dmalloc(ctx, sizeof(int32_t) * loc.size(), op->sub_allocs);
+        std::vector<void*> tmp;
+        int32_t* inv = (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(g->n_local, 1), tmp);
+        CK(launch_compose_inverse(g->new2old, g->n_local, op->sub_caller, op->sub_local, inv, op->sub_int,
+                                  ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        for (void* q : tmp) dfree(ctx, q);
+      } else {
+        op->sub_int = op->sub_caller;
+      }
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
   });
   if (st != ISVD_OK) {  // give back whatever the op had already taken
+    for (void* q : op->sub_allocs) dfree(ctx, q);
     if (op->own_x) dfree(ctx, (void*)op->X);
     dfree(ctx, op->Xrs);
     dfree(ctx, (void*)op->Ylr);
@@ -1509,6 +1581,7 @@ isvd_status isvd_op_destroy(isvd_op op) {
   if (op->own_x) dfree(op->g->ctx, (void*)op->X);
   if (op->Xrs) dfree(op->g->ctx, op->Xrs);
   if (op->Ylr) dfree(op->g->ctx, (void*)op->Ylr);
+  for (void* q : op->sub_allocs) dfree(op->g->ctx, q);
   op->g->refs--;
   delete op;
   return ISVD_OK;
@@ -1534,7 +1607,7 @@ isvd_status isvd_matmul(isvd_op op, const float* Q, int64_t w, int64_t ldq, floa
   if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    op_matmul(op, Q, ldq, out, ldo, round_up(w, 4), true);
+    r_matmul(op, Q, ldq, out, ldo, round_up(w, 4), true);
   });
 }
 
@@ -1547,7 +1620,7 @@ isvd_status isvd_matmul_T(isvd_op op, const float* Q, int64_t w, int64_t ldq, fl
   if (Q == out) { set_err(ctx, "out must not alias Q"); return ISVD_ERR_INVALID_ARG; }
   return guarded(ctx, [&] {
     DeviceGuard dg(ctx->device);
-    op_matmul_T(op, Q, ldq, out, ldo, round_up(w, 4), true);
+    r_matmul_T(op, Q, ldq, out, ldo, round_up(w, 4), true);
   });
 }
 
@@ -1585,7 +1658,7 @@ void ensure_solver_ws(isvd_op op, int64_t l, int64_t k) {
   CK(cudaStreamSynchronize(ctx->stream));
   free_solver_ws(ctx, s);
   const int64_t ld = round_up(l, 4), ldk = round_up(k, 4);
-  const int64_t rr = std::max<int64_t>(op->g->n_local, 1), cr = std::max<int64_t>(c_rows_local(op), 1);
+  const int64_t rr = std::max<int64_t>(r_rows_local(op), 1), cr = std::max<int64_t>(c_rows_local(op), 1);
   auto f = [&](int64_t n) { return (float*)dmalloc(ctx, sizeof(float) * n, s.allocs); };
   auto d = [&](int64_t n) { return (double*)dmalloc(ctx, sizeof(double) * n, s.allocs); };
   s.Qc = f(cr * ld);
@@ -1827,7 +1900,9 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   const int64_t k = p->k;
   const int64_t ld = round_up(l, 4), ldk = round_up(k, 4);
   const bool ne = op->kind == ISVD_OP_POWER_SUM;
-  const int64_t cr = c_rows_local(op), rr = g->n_local;
+  const int64_t cr = c_rows_local(op), rr = r_rows_local(op);
+  int64_t r_glob, c_glob;
+  op_shape(op, &r_glob, &c_glob);
   const bool force = p->flags & ISVD_SVD_FORCE_CHOL_FAIL;
   CK(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
   // Alg. 1 line 4: Q ~ N(0,1)^{c x l}
@@ -1843,7 +1918,7 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   }
   // r-side orthonormalisation: with a small c side (NC) the second CholeskyQR update is folded
   // into the small products (cqr2_deferred); otherwise the plain CholeskyQR2
-  const bool fold = !ne && 4 * cr <= g->n;  // NC: c = d (L + 1) rows, replicated on every rank
+  const bool fold = !ne && 4 * cr <= r_glob;  // NC: c = d (L + 1) rows, replicated on every rank
   float* q_r = s.Yr;  // buffer holding the r-side orthonormal factor (times Rfold when folding)
   auto orth_r = [&](bool exact) {
     Phase ph(ctx, kPhOrth);
@@ -1857,23 +1932,23 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
   // W = M^T Q into Qc (Q = q_r Rfold when folding)
   auto mt_q = [&]() {
     if (fold) {
-      op_matmul_T(op, q_r, ld, s.Qc2, ld, ld, false);
+      r_matmul_T(op, q_r, ld, s.Qc2, ld, ld, false);
       Phase ph(ctx, kPhProducts);
       gemm_fp32(op, s.Qc2, ld, s.Rfold, ld, s.Qc, ld, cr, ld, l, nullptr, false, nullptr);
     } else {
-      op_matmul_T(op, q_r, ld, s.Qc, ld, ld, false);
+      r_matmul_T(op, q_r, ld, s.Qc, ld, ld, false);
     }
   };
   // Alg. 1 lines 5-8
   for (int it = 0; it < p->power_iters; ++it) {
-    op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);            // M Q       (r x l)
+    r_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);             // M Q       (r x l)
     orth_r(it == 0);                                         // orthonorm
     mt_q();                                                  // M^T Q     (c x l)
     Phase ph(ctx, kPhOrth);
     cqr2(op, s.Qc, s.Qc2, cr, ne, l, force, nullptr, true);  // orthonorm
   }
   // Alg. 1 line 9: Q <- orthonorm(M Q)
-  op_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);
+  r_matmul(op, s.Qc, ld, s.Yr, ld, ld, false);
   orth_r(p->power_iters == 0);
   // Alg. 1 line 10: B = (M^T Q)^T, taken as W = M^T Q = Q_W R  (CQR2 keeps R)
   mt_q();
@@ -1892,10 +1967,12 @@ void solver_body(isvd_op op, const isvd_svd_params* p, int64_t l, float* U, int6
     gemm_fp32(op, s.Rfold, ld, s.Ub, ldk, s.Ub2, ldk, l, ldk, l, nullptr, false, nullptr);
     ub = s.Ub2;
   }
-  gemm_fp32(op, q_r, ld, ub, ldk, U, ldu, rr, ldk, l, nullptr, false, nullptr, g->new2old);
+  // (a row subset's r-side rows are already in subset order)
+  gemm_fp32(op, q_r, ld, ub, ldk, U, ldu, rr, ldk, l, nullptr, false, nullptr, op->has_sub ? nullptr : g->new2old);
   gemm_fp32(op, s.Qc, ld, s.Vb, ldk, V, ldv, cr, ldk, l, nullptr, false, nullptr, ne ? g->new2old : nullptr);
   // sign rule (reading O9)
-  CK(launch_col_absmax(U, ldu, rr, (int)k, g->row_begin, s.absmax_ws, s.cand, ctx->stream));
+  CK(launch_col_absmax(U, ldu, rr, (int)k, op->has_sub ? op->sub_offset : g->row_begin, s.absmax_ws, s.cand,
+                       ctx->stream));
   const double* cand = s.cand;
   if (ctx->dist) {
     allgather_f64(ctx, s.cand, s.cand_all, 3 * k);
@@ -2006,7 +2083,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
       solver_body(op, p, l, Ud, lduu, Vd, ldvv);
       launches = g_launches - l0;
     }
-    const int64_t rr = op->g->n_local, cr = c_rows_local(op);
+    const int64_t rr = r_rows_local(op), cr = c_rows_local(op);
     if (staged && !host_out) {  // the op's U / V buffers -> the caller's device outputs
       if (rr > 0)
         CK(cudaMemcpy2DAsync(U, ldu * sizeof(float), Ud, lduu * sizeof(float), ldk * sizeof(float), rr,

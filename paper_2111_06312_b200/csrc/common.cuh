@@ -70,6 +70,12 @@ cudaError_t launch_colsum(const float* Q, int64_t rows, int64_t wpad, int64_t ld
 cudaError_t launch_scale_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows,
                               int64_t wpad, const float* vec, float coef, const int* gate, cudaStream_t st,
                               const int32_t* in_map = nullptr);
+// out[out_map[i], :] = in[i, :] for i < rows, columns < wpad (other rows of out untouched).
+cudaError_t launch_scatter_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
+                               const int32_t* out_map, cudaStream_t st);
+// out[i] = inv[idx[i]] (i < m) with inv the inverse of the permutation perm of [0, n) (inv_ws: n ints).
+cudaError_t launch_compose_inverse(const int32_t* perm, int64_t n, const int32_t* idx, int64_t m, int32_t* inv_ws,
+                                   int32_t* out, cudaStream_t st);
 // out[i, j] = in[i, j] * colvec[j]  (i < rows, j < wpad, wpad % 4 == 0; out may equal in)
 cudaError_t launch_scale_cols(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
                               const float* colvec, cudaStream_t st);

@@ -487,6 +487,27 @@ __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, flo
   }
 }
 
+// out[out_map[i], :] = in[i, :]  (rows of `out` not in the map are left as they are)
+__global__ void scatter_rows_kernel(const float* __restrict__ in, int64_t ldi, float* __restrict__ out, int64_t ldo,
+                                    int64_t rows, int64_t w4, const int32_t* __restrict__ out_map) {
+  const int64_t tot = rows * w4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
+    *reinterpret_cast<float4*>(out + (int64_t)out_map[i] * ldo + c) = *reinterpret_cast<const float4*>(in + i * ldi + c);
+  }
+}
+
+// inv[perm[t]] = t, then out[i] = inv[idx[i]]  (perm: a permutation of [0, n))
+__global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ inv) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[t]] = (int32_t)t;
+}
+__global__ void gather_idx_kernel(const int32_t* __restrict__ table, const int32_t* __restrict__ idx, int64_t m,
+                                  int32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = table[idx[t]];
+}
+
 __global__ void scale_cols_kernel(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t w4,
                                   const float* __restrict__ colvec) {
   const int64_t tot = rows * w4;
@@ -881,6 +902,28 @@ cudaError_t launch_scale_cols(const float* in, int64_t ldi, float* out, int64_t 
   ++g_launches;
   scale_cols_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4,
                                                                                colvec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const float* in, int64_t ldi, float* out, int64_t ldo, int64_t rows, int64_t wpad,
+                               const int32_t* out_map, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  ++g_launches;
+  scatter_rows_kernel<<<grid_for(rows * (wpad / 4), 256, 148 * 16), 256, 0, st>>>(in, ldi, out, ldo, rows, wpad / 4,
+                                                                                 out_map);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compose_inverse(const int32_t* perm, int64_t n, const int32_t* idx, int64_t m, int32_t* inv_ws,
+                                   int32_t* out, cudaStream_t st) {
+  if (n > 0) {
+    ++g_launches;
+    invert_perm_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, st>>>(perm, n, inv_ws);
+  }
+  if (m > 0) {
+    ++g_launches;
+    gather_idx_kernel<<<grid_for(m, 256, 148 * 8), 256, 0, st>>>(inv_ws, idx, m, out);
+  }
   return cudaGetLastError();
 }
 

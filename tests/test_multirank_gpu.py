@@ -228,3 +228,41 @@ def test_multirank_least_norm_allreduce():
     for o in outs:
         assert rel_fro(o["W"], Wref) <= 1e-5
         assert np.array_equal(o["W"], outs[0]["W"])
+
+
+@pytest.mark.parametrize("where", ["spread", "first_block"])
+def test_multirank_row_subset(where):
+    """Implicit row gather on P = 3 simulated ranks: S spread over every rank, or S
+    inside rank 0's block only (ranks 1 and 2 hold ZERO r-side rows: empty Grams, empty GEMMs,
+    empty sign-rule candidates).  Against the oracle's RowSubsetOperator."""
+    from oracle import RowSubsetOperator, isvd, philox_omega
+
+    import paper_2111_06312_b200 as isvd_mod
+
+    cfg, g, X, sp = _ragged("NC")
+    rng = np.random.default_rng(5)
+    if where == "spread":
+        S = np.sort(rng.choice(g.n, 300, replace=False)).astype(np.int64)
+    else:
+        S = np.sort(rng.choice(300, 120, replace=False)).astype(np.int64)  # rank 0 owns rows < 334
+    ref = RowSubsetOperator(oracle_op(cfg, g, X, sp), S)
+
+    def fn(rank, ctx):
+        rb, nl = isvd_mod.partition(g.n, ctx.world, ctx.rank)
+        rp, ci = g.row_slice(rb, rb + nl)
+        graph = isvd_mod.Graph(ctx, g.n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+        op = isvd_mod.NC(graph, torch.from_numpy(np.ascontiguousarray(X[rb : rb + nl])).cuda(), sp["L"], rows=S)
+        res = op.svd(sp["k"], -1, sp["q"], sp["seed"])
+        o = dict(U=res.U.cpu().numpy(), S=res.S.copy(), V=res.V.cpu().numpy(), r=op.r_rows())
+        op.close()
+        graph.close()
+        return o
+
+    outs = run_ranks(3, fn)
+    assert sum(o["r"] for o in outs) == S.size
+    U = np.concatenate([o["U"] for o in outs]).astype(np.float64)
+    om = philox_omega(sp["seed"], 0, ref.shape[1], sp["l"])
+    print(check_isvd_arrays(U, outs[0]["S"], outs[0]["V"].astype(np.float64), isvd(ref, sp["k"], om, sp["q"]),
+                            sp["k"], f"subset {where} P=3"))
+    for o in outs:
+        assert np.array_equal(o["S"], outs[0]["S"]) and np.array_equal(o["V"], outs[0]["V"])

@@ -649,3 +649,29 @@ def test_ne_ahat_basis_complete_graph_is_zero():
     for n in range(4, 10):
         op = NEOperator(_complete(n), context_weights(4), 1.0 / n, basis="Ahat")
         assert np.abs(op.dense()).max() < 1e-15
+
+
+# --------------------------------------------- implicit row gather (option (ii))
+
+
+def test_row_subset_operator_is_the_submatrix_and_its_svd():
+    """M_S = M[S, :] by definition: implicit products equal the explicit rows of dense(M) (both
+    families, both directions), and Alg. 1 with l >= rank(M_S) returns the exact SVD of M[S]
+     -- checked against LAPACK on the explicit submatrix."""
+    from oracle import RowSubsetOperator
+
+    rng = np.random.default_rng(17)
+    A = _random_connected(30, 25, rng)
+    X = rng.standard_normal((30, 3))
+    S = np.sort(rng.choice(30, 11, replace=False))
+    for op in (NEOperator(A, uniform_weights(4), 1 / 30), NCOperator(A, X, 2)):
+        sub = RowSubsetOperator(op, S)
+        Md = op.dense()[S]
+        G = rng.standard_normal((op.shape[1], 5))
+        H = rng.standard_normal((S.size, 5))
+        assert sub.shape == Md.shape
+        assert np.allclose(sub.matmul(G), Md @ G, rtol=0, atol=1e-13)
+        assert np.allclose(sub.matmul_T(H), Md.T @ H, rtol=0, atol=1e-13)
+        r = min(Md.shape)
+        _, s, _, _ = isvd(sub, min(5, r), philox_omega(9, 0, Md.shape[1], r), iterations=1)
+        assert np.allclose(s, np.linalg.svd(Md, compute_uv=False)[: min(5, r)], rtol=1e-10, atol=1e-13)

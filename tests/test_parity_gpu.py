@@ -693,3 +693,46 @@ def test_spectral_kernel_on_a_gpu_spectrum(ctx):
     S = res.S / res.S[0] * 1.9  # spread the spectrum over Eq. 9's (0, 2] range
     for mu, sb in ((1.0, 0.0), (1.5, 3.0), (0.7, -2.0)):
         assert np.allclose(isvd_mod.spectral_kernel(S, mu, sb), o_sk(S, mu, sb), rtol=1e-12, atol=0)
+
+
+# --------------------------------------------- implicit row gather (option (ii))
+
+
+@pytest.mark.parametrize("i", [0, 2, 4])
+def test_row_subset_operator(ctx, i):
+    """M_S = M[S, :] for a 30 % labelled-node subset S (P:209-210 option (ii)) without forming M or
+    the submatrix: products (caller order, every row / column) against the oracle's
+    RowSubsetOperator and, for configs 0 and 2, the isvd (Alg. 1 of M_S).  Config 4 (relabelled
+    graph): the subset rows go through the relabelling maps; products on 8 columns."""
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import RowSubsetOperator, isvd, philox_omega
+
+    cfg, g, X, sp = config_inputs(i)
+    rng = np.random.default_rng(600 + i)
+    S = np.sort(rng.choice(g.n, int(0.3 * g.n), replace=False)).astype(np.int64)
+    graph = isvd_mod.Graph(ctx, g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda())
+    if cfg["op"] == "NE":
+        op = isvd_mod.NE(graph, sp["weights"], sp["lambda_ones"], rows=S)
+    else:
+        op = isvd_mod.NC(graph, torch.from_numpy(np.ascontiguousarray(X)).cuda(), sp["L"], rows=S)
+    ref = RowSubsetOperator(oracle_op(cfg, g, X, sp), S)
+    assert op.shape == ref.shape and op.r_rows() == S.size
+    w = 8 if i == 4 else sp["l"]
+    G = rng.standard_normal((op.shape[1], w)).astype(np.float32)
+    H = rng.standard_normal((S.size, w)).astype(np.float32)
+    if i == 4:
+        Yref, _ = _col_parallel(ref.matmul, G, np.arange(w))
+        Wref, _ = _col_parallel(ref.matmul_T, H, np.arange(w))
+    else:
+        Yref, Wref = ref.matmul(G.astype(np.float64)), ref.matmul_T(H.astype(np.float64))
+    print(assert_product(_to_np(op.matmul(torch.from_numpy(G).cuda())), Yref, f"cfg{i} subset M_S.G"))
+    print(assert_product(_to_np(op.matmul_T(torch.from_numpy(H).cuda())), Wref, f"cfg{i} subset M_S^T.H"))
+    if i != 4:
+        p = -1 if cfg["p"] is None else cfg["p"]
+        l = min(sp["l"], *op.shape)
+        res = op.svd(sp["k"], p, sp["q"], sp["seed"])
+        om = philox_omega(sp["seed"], 0, op.shape[1], res.l)
+        print(_check_isvd(res, isvd(ref, sp["k"], om, sp["q"]), sp["k"], f"cfg{i} subset"))
+        assert res.l == l
+    op.close()
+    graph.close()
