@@ -100,6 +100,9 @@ struct isvd_ctx_s {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_join = nullptr;
   cudaStream_t work = nullptr;  // private non-blocking stream the solver runs (and is captured) on
   cudaStream_t side = nullptr;  // second private stream: NC dense terms overlapped with the SpMM chain
+  cudaStream_t cstream = nullptr;  // collectives stream: all-gathers in flight during the local SpMM pass
+  cudaEvent_t ev_fork = nullptr, ev_gath = nullptr;
+  bool gather_pending = false;     // an all-gather on cstream the next remote pass must wait for
   std::vector<cudaEvent_t> ov_ev;  // fork/join events of the overlap (reused in order)
   size_t max_persist_l2 = 0;    // cudaDevAttrMaxPersistingL2CacheSize
   std::atomic<int> live_graphs{0};
@@ -126,6 +129,13 @@ struct isvd_graph_s {
   int64_t* row_ptr = nullptr;  // device, rebased to 0
   int32_t* col_idx = nullptr;  // device
   float* val = nullptr;        // device edge weights (null: unweighted)
+  // distributed local / remote split (world > 1): own-row columns and the rest, same row order
+  bool split = false;
+  int64_t nnz_loc = 0;
+  int64_t *rp_loc = nullptr, *rp_rem = nullptr;
+  int32_t *ci_loc = nullptr, *ci_rem = nullptr;
+  float *val_loc = nullptr, *val_rem = nullptr;
+  SpmmPlan plan_loc, plan_rem;
   float* inv_deg = nullptr;    // 1/d (0 for d = 0)
   float* s = nullptr;          // (d+1)^-1/2
   float* s2 = nullptr;         // (d+1)^-1
@@ -177,6 +187,7 @@ struct isvd_op_s {
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
   float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
   float* adjbuf = nullptr;  // NE with lambda_adj != 0: lambda_adj A Q (internal row order)
+  float* loc_partial = nullptr;  // distributed split: local-pass row sums (n_local x wpad fp32)
   // NC label re-use: Y_train (internal row order, owned), width, ld, powers
   const float* Ylr = nullptr;
   int64_t ylr = 0, ldylr = 0;
@@ -377,8 +388,38 @@ void coll_allgather(isvd_ctx ctx, void* recv, size_t bytes_per_rank) {
     if (q != me) CK(cudaStreamWaitEvent(ctx->stream, g->done[q], 0));  // peers finished reading my buffer
 }
 
+// The stream the next consumer of an in-flight all-gather must wait on it (remote SpMM pass,
+// end of every product).
+void join_gather(isvd_ctx ctx) {
+  if (!ctx->gather_pending) return;
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_gath, 0));
+  ctx->gather_pending = false;
+}
+
+// All-gather of a full-height SpMM gather source (every rank's slice).  With the local / remote
+// split it runs on the collectives stream: the next SpMM step's local pass (own rows only) runs
+// meanwhile and its remote pass waits (join_gather).
 void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld) {
-  coll_allgather(ctx, full, sizeof(float) * (size_t)g->n_pad * ld);
+  const size_t bytes = sizeof(float) * (size_t)g->n_pad * ld;
+  if (!ctx->dist) return;
+  if (!g->split) {
+    coll_allgather(ctx, full, bytes);
+    return;
+  }
+  join_gather(ctx);  // one all-gather in flight at a time
+  CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_fork, 0));
+  cudaStream_t main = ctx->stream;
+  ctx->stream = ctx->cstream;
+  try {
+    coll_allgather(ctx, full, bytes);
+  } catch (...) {
+    ctx->stream = main;
+    throw;
+  }
+  ctx->stream = main;
+  CK(cudaEventRecord(ctx->ev_gath, ctx->cstream));
+  ctx->gather_pending = true;
 }
 
 void allreduce_f64(isvd_ctx ctx, double* buf, size_t count) {
@@ -441,7 +482,13 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
   const int64_t nptmp = op->kind == ISVD_OP_STACKED_PROPAGATION ? std::max(op->terms, 1) : 1;
   op->ptmp = (float*)dmalloc(ctx, sizeof(float) * (size_t)nptmp * std::max<int64_t>(g->n_local, 1) * wpad,
                              op->ws_allocs);
-  op->partial = (float*)dmalloc(ctx, sizeof(float) * (size_t)spmm_ws_floats(g->plan, wpad), op->ws_allocs);
+  op->partial = (float*)dmalloc(
+      ctx, sizeof(float) * (size_t)std::max({spmm_ws_floats(g->plan, wpad), spmm_ws_floats(g->plan_loc, wpad),
+                                             spmm_ws_floats(g->plan_rem, wpad)}),
+      op->ws_allocs);
+  op->loc_partial = g->split ? (float*)dmalloc(ctx, sizeof(float) * (size_t)std::max<int64_t>(g->n_local, 1) * wpad,
+                                               op->ws_allocs)
+                             : nullptr;
   op->colsum = (double*)dmalloc(ctx, sizeof(double) * wpad, op->ws_allocs);
   op->colsum_ws = (double*)dmalloc(ctx, sizeof(double) * colsum_ws_doubles(g->n_local, wpad), op->ws_allocs);
   int64_t ka = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : wpad;
@@ -558,7 +605,23 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
   if (persist_env && g->new2old) persist = std::min(persist, (size_t)atoll(persist_env) << 20);
   static const char* cols_env = getenv("ISVD_SPMM_COLS");  // tuning override: column block width
   const int64_t col_block = cols_env ? atoll(cols_env) : 0;
-  CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist, col_block));
+  if (g->split && ctx->dist) {
+    // local pass (columns of this rank's own rows: available before the all-gather completes)
+    // -> raw fp32 row sums; remote pass after the all-gather, adding them in its epilogue
+    SpmmArgs lo = a;
+    lo.col_idx = g->ci_loc; lo.val = g->val_loc;
+    lo.self_coef = 0.f; lo.post_vec = nullptr; lo.post_coef = 1.f; lo.T = nullptr; lo.term_vec = nullptr;
+    lo.colsum = nullptr; lo.out = op->loc_partial; lo.ldo = a.wpad; lo.out_map = nullptr; lo.pre = nullptr;
+    CK(launch_spmm(g->plan_loc, lo, op->partial, ctx->num_sms, ctx->stream, 0, col_block));
+    join_gather(ctx);
+    SpmmArgs re = a;
+    re.col_idx = g->ci_rem; re.val = g->val_rem;
+    re.pre = op->loc_partial; re.ldpre = a.wpad;
+    CK(launch_spmm(g->plan_rem, re, op->partial, ctx->num_sms, ctx->stream, 0, col_block));
+  } else {
+    join_gather(ctx);
+    CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist, col_block));
+  }
   if (e1) CK(cudaEventRecord(e1, ctx->stream));
   // algorithmic bytes of the step: CSR, scale vectors, the gather source read
   // once (all n rows), the epilogue operand T, the output
@@ -984,6 +1047,7 @@ void op_matmul(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo,
   if (op->kind == ISVD_OP_POWER_SUM && op->ahat_basis) ne_ahat_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else if (op->kind == ISVD_OP_POWER_SUM) ne_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else nc_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  join_gather(ctx);
 }
 
 void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ldo, int64_t wpad, bool user_order) {
@@ -993,6 +1057,7 @@ void op_matmul_T(isvd_op op, const float* Q, int64_t ldq, float* out, int64_t ld
   if (op->kind == ISVD_OP_POWER_SUM && op->ahat_basis) ne_ahat_matmul(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else if (op->kind == ISVD_OP_POWER_SUM) ne_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
   else nc_matmul_T(ctx, op, Q, ldq, out, ldo, wpad, user_order);
+  join_gather(ctx);
 }
 
 // Implicit row gather (option (ii): "SVD of submatrix of M without explicitly
@@ -1115,6 +1180,9 @@ void ctx_init(isvd_ctx ctx, int device, void* stream, const isvd_allocator* allo
   CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&ctx->work, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_gath, cudaEventDisableTiming));
   ctx->ov_ev.resize(16);
   for (auto& e : ctx->ov_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   int persist = 0;
@@ -1222,6 +1290,12 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
     cudaStreamSynchronize(ctx->side);
     cudaStreamDestroy(ctx->side);
   }
+  if (ctx->cstream) {
+    cudaStreamSynchronize(ctx->cstream);
+    cudaStreamDestroy(ctx->cstream);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_gath) cudaEventDestroy(ctx->ev_gath);
   for (cudaEvent_t e : ctx->ov_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
   delete ctx;
@@ -1229,6 +1303,45 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
 }
 
 // ===================================================================== graph
+namespace {
+// SpMM segment plan of the CSR row_ptr `rp` (device) into p (device arrays owned by `allocs`).
+void build_plan(isvd_ctx ctx, const int64_t* rp, int64_t n_local, SpmmPlan& p, std::vector<void*>& allocs, void* temp,
+                size_t temp_bytes) {
+  std::vector<void*> tmp;
+  struct TmpFree {
+    std::vector<void*>& v;
+    isvd_ctx c;
+    ~TmpFree() { for (void* q : v) dfree(c, q); }
+  } tmp_free{tmp, ctx};
+  int64_t* nseg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+  int64_t* seg_off = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+  int32_t* cnt32 = (int32_t*)dmalloc(ctx, sizeof(int32_t) * 4 * (n_local + 1), tmp);
+  int32_t *nsplit = cnt32, *nslot = cnt32 + (n_local + 1), *split_off = cnt32 + 2 * (n_local + 1),
+          *slot_off = cnt32 + 3 * (n_local + 1);
+  CK(launch_plan_count(rp, n_local, nseg, nsplit, nslot, seg_off, split_off, slot_off, temp, temp_bytes, ctx->stream));
+  int64_t tot_seg = 0;
+  int32_t tot_split = 0, tot_slot = 0;
+  CK(cudaMemcpyAsync(&tot_seg, seg_off + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&tot_split, split_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(&tot_slot, slot_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  p.n_local = n_local;
+  p.n_seg = tot_seg;
+  p.n_split_rows = tot_split;
+  p.n_slots = tot_slot;
+  auto d32 = [&](int64_t n) { return (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(n, 1), allocs); };
+  p.seg_row = d32(tot_seg);
+  p.seg_len = d32(tot_seg);
+  p.seg_slot = d32(tot_seg);
+  p.split_row = d32(tot_split);
+  p.split_slot0 = d32(tot_split);
+  p.split_nslot = d32(tot_split);
+  p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<int64_t>(tot_seg, 1), allocs);
+  CK(launch_plan_fill(rp, n_local, seg_off, split_off, slot_off, p, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+}  // namespace
+
 isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin, int64_t n_local,
                               const int64_t* row_ptr, const int32_t* col_idx, const float* values, uint32_t flags,
                               isvd_graph* out) {
@@ -1355,34 +1468,36 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     phase("scales");
     // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
     // split, their partial sums combined by the fixup pass in segment order (graph_build.cu)
-    int64_t* nseg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
-    int64_t* seg_off = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
-    int32_t* cnt32 = (int32_t*)dmalloc(ctx, sizeof(int32_t) * 4 * (n_local + 1), tmp);
-    int32_t *nsplit = cnt32, *nslot = cnt32 + (n_local + 1), *split_off = cnt32 + 2 * (n_local + 1),
-            *slot_off = cnt32 + 3 * (n_local + 1);
-    CK(launch_plan_count(g->row_ptr, n_local, nseg, nsplit, nslot, seg_off, split_off, slot_off, temp, temp_bytes,
-                         ctx->stream));
-    int64_t tot_seg = 0;
-    int32_t tot_split = 0, tot_slot = 0;
-    CK(cudaMemcpyAsync(&tot_seg, seg_off + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&tot_split, split_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&tot_slot, slot_off + n_local, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    SpmmPlan& p = g->plan;
-    p.n_local = n_local;
-    p.n_seg = tot_seg;
-    p.n_split_rows = tot_split;
-    p.n_slots = tot_slot;
-    auto d32 = [&](int64_t n) { return (int32_t*)dmalloc(ctx, sizeof(int32_t) * std::max<int64_t>(n, 1), g->allocs); };
-    p.seg_row = d32(tot_seg);
-    p.seg_len = d32(tot_seg);
-    p.seg_slot = d32(tot_seg);
-    p.split_row = d32(tot_split);
-    p.split_slot0 = d32(tot_split);
-    p.split_nslot = d32(tot_split);
-    p.seg_beg = (int64_t*)dmalloc(ctx, sizeof(int64_t) * std::max<int64_t>(tot_seg, 1), g->allocs);
-    CK(launch_plan_fill(g->row_ptr, n_local, seg_off, split_off, slot_off, p, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    build_plan(ctx, g->row_ptr, n_local, g->plan, g->allocs, temp, temp_bytes);
+    // distributed (world > 1): the local / remote split of every row's edges, so the local part
+    // of each SpMM step runs while the all-gather of the gather source is in flight (SURVEY 8(e)
+    // overlap item 1); ISVD_DIST_SPLIT=0 keeps the single pass after a blocking all-gather
+    static const bool no_split = getenv("ISVD_DIST_SPLIT") && getenv("ISVD_DIST_SPLIT")[0] == '0';
+    if (ctx->dist && ctx->world > 1 && !no_split && n_local > 0) {
+      int64_t* cl = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+      int64_t* cr = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), tmp);
+      g->rp_loc = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
+      g->rp_rem = (int64_t*)dmalloc(ctx, sizeof(int64_t) * (n_local + 1), g->allocs);
+      CK(launch_split_count(g->row_ptr, g->col_idx, n_local, row_begin, row_begin + n_local, cl, cr, ctx->stream));
+      CK(launch_exclusive_scan64(cl, g->rp_loc, n_local + 1, temp, temp_bytes, ctx->stream));
+      CK(launch_exclusive_scan64(cr, g->rp_rem, n_local + 1, temp, temp_bytes, ctx->stream));
+      int64_t nl_e = 0, nr_e = 0;
+      CK(cudaMemcpyAsync(&nl_e, g->rp_loc + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaMemcpyAsync(&nr_e, g->rp_rem + n_local, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      g->nnz_loc = nl_e;
+      g->ci_loc = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nl_e + kIdxPad), g->allocs);
+      g->ci_rem = (int32_t*)dmalloc(ctx, sizeof(int32_t) * (nr_e + kIdxPad), g->allocs);
+      if (g->val) {
+        g->val_loc = (float*)dmalloc(ctx, sizeof(float) * (nl_e + kIdxPad), g->allocs);
+        g->val_rem = (float*)dmalloc(ctx, sizeof(float) * (nr_e + kIdxPad), g->allocs);
+      }
+      CK(launch_split_fill(g->row_ptr, g->col_idx, g->val, n_local, row_begin, row_begin + n_local, g->rp_loc,
+                           g->rp_rem, g->ci_loc, g->val_loc, g->ci_rem, g->val_rem, ctx->stream));
+      build_plan(ctx, g->rp_loc, n_local, g->plan_loc, g->allocs, temp, temp_bytes);
+      build_plan(ctx, g->rp_rem, n_local, g->plan_rem, g->allocs, temp, temp_bytes);
+      g->split = true;
+    }
     phase("plan");
   });
   if (st != ISVD_OK) {

@@ -118,6 +118,7 @@ struct SpmmArgs {
   float* out; int64_t ldo;
   const int32_t* out_map;  // nullable
   int64_t wpad;            // columns processed (multiple of 4)
+  const float* pre; int64_t ldpre;  // nullable: fp32 partial row sums added to acc first (split passes)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
 // Graph relabelling on the device: new row t = old row order[t], neighbour ids renamed by new_of_old
@@ -140,6 +141,16 @@ cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32
                               cudaStream_t st);
 cudaError_t launch_plan_fill(const int64_t* rp, int64_t n, const int64_t* seg_off, const int32_t* split_off,
                              const int32_t* slot_off, const SpmmPlan& p, cudaStream_t st);
+// Distributed local / remote CSR split (SURVEY 8(e) overlap item 1): per row, the edges whose
+// column is in [lo, hi) (this rank's own rows) and the others, each as a CSR in the same order as
+// the input.  Count pass (cnt_loc[i], int64, n + 1 entries) then fill pass (warp per row, stable).
+cudaError_t launch_split_count(const int64_t* rp, const int32_t* ci, int64_t n, int64_t lo, int64_t hi,
+                               int64_t* cnt_loc, int64_t* cnt_rem, cudaStream_t st);
+cudaError_t launch_split_fill(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t lo, int64_t hi,
+                              const int64_t* rp_loc, const int64_t* rp_rem, int32_t* ci_loc, float* val_loc,
+                              int32_t* ci_rem, float* val_rem, cudaStream_t st);
+cudaError_t launch_exclusive_scan64(const int64_t* in, int64_t* out, int64_t n1, void* temp, size_t temp_bytes,
+                                    cudaStream_t st);
 // `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled
 // graph) are marked L2-persisting for this launch (cudaAccessPolicyWindow on `st`).
 // col_block > 0: process the columns in blocks of that width (one launch each).

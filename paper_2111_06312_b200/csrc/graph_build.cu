@@ -109,6 +109,58 @@ __global__ void plan_fill_kernel(const int64_t* __restrict__ rp, int64_t n, cons
   }
 }
 
+__global__ void split_count_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n,
+                                   int64_t lo, int64_t hi, int64_t* __restrict__ cnt_loc, int64_t* __restrict__ cnt_rem) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i <= n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    if (i == n) {
+      if (lane == 0) { cnt_loc[n] = 0; cnt_rem[n] = 0; }
+      continue;
+    }
+    int64_t c = 0;
+    for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) c += (ci[e] >= lo && ci[e] < hi) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) {
+      cnt_loc[i] = c;
+      cnt_rem[i] = (rp[i + 1] - rp[i]) - c;
+    }
+  }
+}
+
+// warp per row: stable partition of the row's edges (ballot + prefix popcount per 32-edge chunk)
+__global__ void split_fill_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const float* __restrict__ val, int64_t n, int64_t lo, int64_t hi,
+                                  const int64_t* __restrict__ rp_loc, const int64_t* __restrict__ rp_rem,
+                                  int32_t* __restrict__ ci_loc, float* __restrict__ val_loc,
+                                  int32_t* __restrict__ ci_rem, float* __restrict__ val_rem) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t pl = rp_loc[i], pr = rp_rem[i];
+    for (int64_t b = rp[i]; b < rp[i + 1]; b += 32) {
+      const int64_t e = b + lane;
+      const bool valid = e < rp[i + 1];
+      const int32_t j = valid ? ci[e] : 0;
+      const bool loc = valid && j >= lo && j < hi;
+      const unsigned ml = __ballot_sync(0xffffffffu, loc), mr = __ballot_sync(0xffffffffu, valid && !loc);
+      const unsigned below = (1u << lane) - 1u;
+      if (loc) {
+        const int64_t d = pl + __popc(ml & below);
+        ci_loc[d] = j;
+        if (val) val_loc[d] = val[e];
+      } else if (valid) {
+        const int64_t d = pr + __popc(mr & below);
+        ci_rem[d] = j;
+        if (val) val_rem[d] = val[e];
+      }
+      pl += __popc(ml);
+      pr += __popc(mr);
+    }
+  }
+}
+
 unsigned grid_n(int64_t n) { return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n + 1, 256), 1), 148 * 16); }
 
 }  // namespace
@@ -156,6 +208,29 @@ cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32
   if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nsplit, split_off, (int)(n + 1), st);
   if (e == cudaSuccess) e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, nslot, slot_off, (int)(n + 1), st);
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_split_count(const int64_t* rp, const int32_t* ci, int64_t n, int64_t lo, int64_t hi,
+                               int64_t* cnt_loc, int64_t* cnt_rem, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>(std::max<int64_t>(ceil_div((n + 1) * 32, 256), 1), 148 * 16);
+  ++g_launches; split_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(rp, ci, n, lo, hi, cnt_loc, cnt_rem);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_fill(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t lo, int64_t hi,
+                              const int64_t* rp_loc, const int64_t* rp_rem, int32_t* ci_loc, float* val_loc,
+                              int32_t* ci_rem, float* val_rem, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 16);
+  ++g_launches;
+  split_fill_kernel<<<(unsigned)blocks, 256, 0, st>>>(rp, ci, val, n, lo, hi, rp_loc, rp_rem, ci_loc, val_loc, ci_rem,
+                                                      val_rem);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_exclusive_scan64(const int64_t* in, int64_t* out, int64_t n1, void* temp, size_t temp_bytes,
+                                    cudaStream_t st) {
+  return cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n1, st);
 }
 
 cudaError_t launch_plan_fill(const int64_t* rp, int64_t n, const int64_t* seg_off, const int32_t* split_off,

@@ -33,6 +33,10 @@ ISVD_DEVICE void acc_add(Acc4& a, float4 v) { a.x += v.x; a.y += v.y; a.z += v.z
 
 // columns [col, col+4) of local row `row`
 ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4 acc) {
+  if (a.pre) {  // the other pass's partial sums (distributed local / remote split)
+    const float4 q = ldg4(a.pre + row * a.ldpre + col);
+    acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+  }
   if (a.self_coef != 0.f) {
     float4 y = ldg4(a.Y + (row + a.row_offset) * a.ldy + col);
     double sc = a.self_coef;
@@ -244,6 +248,7 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     }
     a.Y += c0;
     if (a.T) a.T += c0;
+    if (a.pre) a.pre += c0;
     if (a.colsum) a.colsum += c0;
     a.out += c0;
     int teams, threads;

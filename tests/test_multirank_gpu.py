@@ -266,3 +266,23 @@ def test_multirank_row_subset(where):
                             sp["k"], f"subset {where} P=3"))
     for o in outs:
         assert np.array_equal(o["S"], outs[0]["S"]) and np.array_equal(o["V"], outs[0]["V"])
+
+
+@pytest.mark.skipif(__import__("os").environ.get("ISVD_DIST_SPLIT") == "0", reason="already the child run")
+def test_multirank_blocking_allgather_path():
+    """The default distributed SpMM step splits every row's edges into local / remote parts so the
+    local pass overlaps the all-gather on the collectives stream; ISVD_DIST_SPLIT=0 keeps the
+    single pass after a blocking all-gather.  Both must meet parity: the P = 3 cases re-run in a
+    child process with the switch off (it is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.abspath(__file__)
+    ids = [f"{here}::test_multirank_products_and_isvd[cfg2-3]", f"{here}::test_multirank_products_and_isvd[ragged-NE-3]",
+           f"{here}::test_multirank_row_subset[first_block]"]
+    env = dict(os.environ, ISVD_DIST_SPLIT="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
+                       cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout, r.stdout[-2000:]
