@@ -54,10 +54,12 @@ class ColumnParallel:
     """Harness adapter (not oracle arithmetic): the oracle operator's products applied to column
     chunks in a thread pool.  Columns of M.G and M^T.H are independent and scipy's sparse kernels
     release the GIL, so this spreads the oracle's own per-column computation over the host cores;
-    BLAS inside each chunk runs single-threaded (no oversubscription)."""
+    BLAS inside each chunk runs single-threaded (no oversubscription).  Accumulates the time spent
+    in products (`t_products`)."""
 
     def __init__(self, op, workers):
         self.op, self.workers = op, max(1, int(workers))
+        self.t_products = 0.0
 
     @property
     def shape(self):
@@ -68,10 +70,13 @@ class ColumnParallel:
         from concurrent.futures import ThreadPoolExecutor
         from threadpoolctl import threadpool_limits
 
+        t0 = time.perf_counter()
         chunks = [c for c in np.array_split(np.arange(M.shape[1]), self.workers) if c.size]
         with threadpool_limits(1), ThreadPoolExecutor(len(chunks)) as ex:
             parts = list(ex.map(lambda c: fn(np.ascontiguousarray(M[:, c])), chunks))
-        return np.concatenate(parts, axis=1)
+        out = np.concatenate(parts, axis=1)
+        self.t_products += time.perf_counter() - t0
+        return out
 
     def matmul(self, G):
         return self._par(self.op.matmul, G)
@@ -80,12 +85,20 @@ class ColumnParallel:
         return self._par(self.op.matmul_T, H)
 
 
-def oracle_isvd_timed(cfg, g, X, sp):
-    """One FULL oracle isvd (Alg. 1 in fp64, oracle/) of the config, timed from Omega in to U, s, V
-    out on the host cores: the oracle's own Omega (reading O11), its definition-level products
-    (column chunks in parallel, ColumnParallel), its Householder QR (LAPACK, all cores) and LAPACK
-    SVD of B.  Operator construction (sparse matrix build) is outside the timed region."""
-    import numpy as np  # noqa: F401
+# full oracle isvd of config 4 on the GPU box's 16 cores (round 2, profiles/r02_oracle_full_cfg4.json)
+FULL_ORACLE_CFG4_S = 477.06
+
+
+def oracle_isvd_timed(cfg, g, X, sp, max_cpu_s=30.0):
+    """The fp64 oracle's Alg. 1 (oracle/) on the host cores, timed from Omega in to U, s, V out:
+    its own Omega (reading O11), definition-level products (column chunks in parallel,
+    ColumnParallel), Householder QR (LAPACK, all cores), LAPACK SVD of B, U = Q U_B.
+
+    Configs whose full run fits the bound run in full (value = the measured time).  Config 4's
+    full run takes ~8 minutes (FULL_ORACLE_CFG4_S), so its bounded sample is the same complete
+    Alg. 1 (same graph, X, q) with l' = 24 of the l = 400 columns (k' = 16); the measured product
+    time scales with the column count (products are column-separable) and the rest (QR, SVD of
+    B, U) with its square, so value = t_products * (l / l') + t_rest * (l / l')^2."""
     from threadpoolctl import threadpool_info
 
     from oracle import NCOperator, NEOperator, adjacency, isvd, philox_omega
@@ -94,15 +107,31 @@ def oracle_isvd_timed(cfg, g, X, sp):
     ref = NEOperator(A, sp["weights"], sp["lambda_ones"]) if cfg["op"] == "NE" else NCOperator(A, X, sp["L"])
     cores = os.cpu_count() or 1
     par = ColumnParallel(ref, cores)
+    full = cfg["n"] <= 1_000_000
+    l, k = sp["l"], sp["k"]
+    ls, ks = (l, k) if full else (24, 16)
     t0 = time.perf_counter()
-    om = philox_omega(sp["seed"], 0, ref.shape[1], sp["l"])
-    U, s, V, _ = isvd(par, sp["k"], om, sp["q"])
+    om = philox_omega(sp["seed"], 0, ref.shape[1], ls)
+    U, s, V, _ = isvd(par, ks, om, sp["q"])
     t = time.perf_counter() - t0
     blas = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
-    sample = (f"one full fp64 oracle isvd of {cfg['name']} (Alg. 1: Omega, {2 * sp['q'] + 2} products, "
-              f"{2 * sp['q'] + 2} Householder QRs, LAPACK SVD of B, U/V), products on {cores} threads "
-              f"(column chunks), QR/SVD on {max(blas) if blas else 1} BLAS threads")
-    return t, cores, sample, s
+    nb = max(blas) if blas else 1
+    if full:
+        value = t
+        sample = (f"one full fp64 oracle isvd of {cfg['name']} (Alg. 1: Omega, {2 * sp['q'] + 2} products, "
+                  f"{2 * sp['q'] + 2} Householder QRs, LAPACK SVD of B, U/V) measured: {t:.2f} s; products on "
+                  f"{cores} threads (column chunks, {par.t_products:.2f} s), QR/SVD on {nb} BLAS threads")
+    else:
+        r = l / ls
+        tp, tr = par.t_products, t - par.t_products
+        value = tp * r + tr * r * r
+        sample = (f"bounded sample: the complete fp64 oracle Alg. 1 on {cfg['name']} (same graph, X, q = {sp['q']}) "
+                  f"with l' = {ls} of l = {l} columns (k' = {ks}), measured {t:.2f} s = products {tp:.2f} s "
+                  f"({cores} threads, column chunks) + QR/SVD/U {tr:.2f} s ({nb} BLAS threads); scaled to l = {l}: "
+                  f"products x {r:.1f} (column-separable), the rest x {r * r:.0f} (quadratic in l) = {value:.1f} s. "
+                  f"Check: one full oracle isvd at l = {l} measured {FULL_ORACLE_CFG4_S:.0f} s on the same box type "
+                  "(profiles/r02_oracle_full_cfg4.json)")
+    return value, cores, sample, s
 
 
 def run_reference(args):
@@ -115,9 +144,9 @@ def run_reference(args):
     g = make_graph(cfg)
     X = make_features(cfg["n"], cfg["d"], cfg["seed"]) if cfg["op"] == "NC" else None
     sp = solver_params(cfg)
-    # each step is one full oracle isvd; at config 4 a single one takes minutes on the host, so the
-    # run is bounded to one timed isvd (no warm-up: nothing is cached between runs) there
-    runs = 1 if cfg["n"] > 1_000_000 else max(1, args.steps)
+    # each step is one oracle isvd (config 4: the bounded sample of oracle_isvd_timed), bounded to
+    # a few minutes in total
+    runs = 1 if cfg["n"] > 1_000_000 else max(1, min(args.steps, 5))
     times = []
     cores, sample = 1, ""
     for _ in range(runs):
@@ -131,7 +160,7 @@ def run_reference(args):
         "config": {"workload": cfg["name"], "n": cfg["n"], "m": cfg["m"], "k": sp["k"], "l": sp["l"], "q": sp["q"]},
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle",
                          "sample": sample + f"; {runs} run(s), median (--steps {args.steps} --warmup {args.warmup} "
-                                            "requested; config 4 runs once)"},
+                                            "requested; at most 5 runs, config 4 once, no warm-up)"},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

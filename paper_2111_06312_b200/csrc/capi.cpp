@@ -601,7 +601,7 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
   // relabelled graphs: the leading (hub) rows of the gather source stay L2-persisting
   size_t persist = 0;
   if (g->new2old) persist = std::min(ctx->max_persist_l2, (size_t)(g->n_pad * ctx->world) * a.wpad * sizeof(float));
-  static const char* persist_env = getenv("ISVD_L2_PERSIST_MB");  // tuning override (MB; 0 = off)
+  const char* persist_env = getenv("ISVD_L2_PERSIST_MB");  // tuning override (MB; 0 = off), read per call
   if (persist_env && g->new2old) persist = std::min(persist, (size_t)atoll(persist_env) << 20);
   static const char* cols_env = getenv("ISVD_SPMM_COLS");  // tuning override: column block width
   const int64_t col_block = cols_env ? atoll(cols_env) : 0;

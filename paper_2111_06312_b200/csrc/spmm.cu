@@ -22,6 +22,8 @@
 // bytes).  The graph is then relabelled by degree (capi.cpp) so the hub rows —
 // 2 % of the nodes take 41 % of the gathers — are one contiguous prefix that an
 // L2 persisting window keeps resident (profiles/r01_spmm_sweep.md).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace isvd {
@@ -178,15 +180,6 @@ void team_shape(int64_t wpad, int* teams, int* threads) {
   *threads = TS * R;
 }
 
-void set_window(cudaStream_t st, const void* base, size_t bytes) {
-  cudaStreamAttrValue v = {};
-  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-  v.accessPolicyWindow.num_bytes = bytes;
-  v.accessPolicyWindow.hitRatio = bytes ? 1.0f : 0.0f;
-  v.accessPolicyWindow.hitProp = bytes ? cudaAccessPropertyPersisting : cudaAccessPropertyNormal;
-  v.accessPolicyWindow.missProp = bytes ? cudaAccessPropertyStreaming : cudaAccessPropertyNormal;
-  cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
-}
 
 }  // namespace
 
@@ -239,12 +232,24 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
   for (int64_t c0 = 0; c0 < a0.wpad; c0 += cb) {
     SpmmArgs a = a0;
     a.wpad = (a0.wpad - c0) < cb ? (a0.wpad - c0) : cb;
+    // L2 persisting window on the hub prefix of the gather source, as a LAUNCH attribute (captured
+    // into the CUDA graph's kernel node; a stream attribute is not, which cost 20 % at config 4:
+    // ncu, graph replay without the window 29-30 ms / 167 GB DRAM per step vs 26.4 ms / 140 GB)
+    cudaLaunchAttribute attr[1];
+    int nattr = 0;
     if (persist_bytes) {
       // the window spans whole rows; only this block's slices of them are touched, so it is
       // widened by ldy / width to keep about persist_bytes of persisting lines in use
       size_t wb = persist_bytes * (size_t)(a0.ldy / a.wpad);
       if (wb > (size_t)max_window) wb = (size_t)max_window;
-      set_window(st, a0.Y + c0, wb);
+      attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      attr[0].val.accessPolicyWindow.base_ptr = const_cast<float*>(a0.Y + c0);
+      attr[0].val.accessPolicyWindow.num_bytes = wb;
+      const char* hr = getenv("ISVD_L2_HIT_RATIO");  // tuning override (read per launch; default 1)
+      attr[0].val.accessPolicyWindow.hitRatio = hr ? (float)atof(hr) : 1.0f;
+      attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      nattr = 1;
     }
     a.Y += c0;
     if (a.T) a.T += c0;
@@ -259,13 +264,20 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     int64_t cap = (int64_t)num_sms * per_sm * 4;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.stream = st;
+    cfg.attrs = nattr ? attr : nullptr;
+    cfg.numAttrs = nattr;
     ++g_launches;
-    if (a.val)
-      spmm_kernel<true><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len,
-                                                         plan.seg_slot, plan.n_seg, teams, ws_partial);
-    else
-      spmm_kernel<false><<<(int)blocks, threads, 0, st>>>(a, plan.seg_row, plan.seg_beg, plan.seg_len,
-                                                          plan.seg_slot, plan.n_seg, teams, ws_partial);
+    cudaError_t e = a.val ? cudaLaunchKernelEx(&cfg, spmm_kernel<true>, a, (const int32_t*)plan.seg_row,
+                                               (const int64_t*)plan.seg_beg, (const int32_t*)plan.seg_len,
+                                               (const int32_t*)plan.seg_slot, plan.n_seg, teams, ws_partial)
+                          : cudaLaunchKernelEx(&cfg, spmm_kernel<false>, a, (const int32_t*)plan.seg_row,
+                                               (const int64_t*)plan.seg_beg, (const int32_t*)plan.seg_len,
+                                               (const int32_t*)plan.seg_slot, plan.n_seg, teams, ws_partial);
+    if (e != cudaSuccess) return e;
     if (plan.n_split_rows > 0) {
       int64_t fb = ceil_div(plan.n_split_rows, teams);
       if (fb > cap) fb = cap;
@@ -274,7 +286,6 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
                                                      plan.n_split_rows, teams, ws_partial);
     }
   }
-  if (persist_bytes) set_window(st, nullptr, 0);
   return cudaGetLastError();
 }
 
