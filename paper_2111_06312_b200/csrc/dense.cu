@@ -559,18 +559,9 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
     ++g_launches;
     // 3 CTAs per SM (128 registers, a few bytes of spill) hide the per-tile prologue and the
     // barriers better than 2: X G_j 5.47 -> 5.04 ms, Y R^-1 11.65 -> 11.34 ms at config 4
-    static const int tm16 = getenv("ISVD_GEMM_TM16") ? atoi(getenv("ISVD_GEMM_TM16")) : 0;  // experiment
-    if (tm16 > 0) {
-      // 16 x 8 register tiles: 6 shared-memory float4 reads per 128 FMAs instead of 4 per 64
-      dim3 g16((unsigned)ceil_div(N, 80), (unsigned)ceil_div(M, 256));
-      dim3 g12((unsigned)ceil_div(N, 80), (unsigned)ceil_div(M, 192));
-      if (tm16 == 3)
-        gemm_tn_kernel<192, 80, 8, 12, 8, 2><<<g12, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                                 upper_tri_b ? 1 : 0, gate, out_map);
-      else
-        gemm_tn_kernel<256, 80, 8, 16, 8, 1><<<g16, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
-                                                                 upper_tri_b ? 1 : 0, gate, out_map);
-    } else if (K >= 256)
+    // (16 x 8 and 12 x 8 register tiles -- fewer shared-memory reads per FMA -- measured slower:
+    //  X G_j 7.41 / 6.30 ms, Y R^-1 15.8 / 13.6 ms vs 5.04 / 11.3 ms; profiles/r02b_dense_check.txt)
+    if (K >= 256)
       gemm_tn_kernel<128, 80, 16, 8, 8, 3><<<grid, 160, 0, st>>>(A, lda, B, ldb, C, ldc, M, N, K, row_scale, alpha,
                                                                 upper_tri_b ? 1 : 0, gate, out_map);
     else
