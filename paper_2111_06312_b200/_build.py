@@ -74,10 +74,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
     nccl_inc, nccl_lib = _nccl_dirs()
+    checked = ["-DISVD_BOUNDS_CHECK"] if os.environ.get("ISVD_BOUNDS_CHECK") == "1" else []
     objs = []
     for src, extra in SOURCES:
         obj = os.path.join(BUILD, src + ".o")
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-I" + nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc, *ARCH, *COMMON, *extra, *checked, "-I" + nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         _run(cmd)

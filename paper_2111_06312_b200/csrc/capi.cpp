@@ -581,6 +581,7 @@ SpmmArgs spmm_base(const isvd_graph_s* g, int64_t wpad) {
   a.post_coef = 1.f;
   a.term_coef = 1.f;
   a.wpad = wpad;
+  a.n_src = g->n_pad * g->ctx->world;  // full-height gather sources (the caller's Q for n_local-row sources)
   return a;
 }
 

@@ -6,6 +6,15 @@
 
 #define ISVD_DEVICE __device__ __forceinline__
 
+// Checked build (ISVD_BOUNDS_CHECK=1 python -m paper_2111_06312_b200._build --force): device-side
+// bounds asserts on every gathered / mapped row index (compute-sanitizer is closed on this pool).
+#if defined(ISVD_BOUNDS_CHECK) && defined(__CUDACC__)
+#include <cassert>
+#define ISVD_ASSERT(c) assert(c)
+#else
+#define ISVD_ASSERT(c) ((void)0)
+#endif
+
 namespace isvd {
 
 // Device-side status word shared by every kernel of one solver call.
@@ -119,6 +128,7 @@ struct SpmmArgs {
   const int32_t* out_map;  // nullable
   int64_t wpad;            // columns processed (multiple of 4)
   const float* pre; int64_t ldpre;  // nullable: fp32 partial row sums added to acc first (split passes)
+  int64_t n_src;                    // rows readable in Y (bounds-checked builds assert every gather)
 };
 int64_t spmm_ws_floats(const SpmmPlan& plan, int64_t wpad);
 // Graph relabelling on the device: new row t = old row order[t], neighbour ids renamed by new_of_old

@@ -482,6 +482,7 @@ __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, flo
     int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
     float s = coef * (vec ? vec[i] : 1.f);
     const int64_t src = in_map ? (int64_t)in_map[i] : i;
+    ISVD_ASSERT(src >= 0 && c + 3 < ldi && c + 3 < ldo);
     float4 v = *reinterpret_cast<const float4*>(in + src * ldi + c);
     *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
   }
@@ -493,6 +494,7 @@ __global__ void scatter_rows_kernel(const float* __restrict__ in, int64_t ldi, f
   const int64_t tot = rows * w4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
+    ISVD_ASSERT(out_map[i] >= 0 && c + 3 < ldo);
     *reinterpret_cast<float4*>(out + (int64_t)out_map[i] * ldo + c) = *reinterpret_cast<const float4*>(in + i * ldi + c);
   }
 }

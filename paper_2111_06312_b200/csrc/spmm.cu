@@ -40,6 +40,7 @@ ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4
     acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
   }
   if (a.self_coef != 0.f) {
+    ISVD_ASSERT(row + a.row_offset < a.n_src);
     float4 y = ldg4(a.Y + (row + a.row_offset) * a.ldy + col);
     double sc = a.self_coef;
     acc.x += sc * y.x; acc.y += sc * y.y; acc.z += sc * y.z; acc.w += sc * y.w;
@@ -59,6 +60,7 @@ ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4
     acc.z -= r * a.colsum[col + 2]; acc.w -= r * a.colsum[col + 3];
   }
   const int64_t orow = a.out_map ? (int64_t)a.out_map[row] : row;
+  ISVD_ASSERT(orow >= 0 && col + 3 < a.ldo);
   st4(a.out + orow * a.ldo + col, make_float4((float)acc.x, (float)acc.y, (float)acc.z, (float)acc.w));
 }
 
@@ -69,10 +71,13 @@ ISVD_DEVICE void spmm_epilogue(const SpmmArgs& a, int64_t row, int64_t col, Acc4
 // kW: weighted graph, each row scaled by its edge weight A_ij inside the fp32 batch.
 template <bool kW>
 ISVD_DEVICE void load_batch(const int32_t* __restrict__ idx, const float* __restrict__ val,
-                            const float* __restrict__ y, int64_t ld, float4 v[8], float wv[8]) {
+                            const float* __restrict__ y, int64_t ld, float4 v[8], float wv[8], int64_t n_src) {
   int j[8];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) j[u] = __ldg(idx + u);
+  for (int u = 0; u < 8; ++u) {
+    j[u] = __ldg(idx + u);
+    ISVD_ASSERT(j[u] >= 0 && j[u] < n_src);
+  }
   if constexpr (kW) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) wv[u] = __ldg(val + u);
@@ -100,15 +105,15 @@ ISVD_DEVICE float4 sum_batch(const float4 v[8], const float wv[8]) {
 
 template <bool kW>
 ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __restrict__ val, int len,
-                                const float* __restrict__ y, int64_t ld) {
+                                const float* __restrict__ y, int64_t ld, int64_t n_src) {
   Acc4 acc{0.0, 0.0, 0.0, 0.0};
   int e = 0;
   if (len >= 8) {
     float4 cur[8], nxt[8];
     float wc[8], wn[8];
-    load_batch<kW>(idx, val, y, ld, cur, wc);
+    load_batch<kW>(idx, val, y, ld, cur, wc, n_src);
     for (e = 8; e + 8 <= len; e += 8) {
-      load_batch<kW>(idx + e, kW ? val + e : val, y, ld, nxt, wn);
+      load_batch<kW>(idx + e, kW ? val + e : val, y, ld, nxt, wn, n_src);
       acc_add(acc, sum_batch<kW>(cur, wc));
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -121,6 +126,7 @@ ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __
   if (e < len) {
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     for (; e < len; ++e) {
+      ISVD_ASSERT(__ldg(idx + e) >= 0 && __ldg(idx + e) < n_src);
       const float4 r = ldg4(y + (int64_t)__ldg(idx + e) * ld);
       t = kW ? f4fma(__ldg(val + e), r, t) : f4add(t, r);
     }
@@ -143,7 +149,8 @@ __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* _
   for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
     const int64_t row = seg_row[s];
     const int64_t b = seg_beg[s];
-    Acc4 acc = gather_segment<kW>(a.col_idx + b, kW ? a.val + b : nullptr, seg_len[s], Yc, a.ldy);
+    ISVD_ASSERT(row >= 0 && seg_len[s] >= 0 && seg_len[s] <= kSegEdges);
+    Acc4 acc = gather_segment<kW>(a.col_idx + b, kW ? a.val + b : nullptr, seg_len[s], Yc, a.ldy, a.n_src);
     const int slot = seg_slot[s];
     if (slot < 0) {
       spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
