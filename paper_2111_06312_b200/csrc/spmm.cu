@@ -103,7 +103,7 @@ ISVD_DEVICE float4 sum_batch(const float4 v[8], const float wv[8]) {
   }
 }
 
-template <bool kW>
+template <bool kW, bool kMaskedTail>
 ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __restrict__ val, int len,
                                 const float* __restrict__ y, int64_t ld, int64_t n_src) {
   Acc4 acc{0.0, 0.0, 0.0, 0.0};
@@ -123,7 +123,7 @@ ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __
     }
     acc_add(acc, sum_batch<kW>(cur, wc));
   }
-  if (e < len) {
+  if (!kMaskedTail && e < len) {  // one dependent load chain per remaining neighbour
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
     for (; e < len; ++e) {
       ISVD_ASSERT(__ldg(idx + e) >= 0 && __ldg(idx + e) < n_src);
@@ -131,27 +131,63 @@ ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __
       t = kW ? f4fma(__ldg(val + e), r, t) : f4add(t, r);
     }
     acc_add(acc, t);
+  } else if (e < len) {
+    // the last (or only) partial batch: its < 8 row loads are all issued before any add (a masked
+    // batch; rows of degree < 8 -- a large share of a power-law graph -- get the same memory-level
+    // parallelism as full batches instead of one dependent load chain per neighbour)
+    const int rem = len - e;
+    int j[8];
+    float4 v[8];
+    float wv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      j[u] = u < rem ? __ldg(idx + e + u) : -1;
+      ISVD_ASSERT(j[u] < n_src);
+      if constexpr (kW) wv[u] = u < rem ? __ldg(val + e + u) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = j[u] >= 0 ? ldg4(y + (int64_t)j[u] * ld) : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc_add(acc, sum_batch<kW>(v, wv));
   }
   return acc;
 }
 
-template <bool kW>
+// kVar bit 0: masked last batch (its < 8 loads in flight together); bit 1: the next segment's
+// descriptor is loaded while this one gathers (it heads a dependent chain: descriptor -> indices
+// -> rows)
+template <bool kW, int kVar>
 __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
                                                     const int64_t* __restrict__ seg_beg,
                                                     const int32_t* __restrict__ seg_len,
                                                     const int32_t* __restrict__ seg_slot, int64_t n_seg,
                                                     int teams, float* __restrict__ partial) {
+  constexpr bool kMasked = kVar & 1, kPrefetch = kVar & 2;
   const int TS = (int)(a.wpad >> 2);
   const int team = threadIdx.x / TS;
   const int c4 = threadIdx.x - team * TS;
   if (team >= teams) return;
   const float* __restrict__ Yc = a.Y + 4 * (int64_t)c4;
-  for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
-    const int64_t row = seg_row[s];
-    const int64_t b = seg_beg[s];
-    ISVD_ASSERT(row >= 0 && seg_len[s] >= 0 && seg_len[s] <= kSegEdges);
-    Acc4 acc = gather_segment<kW>(a.col_idx + b, kW ? a.val + b : nullptr, seg_len[s], Yc, a.ldy, a.n_src);
-    const int slot = seg_slot[s];
+  const int64_t stride = (int64_t)gridDim.x * teams;
+  int64_t s = (int64_t)blockIdx.x * teams + team;
+  int64_t row_n = 0, b_n = 0;
+  int len_n = 0, slot_n = -1;
+  if (kPrefetch && s < n_seg) {
+    row_n = seg_row[s]; b_n = seg_beg[s]; len_n = seg_len[s]; slot_n = seg_slot[s];
+  }
+  for (; s < n_seg; s += stride) {
+    int64_t row, b;
+    int len, slot;
+    if constexpr (kPrefetch) {
+      row = row_n; b = b_n; len = len_n; slot = slot_n;
+      if (s + stride < n_seg) {
+        row_n = seg_row[s + stride]; b_n = seg_beg[s + stride]; len_n = seg_len[s + stride];
+        slot_n = seg_slot[s + stride];
+      }
+    } else {
+      row = seg_row[s]; b = seg_beg[s]; len = seg_len[s]; slot = seg_slot[s];
+    }
+    ISVD_ASSERT(row >= 0 && len >= 0 && len <= kSegEdges);
+    Acc4 acc = gather_segment<kW, kMasked>(a.col_idx + b, kW ? a.val + b : nullptr, len, Yc, a.ldy, a.n_src);
     if (slot < 0) {
       spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
     } else {
@@ -187,6 +223,8 @@ void team_shape(int64_t wpad, int* teams, int* threads) {
   *threads = TS * R;
 }
 
+
+constexpr int kSpmmDefaultVariant = 1;  // masked tail batch (round 2 sweep: profiles/r02c_spmm_variants.jsonl)
 
 }  // namespace
 
@@ -278,12 +316,22 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     cfg.attrs = nattr ? attr : nullptr;
     cfg.numAttrs = nattr;
     ++g_launches;
-    cudaError_t e = a.val ? cudaLaunchKernelEx(&cfg, spmm_kernel<true>, a, (const int32_t*)plan.seg_row,
-                                               (const int64_t*)plan.seg_beg, (const int32_t*)plan.seg_len,
-                                               (const int32_t*)plan.seg_slot, plan.n_seg, teams, ws_partial)
-                          : cudaLaunchKernelEx(&cfg, spmm_kernel<false>, a, (const int32_t*)plan.seg_row,
-                                               (const int64_t*)plan.seg_beg, (const int32_t*)plan.seg_len,
-                                               (const int32_t*)plan.seg_slot, plan.n_seg, teams, ws_partial);
+    const char* ve = getenv("ISVD_SPMM_VARIANT");  // experiment switch (read per launch)
+    const int var = ve ? (atoi(ve) & 3) : kSpmmDefaultVariant;
+    void (*kern)(SpmmArgs, const int32_t*, const int64_t*, const int32_t*, const int32_t*, int64_t, int, float*);
+    switch (var + (a.val ? 4 : 0)) {
+      case 0: kern = spmm_kernel<false, 0>; break;
+      case 1: kern = spmm_kernel<false, 1>; break;
+      case 2: kern = spmm_kernel<false, 2>; break;
+      case 3: kern = spmm_kernel<false, 3>; break;
+      case 4: kern = spmm_kernel<true, 0>; break;
+      case 5: kern = spmm_kernel<true, 1>; break;
+      case 6: kern = spmm_kernel<true, 2>; break;
+      default: kern = spmm_kernel<true, 3>; break;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, (const int32_t*)plan.seg_row, (const int64_t*)plan.seg_beg,
+                                       (const int32_t*)plan.seg_len, (const int32_t*)plan.seg_slot, plan.n_seg, teams,
+                                       ws_partial);
     if (e != cudaSuccess) return e;
     if (plan.n_split_rows > 0) {
       int64_t fb = ceil_div(plan.n_split_rows, teams);
