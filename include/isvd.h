@@ -263,6 +263,9 @@ typedef struct {
    * small = Omega, the final SVD of R^T, U / V and the sign rule; comm = the collectives alone
    * (a subset of the other three). */
   double ms_products, ms_orth, ms_small, ms_comm;
+  int32_t gram_probe_fallbacks; /* first-pass tensor-core Gram probes that fell back to the exact fp64
+                                   Gram (ill-conditioned M Omega)                   */
+  int32_t pad1;
 } isvd_svd_report;
 
 /* Rank-k randomized SVD of M (Alg. 1) with CholeskyQR2

@@ -95,6 +95,8 @@ class SvdReport(C.Structure):
         ("ms_orth", C.c_double),
         ("ms_small", C.c_double),
         ("ms_comm", C.c_double),
+        ("gram_probe_fallbacks", C.c_int32),
+        ("pad1", C.c_int32),
     ]
 
 

@@ -197,6 +197,7 @@ class SvdResult:
     ms_spmm: float = 0.0
     spmm_alg_bytes: float = 0.0
     phases: "dict | None" = None  # profile=True: ms by phase (products / orth / small / comm)
+    gram_probe_fallbacks: int = 0  # first-pass tensor-core Gram probes that fell back to the exact Gram
 
 
 class _Operator:
@@ -329,7 +330,7 @@ class _Operator:
         if profile:
             phases = dict(products=rep.ms_products, orth=rep.ms_orth, small=rep.ms_small, comm=rep.ms_comm)
         return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
-                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases)
+                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases, rep.gram_probe_fallbacks)
 
 
 class NE(_Operator):

@@ -25,7 +25,9 @@ struct DevStatus {
   int nonfinite;        // NaN/Inf produced
   int jacobi_sweeps;    // sweeps used by the last Jacobi SVD
   int need_extra_pass;  // set by a Cholesky that used the shift: run the third CQR pass
-  int pad[3];
+  int need_exact_gram;  // set by a probe-mode Cholesky: recompute the Gram exactly (fp64) and refactor
+  int probes_failed;    // count of those (reported)
+  int pad;
 };
 
 #if defined(__CUDACC__)
@@ -226,8 +228,11 @@ cudaError_t launch_f64_to_f32(const double* G, int64_t ldg, float* out, int64_t 
 // status->need_extra_pass = 1.  force_fail treats the first attempt as broken.
 // `ws` needs l*l doubles when l > 512 (global-memory path).
 constexpr int kCholSmemMax = 160;
+// probe_tol > 0 (blocked path, l <= 512 only): probe mode -- no shift; a breakdown or a pivot spread
+// min r_kk^2 < probe_tol max r_kk^2 sets *probe_flag (the Gram was too inexact for this conditioning).
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64,
-                            double* ws, DevStatus* status, bool force_fail, const int* gate, cudaStream_t st);
+                            double* ws, DevStatus* status, bool force_fail, const int* gate, cudaStream_t st,
+                            double probe_tol = 0.0, int* probe_flag = nullptr);
 // out = Rnew * Racc (upper l x l fp64, ld = l); when gated off: out = Racc.
 cudaError_t launch_trmm(const double* Rnew, const double* Racc, double* out, int l, const int* gate,
                         cudaStream_t st);

@@ -599,10 +599,14 @@ struct ClusterLayout {
   ISVD_DEVICE int global_row(int r) const { return ((r / kPanel) * CS + c) * kPanel + (r % kPanel); }
 };
 
+// probe_tol > 0 (probe mode, for a Gram with fp32-class error): a breakdown, or a pivot spread
+// min_k r_kk^2 < probe_tol * max_k r_kk^2 (kappa(Y)^2 too large for that Gram), sets *probe_flag
+// instead of shifting; the caller then recomputes the Gram exactly and refactors (gated on the flag).
 __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __restrict__ G, int64_t ldg, int l,
                                                                int64_t ld, float* __restrict__ Rinv32,
                                                                double* __restrict__ R64, DevStatus* status,
-                                                               int force_fail, const int* gate) {
+                                                               int force_fail, const int* gate, double probe_tol,
+                                                               int* probe_flag) {
   if (gate && *((volatile const int*)gate) == 0) return;  // same value for every CTA of the cluster
   cg::cluster_group cl = cg::this_cluster();
   ClusterLayout L;
@@ -615,9 +619,14 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
   double* P = sm + (size_t)L.rows_max * l;         // kPanel x l (panel copy)
   double* colk = P + (size_t)kPanel * l;           // rows_max x kPanel
   __shared__ double s_misc[4];
+  __shared__ double s_pmin, s_pmax;  // pivots factored by this CTA (probe mode)
   __shared__ int s_bad, s_remote_bad;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int my_rows = ((L.nblk - L.c + L.CS - 1) / L.CS) * kPanel;
+  if (tid == 0) {
+    s_pmin = INFINITY;
+    s_pmax = 0.0;
+  }
 
   if (tid == 0) {
     double tr = 0.0, mx = 0.0;
@@ -655,6 +664,8 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
             double piv = rk[kk];
             int b = !(piv > tol) || !isfinite(piv);
             if (b) s_bad = 1;
+            s_pmin = fmin(s_pmin, piv);
+            s_pmax = fmax(s_pmax, piv);
             double rr = b ? 1.0 : sqrt(piv);
             rk[kk] = rr;
             s_misc[0] = 1.0 / rr;
@@ -696,10 +707,26 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
       __syncthreads();
     }
     if (force_fail && attempt == 0) bad = 1;
+    if (probe_tol > 0.0) {  // probe mode: never shift; flag breakdown or a too-wide pivot spread
+      cl.sync();
+      if (L.c == 0 && tid == 0) {
+        double pmin = INFINITY, pmax = 0.0;
+        for (int q = 0; q < L.CS; ++q) {
+          pmin = fmin(pmin, *cl.map_shared_rank(&s_pmin, q));
+          pmax = fmax(pmax, *cl.map_shared_rank(&s_pmax, q));
+        }
+        if (bad || !(pmin >= probe_tol * pmax)) {
+          *probe_flag = 1;
+          atomicAdd(&status->probes_failed, 1);
+        }
+      }
+      failed = 0;
+      break;
+    }
     if (!bad) { failed = 0; break; }
     shift = (attempt == 0) ? 1e-10 * trace : shift * 100.0;
   }
-  if (L.c == 0 && tid == 0) {
+  if (L.c == 0 && tid == 0 && probe_tol <= 0.0) {
     if (attempt > 0) {
       atomicAdd(&status->chol_breakdown, 1);
       status->need_extra_pass = 1;
@@ -783,7 +810,8 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
 }  // namespace
 
 cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, float* Rinv32, double* R64, double* ws,
-                            DevStatus* status, bool force_fail, const int* gate, cudaStream_t st) {
+                            DevStatus* status, bool force_fail, const int* gate, cudaStream_t st, double probe_tol,
+                            int* probe_flag) {
   // Blocked (panel) algorithm: one CTA for l <= kCholSmemMax (whole matrix in its shared
   // memory), a cluster of 8 / 16 CTAs sharing it through DSMEM above that.
   if (l <= 512 && !getenv("ISVD_CHOL_UNBLOCKED")) {
@@ -813,7 +841,7 @@ cudaError_t launch_chol_inv(const double* G, int64_t ldg, int l, int64_t ld, flo
     cfg.numAttrs = 1;
     ++g_launches;
     return cudaLaunchKernelEx(&cfg, chol_inv_cluster_kernel, G, ldg, l, ld, Rinv32, R64, status,
-                              force_fail ? 1 : 0, gate);
+                              force_fail ? 1 : 0, gate, probe_tol, probe_flag);
   }
   size_t smem = (l <= kCholSmemMax) ? sizeof(double) * (size_t)l * l : 0;
   static bool attr_set = false;

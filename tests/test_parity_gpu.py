@@ -186,7 +186,12 @@ def test_cholesky_fallback_nc_deferred_update_in_parity(ctx):
     op, _, cfg, sp = _op(ctx, 2)
     res = op.svd(sp["k"], -1 if cfg["p"] is None else cfg["p"], sp["q"], sp["seed"], force_chol_fail=True)
     assert res.chol_fallbacks > 0
+    # the first tall pass probes with the tensor-core Gram; the forced breakdown must take the
+    # gated exact-Gram path (gram_probe_fallbacks) and still meet parity
+    assert res.gram_probe_fallbacks > 0
     _check_isvd(res, _oracle_result(2), sp["k"], "cfg2/fallback")
+    clean = op.svd(sp["k"], -1 if cfg["p"] is None else cfg["p"], sp["q"], sp["seed"])
+    assert clean.gram_probe_fallbacks == 0  # config 2's M Omega is well conditioned: the probe holds
 
 
 # ------------------------------------------------------------ edge cases
@@ -355,8 +360,10 @@ def test_tc_products_mode_parity():
 def test_alternative_kernel_paths_parity():
     """The switchable alternatives stay in parity: DFMA exact Gram (ISVD_DMMA=0), pairwise
     cooperative Jacobi (ISVD_JACOBI_PAIRWISE=1), SIMT Grams (ISVD_TC_GRAM=0), no allocator cache
-    (ISVD_NO_POOL=1), NC dense terms overlapped on a second stream (ISVD_OVERLAP=1) -- all at once, configs 2 (NC, l = 256) and 3 (NE, l = 160), in a child
-    process (some switches are read once per process)."""
+    (ISVD_NO_POOL=1), NC dense terms overlapped on a second stream (ISVD_OVERLAP=1), the exact
+    first Gram without the tensor-core probe (ISVD_GRAM_PROBE=0), the SpMM descriptor-prefetch
+    variant without the masked tail (ISVD_SPMM_VARIANT=2) -- all at once, configs 2 (NC, l = 256)
+    and 3 (NE, l = 160), in a child process (some switches are read once per process)."""
     import os
     import subprocess
     import sys
@@ -364,7 +371,7 @@ def test_alternative_kernel_paths_parity():
     here = os.path.abspath(__file__)
     ids = [f"{here}::test_isvd_parity[2]", f"{here}::test_isvd_parity[3]", f"{here}::test_products[orthonormal-2]"]
     env = dict(os.environ, ISVD_ALT_PATHS="1", ISVD_DMMA="0", ISVD_JACOBI_PAIRWISE="1", ISVD_TC_GRAM="0",
-               ISVD_NO_POOL="1", ISVD_OVERLAP="1")
+               ISVD_NO_POOL="1", ISVD_OVERLAP="1", ISVD_GRAM_PROBE="0", ISVD_SPMM_VARIANT="2")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
                        cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
