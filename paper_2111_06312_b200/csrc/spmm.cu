@@ -152,42 +152,28 @@ ISVD_DEVICE Acc4 gather_segment(const int32_t* __restrict__ idx, const float* __
   return acc;
 }
 
-// kVar bit 0: masked last batch (its < 8 loads in flight together); bit 1: the next segment's
-// descriptor is loaded while this one gathers (it heads a dependent chain: descriptor -> indices
-// -> rows)
-template <bool kW, int kVar>
+// kMasked: the last (partial) batch of a segment issues all its < 8 loads together (default);
+// otherwise one dependent load chain per remaining neighbour.  (A variant that loaded the next
+// segment's descriptor during the gather spilled 156 B at the 64-register cap and ran 25 % slower:
+// profiles/r02c_spmm_variants.jsonl.)
+template <bool kW, bool kMasked>
 __global__ void __launch_bounds__(1024) spmm_kernel(SpmmArgs a, const int32_t* __restrict__ seg_row,
                                                     const int64_t* __restrict__ seg_beg,
                                                     const int32_t* __restrict__ seg_len,
                                                     const int32_t* __restrict__ seg_slot, int64_t n_seg,
                                                     int teams, float* __restrict__ partial) {
-  constexpr bool kMasked = kVar & 1, kPrefetch = kVar & 2;
   const int TS = (int)(a.wpad >> 2);
   const int team = threadIdx.x / TS;
   const int c4 = threadIdx.x - team * TS;
   if (team >= teams) return;
   const float* __restrict__ Yc = a.Y + 4 * (int64_t)c4;
-  const int64_t stride = (int64_t)gridDim.x * teams;
-  int64_t s = (int64_t)blockIdx.x * teams + team;
-  int64_t row_n = 0, b_n = 0;
-  int len_n = 0, slot_n = -1;
-  if (kPrefetch && s < n_seg) {
-    row_n = seg_row[s]; b_n = seg_beg[s]; len_n = seg_len[s]; slot_n = seg_slot[s];
-  }
-  for (; s < n_seg; s += stride) {
-    int64_t row, b;
-    int len, slot;
-    if constexpr (kPrefetch) {
-      row = row_n; b = b_n; len = len_n; slot = slot_n;
-      if (s + stride < n_seg) {
-        row_n = seg_row[s + stride]; b_n = seg_beg[s + stride]; len_n = seg_len[s + stride];
-        slot_n = seg_slot[s + stride];
-      }
-    } else {
-      row = seg_row[s]; b = seg_beg[s]; len = seg_len[s]; slot = seg_slot[s];
-    }
+  for (int64_t s = (int64_t)blockIdx.x * teams + team; s < n_seg; s += (int64_t)gridDim.x * teams) {
+    const int64_t row = seg_row[s];
+    const int64_t b = seg_beg[s];
+    const int len = seg_len[s];
     ISVD_ASSERT(row >= 0 && len >= 0 && len <= kSegEdges);
     Acc4 acc = gather_segment<kW, kMasked>(a.col_idx + b, kW ? a.val + b : nullptr, len, Yc, a.ldy, a.n_src);
+    const int slot = seg_slot[s];
     if (slot < 0) {
       spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
     } else {
@@ -223,8 +209,6 @@ void team_shape(int64_t wpad, int* teams, int* threads) {
   *threads = TS * R;
 }
 
-
-constexpr int kSpmmDefaultVariant = 1;  // masked tail batch (round 2 sweep: profiles/r02c_spmm_variants.jsonl)
 
 }  // namespace
 
@@ -316,19 +300,11 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     cfg.attrs = nattr ? attr : nullptr;
     cfg.numAttrs = nattr;
     ++g_launches;
-    const char* ve = getenv("ISVD_SPMM_VARIANT");  // experiment switch (read per launch)
-    const int var = ve ? (atoi(ve) & 3) : kSpmmDefaultVariant;
-    void (*kern)(SpmmArgs, const int32_t*, const int64_t*, const int32_t*, const int32_t*, int64_t, int, float*);
-    switch (var + (a.val ? 4 : 0)) {
-      case 0: kern = spmm_kernel<false, 0>; break;
-      case 1: kern = spmm_kernel<false, 1>; break;
-      case 2: kern = spmm_kernel<false, 2>; break;
-      case 3: kern = spmm_kernel<false, 3>; break;
-      case 4: kern = spmm_kernel<true, 0>; break;
-      case 5: kern = spmm_kernel<true, 1>; break;
-      case 6: kern = spmm_kernel<true, 2>; break;
-      default: kern = spmm_kernel<true, 3>; break;
-    }
+    const char* ve = getenv("ISVD_SPMM_VARIANT");  // 0: sequential tail (A/B switch, read per launch)
+    const bool masked = ve ? atoi(ve) != 0 : true;
+    void (*kern)(SpmmArgs, const int32_t*, const int64_t*, const int32_t*, const int32_t*, int64_t, int, float*) =
+        a.val ? (masked ? spmm_kernel<true, true> : spmm_kernel<true, false>)
+              : (masked ? spmm_kernel<false, true> : spmm_kernel<false, false>);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, (const int32_t*)plan.seg_row, (const int64_t*)plan.seg_beg,
                                        (const int32_t*)plan.seg_len, (const int32_t*)plan.seg_slot, plan.n_seg, teams,
                                        ws_partial);

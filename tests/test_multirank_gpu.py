@@ -286,3 +286,44 @@ def test_multirank_blocking_allgather_path():
                        cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "3 passed" in r.stdout, r.stdout[-2000:]
+
+
+def test_multirank_more_ranks_than_rows():
+    """P = 8 simulated ranks on an n = 5 graph: ranks 5..7 own no rows (zero-row CSR, empty
+    gather-source slices, empty Grams and sign-rule candidates), NE and NC, against the oracle."""
+    from oracle import NCOperator, NEOperator, adjacency, isvd, philox_omega
+    from synth.graphs import edges_to_graph
+
+    import paper_2111_06312_b200 as isvd_mod
+
+    g = edges_to_graph(5, [(0, 1), (1, 2), (2, 3), (3, 4), (0, 4), (1, 3)])
+    A = adjacency(g.n, g.row_ptr, g.col_idx)
+    X = np.random.default_rng(1).standard_normal((5, 2)).astype(np.float32)
+    w = np.full(3, 1 / 3)
+
+    def fn(rank, ctx):
+        rb, nl = isvd_mod.partition(g.n, ctx.world, ctx.rank)
+        rp, ci = g.row_slice(rb, rb + nl)
+        graph = isvd_mod.Graph(ctx, g.n, rp, ci)
+        ne = isvd_mod.NE(graph, w, 0.2)
+        a = ne.svd(2, 2, 1, 3)
+        Xl = torch.from_numpy(np.ascontiguousarray(X[rb : rb + nl])).cuda() if nl > 0 else np.zeros((0, 2), np.float32)
+        nc = isvd_mod.NC(graph, Xl, 1)
+        b = nc.svd(2, 2, 1, 4)
+        o = dict(Sa=a.S.copy(), Ua=a.U.cpu().numpy(), Va=a.V.cpu().numpy(), Sb=b.S.copy(), Ub=b.U.cpu().numpy(),
+                 Vb=b.V.cpu().numpy(), nl=nl)
+        nc.close()
+        ne.close()
+        graph.close()
+        return o
+
+    outs = run_ranks(8, fn)
+    assert [o["nl"] for o in outs] == [1, 1, 1, 1, 1, 0, 0, 0]
+    ref = NEOperator(A, w, 0.2)
+    Ua = np.concatenate([o["Ua"] for o in outs]).astype(np.float64)
+    Va = np.concatenate([o["Va"] for o in outs]).astype(np.float64)
+    print(check_isvd_arrays(Ua, outs[0]["Sa"], Va, isvd(ref, 2, philox_omega(3, 0, 5, 4), 1), 2, "NE n=5 P=8"))
+    refc = NCOperator(A, X, 1)
+    Ub = np.concatenate([o["Ub"] for o in outs]).astype(np.float64)
+    print(check_isvd_arrays(Ub, outs[0]["Sb"], outs[0]["Vb"].astype(np.float64),
+                            isvd(refc, 2, philox_omega(4, 0, 4, 4), 1), 2, "NC n=5 P=8"))

@@ -361,8 +361,8 @@ def test_alternative_kernel_paths_parity():
     """The switchable alternatives stay in parity: DFMA exact Gram (ISVD_DMMA=0), pairwise
     cooperative Jacobi (ISVD_JACOBI_PAIRWISE=1), SIMT Grams (ISVD_TC_GRAM=0), no allocator cache
     (ISVD_NO_POOL=1), NC dense terms overlapped on a second stream (ISVD_OVERLAP=1), the exact
-    first Gram without the tensor-core probe (ISVD_GRAM_PROBE=0), the SpMM descriptor-prefetch
-    variant without the masked tail (ISVD_SPMM_VARIANT=2) -- all at once, configs 2 (NC, l = 256)
+    first Gram without the tensor-core probe (ISVD_GRAM_PROBE=0), the SpMM's sequential tail instead
+    of the masked last batch (ISVD_SPMM_VARIANT=0) -- all at once, configs 2 (NC, l = 256)
     and 3 (NE, l = 160), in a child process (some switches are read once per process)."""
     import os
     import subprocess
@@ -371,7 +371,7 @@ def test_alternative_kernel_paths_parity():
     here = os.path.abspath(__file__)
     ids = [f"{here}::test_isvd_parity[2]", f"{here}::test_isvd_parity[3]", f"{here}::test_products[orthonormal-2]"]
     env = dict(os.environ, ISVD_ALT_PATHS="1", ISVD_DMMA="0", ISVD_JACOBI_PAIRWISE="1", ISVD_TC_GRAM="0",
-               ISVD_NO_POOL="1", ISVD_OVERLAP="1", ISVD_GRAM_PROBE="0", ISVD_SPMM_VARIANT="2")
+               ISVD_NO_POOL="1", ISVD_OVERLAP="1", ISVD_GRAM_PROBE="0", ISVD_SPMM_VARIANT="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *ids], env=env,
                        cwd=os.path.dirname(os.path.dirname(here)), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
@@ -742,4 +742,58 @@ def test_row_subset_operator(ctx, i):
         print(_check_isvd(res, isvd(ref, sp["k"], om, sp["q"]), sp["k"], f"cfg{i} subset"))
         assert res.l == l
     op.close()
+    graph.close()
+
+
+# --------------------------------------------- degenerate inputs
+
+
+def test_edgeless_graph_both_families(ctx):
+    """nnz = 0 (every node isolated): NE's T is 0 (reading O3), so M = -lambda 1 1^T (rank 1,
+    sigma_1 = lambda n); NC's A_hat is I, so M = [X | X | X | X].  Products and the isvd (k = 1 for
+    NE: the only nonzero singular value; k = l = 3 = rank(M) for NC) against the oracle."""
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import NCOperator, NEOperator, adjacency, isvd, philox_omega
+
+    n = 6
+    rp = np.zeros(n + 1, dtype=np.int64)
+    ci = np.zeros(0, dtype=np.int32)
+    A = adjacency(n, rp, ci)
+    graph = isvd_mod.Graph(ctx, n, rp, ci)
+    ne = isvd_mod.NE(graph, [0.5, 0.5], 0.25)
+    ref = NEOperator(A, [0.5, 0.5], 0.25)
+    rng = np.random.default_rng(3)
+    Q = rng.standard_normal((n, 4)).astype(np.float32)
+    assert_product(_to_np(ne.matmul(torch.from_numpy(Q).cuda())), ref.matmul(Q.astype(np.float64)))
+    assert_product(_to_np(ne.matmul_T(torch.from_numpy(Q).cuda())), ref.matmul_T(Q.astype(np.float64)))
+    res = ne.svd(1, 3, 1, 7)
+    assert abs(res.S[0] - 0.25 * n) <= 1e-6 * 0.25 * n
+    X = rng.standard_normal((n, 3)).astype(np.float32)
+    nc = isvd_mod.NC(graph, torch.from_numpy(X).cuda(), 3)
+    refc = NCOperator(A, X, 3)
+    G = rng.standard_normal((12, 5)).astype(np.float32)
+    assert_product(_to_np(nc.matmul(torch.from_numpy(G).cuda())), refc.matmul(G.astype(np.float64)))
+    assert_product(_to_np(nc.matmul_T(torch.from_numpy(Q).cuda())), refc.matmul_T(Q.astype(np.float64)))
+    r2 = nc.svd(3, 0, 1, 11)  # l = 3 = rank(M): Y = M Omega has full column rank
+    om = philox_omega(11, 0, 12, 3)
+    _check_isvd(r2, isvd(refc, 3, om, 1), 3, "edgeless NC")
+    nc.close()
+    ne.close()
+    graph.close()
+
+
+def test_single_node_graph(ctx):
+    """n = 1: NE with C = 1, lambda = 0 is T = [0]; NC (L = 2) of a single node is [x | x | x]
+    (A_hat = [1]).  k = 1 isvd of the NC op against its exact SVD."""
+    import paper_2111_06312_b200 as isvd_mod
+
+    rp = np.zeros(2, dtype=np.int64)
+    ci = np.zeros(0, dtype=np.int32)
+    graph = isvd_mod.Graph(ctx, 1, rp, ci)
+    x = np.array([[3.0, 4.0]], dtype=np.float32)
+    nc = isvd_mod.NC(graph, torch.from_numpy(x).cuda(), 2)
+    assert nc.shape == (1, 6)
+    res = nc.svd(1, 0, 1, 0)
+    assert abs(res.S[0] - np.sqrt(3 * 25.0)) <= 1e-5 * np.sqrt(75.0)
+    nc.close()
     graph.close()
