@@ -237,6 +237,31 @@ def load_traffic(workload):
     return None
 
 
+def gather_floor(g, sp, world, alg_bytes_per_launch, avg_launch_ms):
+    """A floor for one SpMM step of a relabelled single-GPU graph: the gathers of
+    rows outside the 79 MB persisting hub window must come from DRAM at <= 6.3 TB/s (measured random
+    1600-B row gathers, profiles/r02_l2_gather_bench2.jsonl) and the rest of the algorithmic bytes
+    (CSR, scales, epilogue operand, output) at the measured copy peak.  Row sums of the degree
+    sequence give the hub share exactly."""
+    import numpy as np
+
+    l = sp["l"]
+    ld = (l + 3) // 4 * 4
+    if world != 1 or 4 * g.n * ld < 8 * 126e6 or not avg_launch_ms:  # gather source must dwarf L2
+        return None
+    rows_in_window = int(79e6 // (4 * ld))
+    deg = np.sort(np.diff(g.row_ptr))[::-1]
+    hub_share = float(deg[:rows_in_window].sum() / deg.sum())
+    cold = 4.0 * ld * float(deg[rows_in_window:].sum())
+    rest = alg_bytes_per_launch - 4.0 * g.n * ld
+    peak, _ = load_peaks()
+    floor_ms = (cold / 6.3e12 + rest / (peak * 1e9)) * 1e3
+    return {"floor_ms": floor_ms, "achieved_ms": avg_launch_ms, "frac": floor_ms / avg_launch_ms,
+            "hub_share_of_gathers": hub_share, "cold_gather_GB": cold / 1e9,
+            "basis": "cold-row gathers at the measured 6.3 TB/s random-1600B-row DRAM rate + the other algorithmic "
+                     "bytes at the measured copy peak (DESIGN.md §6)"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -481,6 +506,7 @@ def main():
                                "step on the library stream), after the headline",
                 "traffic": load_traffic(cfg["name"]),
                 "traffic_source": "ncu --set full capture of this kernel at this config (profiles/spmm_traffic.json)",
+                "gather_floor": gather_floor(g, sp, world, per_launch_bytes, spmm_ms / spmm_n if spmm_n else None),
             },
             "phases_ms": phases,
             "cpu_baseline": cpu,
