@@ -108,7 +108,10 @@ def sigma_rel(s, sref) -> float:
 
 
 def gap_index(s_all, k, thresh=1e-2) -> int:
-    """k' = largest index <= k with relative gap (s_k' - s_k'+1)/s_k' >= thresh (reading O20)."""
+    """k' = largest index <= k with relative gap (s_k' - s_k'+1)/s_k' >= thresh (reading O20).
+    k = len(s_all) (l = rank: the whole spectrum) has no boundary: k' = k."""
+    if k >= len(s_all):
+        return k
     for kk in range(k, 0, -1):
         if (s_all[kk - 1] - s_all[kk]) / s_all[kk - 1] >= thresh:
             return kk
@@ -129,7 +132,8 @@ def check_isvd_arrays(Ug, S, Vg, oref, k, label):
     es = sigma_rel(S, so)
     su, sv = sin_theta(Ug, Uo), sin_theta(Vg, Vo)
     kp = gap_index(so_all, k)
-    msg = f"{label}: sigma {es:.2e} sinU {su:.2e} sinV {sv:.2e} gap_k {(so_all[k-1]-so_all[k])/so_all[k-1]:.2e} k'={kp}"
+    gap = (so_all[k - 1] - so_all[k]) / so_all[k - 1] if k < len(so_all) else float("inf")
+    msg = f"{label}: sigma {es:.2e} sinU {su:.2e} sinV {sv:.2e} gap_k {gap:.2e} k'={kp}"
     assert es <= SIG_TOL, msg
     if su > ANGLE_TOL or sv > ANGLE_TOL:
         # documented fallback (reading O20): near-degenerate boundary -> compare the top k' subspace
