@@ -32,6 +32,7 @@
 //     32 (w % 4) .. +31, column quarter w / 4) and release the accumulator.
 // Operand descriptors and the instruction descriptor follow the sm_100 UMMA bit layouts.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "umma.cuh"
@@ -302,6 +303,214 @@ __global__ void __launch_bounds__(kTcWsThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
+// ----------------------------------------------------------------------------------------------
+// Round 2: the same product with MN-major operands, no transposition.  The sm_100 smem descriptor
+// has a layout type for 32-bit MN-major operands, SWIZZLE_128B_BASE32B (encoding 1: 32-byte atoms
+// swizzled in a 128-byte span, Swizzle<2,5,2> on byte offsets), which TMA writes directly
+// (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).  profiles/umma_mn_probe2.cu: exact with LBO = stride of
+// the 32-column boxes and SBO = 512 B (4-row groups); the 16-byte-atom layouts the round-1 probe
+// tried return zeros.  So a row-major tile of Y *is* a UMMA operand of Y^T Y:
+//   * the producer TMA-loads, per 16-row step, ceil(128/32) boxes of A and ceil(N/32) boxes of B
+//     (32 columns x 16 rows each) into a ring slot; the raw fp32 values are the hi operands as
+//     loaded (the tensor core reads the top 19 bits: hi = x with the low 13 mantissa bits cleared,
+//     profiles/umma_mn_probe.cu variant 3);
+//   * 16 converter warps write lo = x - hi at the same offsets of the slot (an elementwise pass:
+//     the layout needs no index arithmetic), and, for a row-scaled A, the scaled hi in place
+//     (row k of a box is the 128-byte line k);
+//   * the MMA warp issues 2 k-steps x 3 MMAs per step, each k-step 8 rows = 1024 B further into
+//     every box;
+//   * chunked TMEM accumulation, draining and the fp32 partials are as in tc_atb_kernel.
+// Shared-memory traffic per step falls from ~150 KB (raw write, transposing read, hi + lo writes)
+// to the raw write, one read and one lo write (~68 KB at N = 208), below the MMAs' own time.
+template <int N>
+struct TcMnCfg {
+  static constexpr int kStep = 16;
+  static constexpr int kStepsPerChunk = kTcChunk / kStep;
+  static constexpr int kSlots = 4;
+  static constexpr int A_BOX = kTcM / 32, B_BOX = (N + 31) / 32;  // 32-column boxes
+  static constexpr int BOX_FL = 32 * kStep;                      // floats per box (16 rows x 128 B)
+  static constexpr int A_FL = A_BOX * BOX_FL, B_FL = B_BOX * BOX_FL;
+  static constexpr int SLOT_FL = 2 * A_FL + 2 * B_FL;            // A hi | A lo | B hi | B lo
+  static constexpr size_t smem_bytes() { return (size_t)kSlots * SLOT_FL * sizeof(float) + 1024; }
+};
+
+template <int N>
+__global__ void __launch_bounds__(kTcWsThreads, 1)
+    tc_atb_mn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const float* __restrict__ rs, int64_t rows, int ta, int tb, int symmetric, int64_t rows_per_cta,
+                     float* __restrict__ ws, int64_t ws_lda, int64_t ws_ld, const int* gate) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  using C = TcMnCfg<N>;
+  static_assert(N % 16 == 0 && N >= 32 && N <= 256, "UMMA N");
+  constexpr int KS = C::kStep;
+  constexpr uint32_t LBO = C::BOX_FL * 4, SBO = 512;        // bytes: box stride, 4-row group stride
+  constexpr int CT = kTcConvWarps * 32;
+  constexpr int A_V4 = C::A_FL / 4, ALL_V4 = (C::A_FL + C::B_FL) / 4;
+  constexpr int QTR = N / (kTcConvWarps / 4);
+  constexpr uint32_t kCols = 2 * N <= 256 ? 256 : 512;
+  static_assert(QTR % 4 == 0, "drain granularity");
+
+  extern __shared__ uint8_t smraw[];
+  float* const slot0 = reinterpret_cast<float*>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t raw_full[C::kSlots], conv_full[C::kSlots], slot_empty[C::kSlots];
+  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  int ti = 0, tj = 0;
+  {
+    int t = blockIdx.x;
+    for (int i = 0; i < ta; ++i)
+      for (int j = 0; j < tb; ++j) {
+        if (symmetric && (int64_t)i * kTcM > (int64_t)j * N + N - 1) continue;
+        if (t-- == 0) { ti = i; tj = j; }
+      }
+  }
+  const int a0 = ti * kTcM, b0 = tj * N;
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_cta;
+  const int64_t r_end = r_begin + rows_per_cta < rows ? r_begin + rows_per_cta : rows;
+  const int64_t nst = r_end > r_begin ? (r_end - r_begin + KS - 1) / KS : 0;
+  const int64_t nch = (nst + C::kStepsPerChunk - 1) / C::kStepsPerChunk;
+
+  if (tid == 0) {
+    for (int i = 0; i < C::kSlots; ++i) {
+      mbar_init(&raw_full[i], 1);
+      mbar_init(&conv_full[i], kTcConvWarps);
+      mbar_init(&slot_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kTcConvWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == kTcConvWarps) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int64_t st = 0; st < nst; ++st) {
+        const int s = (int)(st % C::kSlots);
+        if (st >= C::kSlots) mbar_wait(&slot_empty[s], (uint32_t)((st / C::kSlots - 1) & 1));
+        float* A = slot0 + s * C::SLOT_FL;
+        float* B = A + 2 * C::A_FL;
+        mbar_expect_tx(&raw_full[s], (uint32_t)(C::A_FL + C::B_FL) * 4);
+        const int r0 = (int)(r_begin + st * KS);
+#pragma unroll
+        for (int b = 0; b < C::A_BOX; ++b) tma_2d(A + b * C::BOX_FL, &tmA, a0 + 32 * b, r0, &raw_full[s]);
+#pragma unroll
+        for (int b = 0; b < C::B_BOX; ++b) tma_2d(B + b * C::BOX_FL, &tmB, b0 + 32 * b, r0, &raw_full[s]);
+      }
+    }
+  } else if (warp == kTcConvWarps + 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(kTcM, N) | (1u << 15) | (1u << 16);  // A and B MN-major
+      for (int64_t st = 0; st < nst; ++st) {
+        const int s = (int)(st % C::kSlots);
+        const int64_t ch = st / C::kStepsPerChunk;
+        const bool first = (st % C::kStepsPerChunk) == 0;
+        if (first && ch >= 2) mbar_wait(&acc_empty[ch & 1], (uint32_t)((ch / 2 - 1) & 1));
+        mbar_wait(&conv_full[s], (uint32_t)((st / C::kSlots) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(ch & 1) * N;
+        const uint32_t ah = smem_u32(slot0 + s * C::SLOT_FL), al = ah + C::A_FL * 4;
+        const uint32_t bh = ah + 2 * C::A_FL * 4, bl = bh + C::B_FL * 4;
+#pragma unroll
+        for (int k = 0; k < KS / 8; ++k) {
+          const uint32_t ko = (uint32_t)k * 8 * 128;  // 8 rows of 128 B into every box
+          const uint64_t dah = umma_desc(ah + ko, LBO, SBO, 1), dal = umma_desc(al + ko, LBO, SBO, 1);
+          const uint64_t dbh = umma_desc(bh + ko, LBO, SBO, 1), dbl = umma_desc(bl + ko, LBO, SBO, 1);
+          mma_tf32(d, dah, dbh, idesc, (first && k == 0) ? 0u : 1u);
+          mma_tf32(d, dah, dbl, idesc, 1u);
+          mma_tf32(d, dal, dbh, idesc, 1u);
+        }
+        umma_commit(&slot_empty[s]);
+        if ((st % C::kStepsPerChunk) == C::kStepsPerChunk - 1 || st == nst - 1) umma_commit(&acc_full[ch & 1]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- converters / drainers
+    float acc[QTR];
+#pragma unroll
+    for (int q = 0; q < QTR; ++q) acc[q] = 0.f;
+    const uint32_t lane_base = (uint32_t)(warp & 3) * 32;
+    const uint32_t col_q = (uint32_t)(warp >> 2) * QTR;
+    int64_t drained = 0;
+    auto drain = [&](int64_t c) {
+      mbar_wait(&acc_full[c & 1], (uint32_t)((c >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + (lane_base << 16) + (uint32_t)(c & 1) * N + col_q;
+#pragma unroll
+      for (int q0 = 0; q0 < QTR; q0 += 16) {
+        uint32_t r[16];
+#pragma unroll
+        for (int q = 0; q < 16; q += 4)
+          if (q0 + q < QTR)
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r[q]), "=r"(r[q + 1]), "=r"(r[q + 2]), "=r"(r[q + 3])
+                         : "r"(base + (uint32_t)(q0 + q)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (q0 + q < QTR) acc[q0 + q] += __uint_as_float(r[q]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[c & 1]);
+    };
+    for (int64_t st = 0; st < nst; ++st) {
+      const int s = (int)(st % C::kSlots);
+      if ((st % C::kStepsPerChunk) == 1 && st > C::kStepsPerChunk) drain(drained++);
+      // row scales of this step for the A vectors this thread converts (row k of a box = line k)
+      mbar_wait(&raw_full[s], (uint32_t)((st / C::kSlots) & 1));
+      float* const A = slot0 + s * C::SLOT_FL;
+      const int64_t k0 = r_begin + st * KS;
+#pragma unroll
+      for (int i = 0; i < (ALL_V4 + CT - 1) / CT; ++i) {
+        const int f = tid + i * CT;  // float4 index over [A raw | B raw]
+        if (f < A_V4) {
+          float4 v = reinterpret_cast<const float4*>(A)[f];
+          if (rs) {
+            const int k = (f % (C::BOX_FL / 4)) >> 3;  // 8 float4 per 128-byte line
+            const float sc = k0 + k < r_end ? __ldg(rs + k0 + k) : 0.f;
+            v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+            reinterpret_cast<float4*>(A)[f] = v;
+          }
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          reinterpret_cast<float4*>(A + C::A_FL)[f] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        } else if (f < ALL_V4) {
+          const int g = f - A_V4;
+          float* const B = A + 2 * C::A_FL;
+          const float4 v = reinterpret_cast<const float4*>(B)[g];
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          reinterpret_cast<float4*>(B + C::B_FL)[g] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv_full[s]);
+    }
+    while (drained < nch) drain(drained++);
+    const int64_t row = a0 + lane_base + lane;
+    float* w = ws + ((int64_t)blockIdx.y * ws_lda + row) * ws_ld + b0 + col_q;
+#pragma unroll
+    for (int q = 0; q < QTR; q += 4)
+      *reinterpret_cast<float4*>(w + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
 constexpr int kTcNs[] = {128, 160, 208, 256};  // instantiated tile widths
 
 struct TcTiling {
@@ -345,6 +554,27 @@ cudaError_t tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t 
                         int64_t ldb, int64_t Kb, int64_t rows, bool symmetric, float* ws, int64_t ws_lda,
                         int64_t ws_ld, const int* gate, cudaStream_t st) {
   CUtensorMap tmA, tmB;
+  dim3 grid((unsigned)t.tiles, (unsigned)t.parts);
+  static const bool mn = [] {  // ISVD_TC_MN=0: the round-1 transposing kernel (A/B evidence)
+    const char* e = getenv("ISVD_TC_MN");
+    return !(e && atoi(e) == 0);
+  }();
+  if (mn) {
+    using C = TcMnCfg<N>;
+    if (!make_map(&tmA, A, rows, Ka, lda, 32, C::kStep, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+        !make_map(&tmB, B, rows, Kb, ldb, 32, C::kStep, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return cudaErrorInvalidValue;
+    static bool attr_mn = false;
+    if (!attr_mn) {
+      cudaFuncSetAttribute(tc_atb_mn_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes());
+      attr_mn = true;
+    }
+    ++g_launches;
+    tc_atb_mn_kernel<N><<<grid, kTcWsThreads, C::smem_bytes(), st>>>(tmA, tmB, rs, rows, t.ta_run, t.tb,
+                                                                      symmetric ? 1 : 0, t.rows_per_cta, ws, ws_lda,
+                                                                      ws_ld, gate);
+    return cudaGetLastError();
+  }
   if (!make_map(&tmA, A, rows, Ka, lda, kTcM, TcCfg<N>::kStep, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_map(&tmB, B, rows, Kb, ldb, N, TcCfg<N>::kStep, CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
@@ -354,7 +584,6 @@ cudaError_t tc_launch_n(const TcTiling& t, const float* A, int64_t lda, int64_t 
     cudaFuncSetAttribute(tc_atb_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid((unsigned)t.tiles, (unsigned)t.parts);
   ++g_launches;
   tc_atb_kernel<N><<<grid, kTcWsThreads, smem, st>>>(tmA, tmB, Ka, rs, Kb, rows, t.ta_run, t.tb, symmetric ? 1 : 0,
                                                    t.rows_per_cta, ws, ws_lda, ws_ld, gate);
