@@ -22,12 +22,17 @@
 // bytes).  The graph is then relabelled by degree (capi.cpp) so the hub rows —
 // 2 % of the nodes take 41 % of the gathers — are one contiguous prefix that an
 // L2 persisting window keeps resident (profiles/r01_spmm_sweep.md).
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
 
 namespace isvd {
 namespace {
+
+// ISVD_SPMM_VARIANT default: 1 = register (LDG) gather with the masked last batch, 2 = shared-memory
+// (bulk-copy) staged gather
+constexpr int kSpmmDefaultVariant = 1;
 
 struct Acc4 { double x, y, z, w; };
 
@@ -201,6 +206,185 @@ __global__ void __launch_bounds__(1024) spmm_fixup_kernel(SpmmArgs a, const int3
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Shared-memory / TMA-staged gather (north_star: "a shared-memory/TMA-staged gather"; round 2).
+// One CTA = one producer warp + one consumer team of w/4 threads (rounded up to warps).  The
+// producer walks the CTA's segments (the same strided assignment as spmm_kernel with one team per
+// CTA) and, per neighbour j, issues one bulk copy (cp.async.bulk, 16-byte granules, the whole row
+// slice Y[j, 0:w) = 1600 B at w = 400) into the next slot of an S-slot shared-memory ring, completing
+// on that slot's "full" mbarrier; a slot is reused once every consumer warp has arrived on its
+// "empty" mbarrier.  Lane e of the producer handles neighbour e of a 32-neighbour group, so up to 32
+// copies are issued per warp instruction and the ring (S >= 32 rows per CTA, several CTAs per SM)
+// keeps 100-200 KB of gathers in flight per SM without any register cost, across segment and row
+// boundaries (no dependent index -> row bubble at the start of a row, the LDG kernel's stall).
+// The consumers read each staged row once from shared memory (thread t: columns [4t, 4t+4), one
+// conflict-free LDS.128) and sum exactly as spmm_kernel does -- the same fp32 batches of 8 (missing
+// neighbours of the last batch as zeros), the same fp64 accumulation, the same epilogue -- so the
+// two kernels are bitwise identical (tests/test_parity_gpu.py::test_spmm_bulk_equals_ldg).
+// Optional per-copy L2 policy (hint_mode 1): hub rows (j < hub_rows, the persisting prefix of a
+// degree-relabelled gather source) evict_last, the others evict_first.
+ISVD_DEVICE void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+ISVD_DEVICE void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+ISVD_DEVICE uint32_t sm32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+ISVD_DEVICE void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm32(b)), "r"(n));
+}
+ISVD_DEVICE void bar_wait(const uint64_t* b, uint32_t parity) {
+  for (uint32_t it = 0;; ++it) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t"
+        "}\n"
+        : "=r"(done)
+        : "r"(sm32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 28)) __trap();  // a copy that never lands fails the launch instead of hanging the GPU
+  }
+}
+ISVD_DEVICE void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm32(b)) : "memory");
+}
+ISVD_DEVICE void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm32(b)), "r"(bytes) : "memory");
+}
+
+constexpr int kBulkMaxThreads = 32 + 256;  // producer warp + up to 256 consumers (w <= 1024)
+
+template <bool kW>
+__global__ void __launch_bounds__(kBulkMaxThreads) spmm_bulk_kernel(
+    SpmmArgs a, const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_beg,
+    const int32_t* __restrict__ seg_len, const int32_t* __restrict__ seg_slot, int64_t n_seg, float* __restrict__ partial,
+    int log_slots, int64_t hub_rows, int hint_mode) {
+  extern __shared__ __align__(128) uint8_t bulk_sm[];
+  const int S = 1 << log_slots;
+  const uint32_t row_bytes = (uint32_t)a.wpad * 4u;
+  uint8_t* const ring = bulk_sm;
+  uint64_t* const full = reinterpret_cast<uint64_t*>(bulk_sm + (size_t)S * row_bytes);
+  uint64_t* const empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int TS = (int)(a.wpad >> 2);
+  const int CW = (TS + 31) >> 5;  // consumer warps
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      bar_init(&full[i], 1);
+      bar_init(&empty[i], (uint32_t)CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t G = gridDim.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    uint64_t pol_hub = 0, pol_cold = 0;
+    if (hint_mode == 1) {
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_hub));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_cold));
+    }
+    const uint32_t ring_s = sm32(ring), full_s = sm32(full);
+    uint32_t ctr = 0;
+    for (int64_t s0 = blockIdx.x; s0 < n_seg; s0 += 32 * G) {
+      const int64_t s = s0 + (int64_t)lane * G;
+      int64_t b = 0;
+      int len = 0;
+      if (s < n_seg) {
+        b = seg_beg[s];
+        len = seg_len[s];
+      }
+      const int64_t left = (n_seg - s0 + G - 1) / G;
+      const int nq = left < 32 ? (int)left : 32;
+      for (int q = 0; q < nq; ++q) {
+        const int64_t bq = __shfl_sync(0xffffffffu, b, q);
+        const int lq = __shfl_sync(0xffffffffu, len, q);
+        for (int e0 = 0; e0 < lq; e0 += 32) {
+          const int e = e0 + lane;
+          if (e < lq) {
+            const int j = __ldg(a.col_idx + bq + e);
+            ISVD_ASSERT(j >= 0 && j < a.n_src);
+            const uint32_t c = ctr + (uint32_t)e;
+            const uint32_t slot = c & (uint32_t)(S - 1);
+            bar_wait(&empty[slot], ((c >> log_slots) & 1u) ^ 1u);
+            bar_expect_tx(&full[slot], row_bytes);
+            const float* src = a.Y + (int64_t)j * a.ldy;
+            const uint32_t dst = ring_s + slot * row_bytes, bar = full_s + slot * 8u;
+            if (hint_mode == 1) bulk_g2s_hint(dst, src, row_bytes, bar, j < hub_rows ? pol_hub : pol_cold);
+            else bulk_g2s(dst, src, row_bytes, bar);
+          }
+        }
+        ctr += (uint32_t)lq;
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------------- consumers
+  const int c4 = tid - 32;
+  const bool active = c4 < TS;
+  uint32_t ctr = 0;
+  int64_t s = blockIdx.x;
+  int64_t row_n = 0, b_n = 0;
+  int len_n = 0, slot_n = -1;
+  if (s < n_seg) {
+    row_n = seg_row[s];
+    b_n = seg_beg[s];
+    len_n = seg_len[s];
+    slot_n = seg_slot[s];
+  }
+  for (; s < n_seg; s += G) {
+    const int64_t row = row_n, b = b_n;
+    const int len = len_n, pslot = slot_n;
+    if (s + G < n_seg) {  // the next segment's descriptor, in flight during this one
+      row_n = seg_row[s + G];
+      b_n = seg_beg[s + G];
+      len_n = seg_len[s + G];
+      slot_n = seg_slot[s + G];
+    }
+    ISVD_ASSERT(row >= 0 && len >= 0 && len <= kSegEdges);
+    Acc4 acc{0.0, 0.0, 0.0, 0.0};
+    for (int e = 0; e < len; e += 8) {
+      const int n8 = len - e < 8 ? len - e : 8;
+      float4 v[8];
+      float wv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        wv[u] = 0.f;
+        if (u < n8) {
+          const uint32_t c = ctr + (uint32_t)(e + u);
+          const uint32_t slot = c & (uint32_t)(S - 1);
+          bar_wait(&full[slot], (c >> log_slots) & 1u);
+          if (active) v[u] = *reinterpret_cast<const float4*>(ring + (size_t)slot * row_bytes + 16 * c4);
+          if constexpr (kW) wv[u] = __ldg(a.val + b + e + u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int u = 0; u < n8; ++u) bar_arrive(&empty[(ctr + (uint32_t)(e + u)) & (uint32_t)(S - 1)]);
+      acc_add(acc, sum_batch<kW>(v, wv));
+    }
+    ctr += (uint32_t)len;
+    if (!active) continue;
+    if (pslot < 0) {
+      spmm_epilogue(a, row, 4 * (int64_t)c4, acc);
+    } else {
+      st4(partial + (int64_t)pslot * a.wpad + 4 * (int64_t)c4,
+          make_float4((float)acc.x, (float)acc.y, (float)acc.z, (float)acc.w));
+    }
+  }
+}
+
 void team_shape(int64_t wpad, int* teams, int* threads) {
   int TS = (int)(wpad / 4);
   int R = TS >= 512 ? 1 : 512 / TS;
@@ -301,7 +485,48 @@ cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_part
     cfg.numAttrs = nattr;
     ++g_launches;
     const char* ve = getenv("ISVD_SPMM_VARIANT");  // 0: sequential tail (A/B switch, read per launch)
-    const bool masked = ve ? atoi(ve) != 0 : true;
+    const int variant = ve ? atoi(ve) : kSpmmDefaultVariant;
+    const bool masked = variant != 0;
+    if (variant == 2 && a.wpad <= 1024) {
+      // shared-memory / TMA-staged gather (spmm_bulk_kernel): S-slot ring per CTA
+      const char* se = getenv("ISVD_SPMM_BULK_SLOTS");
+      int S = se ? atoi(se) : 32;
+      int log_s = 5;
+      while ((1 << log_s) < S) ++log_s;
+      const size_t row_bytes = (size_t)a.wpad * 4;
+      while (log_s > 5 && ((size_t)1 << log_s) * (row_bytes + 16) > 200 * 1024) --log_s;
+      const size_t smem = ((size_t)1 << log_s) * (row_bytes + 16);
+      if (smem <= 227 * 1024) {
+        const int bthreads = 32 + (int)round_up(a.wpad / 4, 32);
+        void (*kb)(SpmmArgs, const int32_t*, const int64_t*, const int32_t*, const int32_t*, int64_t, float*, int,
+                   int64_t, int) = a.val ? spmm_bulk_kernel<true> : spmm_bulk_kernel<false>;
+        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kb, bthreads, smem);
+        if (per_sm < 1) per_sm = 1;
+        int64_t nb = std::min<int64_t>(plan.n_seg, (int64_t)num_sms * per_sm);
+        if (nb < 1) nb = 1;
+        const char* he = getenv("ISVD_SPMM_BULK_HINT");
+        const int hint = he ? atoi(he) : 0;
+        const int64_t hub_rows = persist_bytes ? (int64_t)(persist_bytes / ((size_t)a0.ldy * 4)) : 0;
+        cfg.gridDim = dim3((unsigned)nb);
+        cfg.blockDim = dim3((unsigned)bthreads);
+        cfg.dynamicSmemBytes = smem;
+        ++g_launches;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kb, a, (const int32_t*)plan.seg_row, (const int64_t*)plan.seg_beg,
+                                           (const int32_t*)plan.seg_len, (const int32_t*)plan.seg_slot, plan.n_seg,
+                                           ws_partial, log_s, hub_rows, hint);
+        if (e != cudaSuccess) return e;
+        if (plan.n_split_rows > 0) {
+          int64_t fb = ceil_div(plan.n_split_rows, teams);
+          if (fb > cap) fb = cap;
+          ++g_launches;
+          spmm_fixup_kernel<<<(int)fb, threads, 0, st>>>(a, plan.split_row, plan.split_slot0, plan.split_nslot,
+                                                         plan.n_split_rows, teams, ws_partial);
+        }
+        continue;
+      }
+    }
     void (*kern)(SpmmArgs, const int32_t*, const int64_t*, const int32_t*, const int32_t*, int64_t, int, float*) =
         a.val ? (masked ? spmm_kernel<true, true> : spmm_kernel<true, false>)
               : (masked ? spmm_kernel<false, true> : spmm_kernel<false, false>);

@@ -797,3 +797,63 @@ def test_single_node_graph(ctx):
     assert abs(res.S[0] - np.sqrt(3 * 25.0)) <= 1e-5 * np.sqrt(75.0)
     nc.close()
     graph.close()
+
+
+# ------------------------------------- SpMM variants: register (LDG) gather vs shared-memory staged gather
+
+
+def _with_spmm_variant(v, fn):
+    import os
+
+    old = os.environ.get("ISVD_SPMM_VARIANT")
+    os.environ["ISVD_SPMM_VARIANT"] = str(v)  # read per launch by launch_spmm
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+        return out
+    finally:
+        if old is None:
+            del os.environ["ISVD_SPMM_VARIANT"]
+        else:
+            os.environ["ISVD_SPMM_VARIANT"] = old
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 3, 4])
+def test_spmm_bulk_equals_ldg(ctx, i):
+    """The shared-memory / bulk-copy staged gather (ISVD_SPMM_VARIANT=2, spmm_bulk_kernel) forms the
+    same fp32 batches of 8 and the same fp64 sums as the register gather (variant 1), so M.Q and
+    M^T.Q are bitwise equal on every config (hub-split segments, relabelled config 4, ragged widths),
+    and -- transitively -- in parity with the oracle wherever variant 1 is."""
+    op, _, cfg, sp = _op(ctx, i)
+    gen = torch.Generator(device="cuda").manual_seed(1000 + i)
+    G = torch.randn(op.c_rows(), sp["l"], device="cuda", generator=gen)
+    H = torch.randn(op.graph.n_local, sp["l"], device="cuda", generator=gen)
+    for f in (lambda: op.matmul(G), lambda: op.matmul_T(H)):
+        a = _with_spmm_variant(1, f)
+        b = _with_spmm_variant(2, f)
+        assert torch.equal(a, b), float((a - b).abs().max())
+
+
+def test_spmm_bulk_equals_ldg_weighted_and_split(ctx):
+    """Bitwise equality of the two gathers on a weighted graph (config 2 with edge weights, the
+    kW kernels) and on a star whose hub row is split into several segments (fixup path)."""
+    import paper_2111_06312_b200 as isvd_mod
+
+    cfg, g, X, sp = config_inputs(2)
+    vals = _edge_weights(g, 9)
+    graph = isvd_mod.Graph(ctx, g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col_idx).cuda(),
+                           values=torch.from_numpy(vals).cuda())
+    op = isvd_mod.NC(graph, torch.from_numpy(np.ascontiguousarray(X)).cuda(), sp["L"])
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    G = torch.randn(op.shape[1], sp["l"], device="cuda", generator=gen)
+    H = torch.randn(g.n, sp["l"], device="cuda", generator=gen)
+    for f in (lambda: op.matmul(G), lambda: op.matmul_T(H)):
+        assert torch.equal(_with_spmm_variant(1, f), _with_spmm_variant(2, f))
+    op.close()
+    graph.close()
+    n = 3001
+    op2, _, rng = _tiny_case(ctx, n, [(0, j) for j in range(1, n)] + [(j, j + 1) for j in range(1, n - 1)],
+                             C=3, lam=1 / n)
+    Q = torch.from_numpy(rng.standard_normal((n, 12)).astype(np.float32)).cuda()
+    for f in (lambda: op2.matmul(Q), lambda: op2.matmul_T(Q)):
+        assert torch.equal(_with_spmm_variant(1, f), _with_spmm_variant(2, f))
