@@ -431,6 +431,38 @@ def main():
                     "n x c matrix (SURVEY 8(f) f3, comparison only; north_star: M never materialised)"}
         opm.close()
         del Mx
+    # ---- variant: NE with A held dense (ISVD_DENSE_A=1, n <= 32768): every SpMM step
+    # as a tcgen05 3xTF32 product A Y plus the same epilogue.  Comparison only (same flush policy).
+    if not args.no_variants and cfg["op"] == "NE" and world == 1 and cfg["n"] <= 32768:
+        os.environ["ISVD_DENSE_A"] = "1"
+        try:
+            gd = isvd.Graph(ctx, g.n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+        finally:
+            del os.environ["ISVD_DENSE_A"]
+        opd = isvd.NE(gd, sp["weights"], sp["lambda_ones"])
+        for _ in range(args.warmup):
+            opd.svd(sp["k"], p, sp["q"], sp["seed"])
+        torch.cuda.synchronize()
+        junk = torch.empty(128 * 2 ** 20, dtype=torch.float32, device="cuda") if flush else None
+        tot = 0.0
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                if junk is not None:
+                    junk.fill_(1.0)
+                e0.record(stream)
+                opd.svd(sp["k"], p, sp["q"], sp["seed"])
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tot += e0.elapsed_time(e1)
+        rd = opd.svd(sp["k"], p, sp["q"], sp["seed"], profile=True)
+        variants["dense_A"] = {
+            "value": tot / args.steps / 1e3, "unit": "s",
+            "spmm_step_ms": rd.ms_spmm / max(rd.spmm_steps, 1),
+            "what": "NE with A held dense (n x n fp32, formed at graph creation) and every SpMM step run as a "
+                    "tcgen05 3xTF32 product A Y + the same fp64 epilogue (SURVEY 8(f) f3, comparison only)"}
+        del junk
+        opd.close()
+        gd.close()
     op.close()
     graph.close()
 

@@ -141,6 +141,10 @@ struct isvd_graph_s {
   float* s2 = nullptr;         // (d+1)^-1
   float* rs = nullptr;         // (d+1)^1/2
   int32_t* new2old = nullptr;  // relabelled graphs: caller row of internal row i (device); else null
+  // SURVEY 8(f) f3 comparison (ISVD_DENSE_A=1, single rank, n <= 32768): A as a dense fp32 n x ld_dense
+  // matrix; every SpMM step of this graph then runs as a tcgen05 3xTF32 product A^T Y = A Y (A = A^T)
+  float* dense = nullptr;
+  int64_t ld_dense = 0;
   SpmmPlan plan;
   std::vector<void*> allocs;
   std::atomic<int> refs{0};
@@ -184,6 +188,7 @@ struct isvd_op_s {
   int64_t ws_wpad = 0;
   std::vector<void*> ws_allocs;
   float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
+  float* dense_ws = nullptr;  // f3 dense-A products: fp32 partial tiles of launch_tc_atb
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
   float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
   float* adjbuf = nullptr;  // NE with lambda_adj != 0: lambda_adj A Q (internal row order)
@@ -501,6 +506,10 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
     atb = std::max(atb, (tc_atb_ws_floats(g->n_local, op->ylr, wpad, false, ctx->num_sms) + 1) / 2);
   }
   op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
+  op->dense_ws = g->dense ? (float*)dmalloc(ctx, sizeof(float) * (size_t)tc_atb_ws_floats(g->n, g->n, wpad, false,
+                                                                                            ctx->num_sms),
+                                            op->ws_allocs)
+                          : nullptr;
   op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
                               op->ws_allocs);
   op->adjbuf = op->lambda_adj != 0.0
@@ -619,6 +628,13 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
     re.col_idx = g->ci_rem; re.val = g->val_rem;
     re.pre = op->loc_partial; re.ldpre = a.wpad;
     CK(launch_spmm(g->plan_rem, re, op->partial, ctx->num_sms, ctx->stream, 0, col_block));
+  } else if (g->dense && !a.pre) {
+    // f3 comparison: acc = A Y as a tensor-core product over the dense adjacency (A symmetric, so
+    // A Y = A^T Y: the Gram kernel's row-contraction form), then the same epilogue
+    int64_t ws_lda = 0, ws_ld = 0, parts = 0;
+    CK(launch_tc_atb(g->dense, g->ld_dense, g->n, nullptr, a.Y, a.ldy, a.wpad, g->n, false, op->dense_ws, &ws_lda,
+                     &ws_ld, &parts, ctx->num_sms, nullptr, ctx->stream));
+    CK(launch_spmm_dense_epilogue(op->dense_ws, parts, ws_lda, ws_ld, a, g->n_local, ctx->num_sms, ctx->stream));
   } else {
     join_gather(ctx);
     CK(launch_spmm(g->plan, a, op->partial, ctx->num_sms, ctx->stream, persist, col_block));
@@ -1467,6 +1483,12 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->rs = (float*)dmalloc(ctx, nb, g->allocs);
     CK(launch_scales(g->row_ptr, g->val, n_local, g->inv_deg, g->s, g->s2, g->rs, ctx->stream));
     phase("scales");
+    if (env_flag("ISVD_DENSE_A", false) && !ctx->dist && n_local == n_global && n_global <= 32768 && !g->new2old &&
+        n_global >= 1) {
+      g->ld_dense = round_up(n_global, 4);
+      g->dense = (float*)dmalloc(ctx, sizeof(float) * (size_t)n_global * g->ld_dense, g->allocs);
+      CK(launch_dense_adjacency(g->row_ptr, g->col_idx, g->val, n_global, g->ld_dense, g->dense, ctx->stream));
+    }
     // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
     // split, their partial sums combined by the fixup pass in segment order (graph_build.cu)
     build_plan(ctx, g->row_ptr, n_local, g->plan, g->allocs, temp, temp_bytes);

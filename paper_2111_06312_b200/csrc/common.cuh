@@ -161,6 +161,14 @@ cudaError_t launch_split_count(const int64_t* rp, const int32_t* ci, int64_t n, 
 cudaError_t launch_split_fill(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t lo, int64_t hi,
                               const int64_t* rp_loc, const int64_t* rp_rem, int32_t* ci_loc, float* val_loc,
                               int32_t* ci_rem, float* val_rem, cudaStream_t st);
+// Dense adjacency (SURVEY 8(f) f3 comparison): out (n x ld fp32, zero-filled here) gets A_ij at (i, j).
+cudaError_t launch_dense_adjacency(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t ld,
+                                   float* out, cudaStream_t st);
+// Epilogue of the dense-A product (f3): acc = sum over `parts` fp32 partial tiles ws32[p][row][col]
+// (ws_lda rows, ws_ld columns per part; summed in fp64 in part order), then the SpMM epilogue of `a`
+// (self term, scales, Horner term, rank-1 correction, out_map) for rows < n_local.
+cudaError_t launch_spmm_dense_epilogue(const float* ws32, int64_t parts, int64_t ws_lda, int64_t ws_ld,
+                                       const SpmmArgs& a, int64_t n_local, int num_sms, cudaStream_t st);
 cudaError_t launch_exclusive_scan64(const int64_t* in, int64_t* out, int64_t n1, void* temp, size_t temp_bytes,
                                     cudaStream_t st);
 // `persist_bytes` > 0: the first persist_bytes of Y (the hub rows of a degree-relabelled

@@ -200,6 +200,28 @@ cudaError_t launch_scales(const int64_t* rp, const float* val, int64_t n, float*
   return cudaGetLastError();
 }
 
+namespace {
+// one warp per row: out[row, col_idx[e]] += (val ? val[e] : 1)  (duplicates sum, as in the CSR)
+__global__ void dense_adj_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const float* __restrict__ val, int64_t n, int64_t ld, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5)
+    for (int64_t e = rp[r] + lane; e < rp[r + 1]; e += 32) atomicAdd(out + r * ld + ci[e], val ? val[e] : 1.f);
+}
+}  // namespace
+
+cudaError_t launch_dense_adjacency(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t ld,
+                                   float* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float) * (size_t)n * ld, st);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), 148 * 16);
+  ++g_launches;
+  dense_adj_kernel<<<(unsigned)blocks, 256, 0, st>>>(rp, ci, val, n, ld, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_plan_count(const int64_t* rp, int64_t n, int64_t* nseg, int32_t* nsplit, int32_t* nslot,
                               int64_t* seg_off, int32_t* split_off, int32_t* slot_off, void* temp, size_t temp_bytes,
                               cudaStream_t st) {

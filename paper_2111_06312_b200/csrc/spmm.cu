@@ -429,6 +429,29 @@ cudaError_t launch_relabel_csr(const int64_t* rp_old, const int32_t* ci_old, con
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void spmm_dense_epilogue_kernel(const float* __restrict__ ws32, int64_t parts, int64_t ws_lda, int64_t ws_ld,
+                                           SpmmArgs a, int64_t n_local) {
+  const int64_t c4n = a.wpad >> 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_local * c4n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / c4n, col = 4 * (t - row * c4n);
+    Acc4 acc{0.0, 0.0, 0.0, 0.0};
+    for (int64_t p = 0; p < parts; ++p) acc_add(acc, ldg4(ws32 + (p * ws_lda + row) * ws_ld + col));
+    spmm_epilogue(a, row, col, acc);
+  }
+}
+}  // namespace
+
+cudaError_t launch_spmm_dense_epilogue(const float* ws32, int64_t parts, int64_t ws_lda, int64_t ws_ld,
+                                       const SpmmArgs& a, int64_t n_local, int num_sms, cudaStream_t st) {
+  if (n_local <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n_local * (a.wpad >> 2), 256), (int64_t)num_sms * 8);
+  ++g_launches;
+  spmm_dense_epilogue_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws32, parts, ws_lda, ws_ld, a, n_local);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmm(const SpmmPlan& plan, const SpmmArgs& a0, float* ws_partial, int num_sms, cudaStream_t st,
                         size_t persist_bytes, int64_t col_block) {
   if (plan.n_local == 0) return cudaSuccess;
