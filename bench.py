@@ -317,8 +317,14 @@ def main():
     op, graph = make_op(True)
     torch.cuda.synchronize()
 
+    # outputs allocated once, outside the timed region (a fresh torch.zeros per call would put a
+    # cudaMalloc and a fill of U -- 2.5 GB at config 4 -- inside every timed step)
+    kk4 = (sp["k"] + 3) // 4 * 4
+    out_uv = (torch.zeros(max(op.r_rows(), 1), kk4, dtype=torch.float32, device="cuda"),
+              torch.zeros(max(op.c_rows(), 1), kk4, dtype=torch.float32, device="cuda"))
+
     def step(profile=False):
-        return op.svd(sp["k"], p, sp["q"], sp["seed"], profile=profile)
+        return op.svd(sp["k"], p, sp["q"], sp["seed"], profile=profile, out=out_uv)
 
     # headline: the default product path (the solver captured once as a CUDA graph and replayed)
     for _ in range(args.warmup):
@@ -346,14 +352,15 @@ def main():
             for a, b in evs:
                 junk.fill_(1.0)
                 a.record(stream)
-                results.append(step())
+                r_ = step()
                 b.record(stream)
+                results.append(r_.kernel_launches)
         torch.cuda.synchronize()
         step_ms = [a.elapsed_time(b) for a, b in evs]
         del junk
     else:
         e0.record(stream)
-        results = [step() for _ in range(args.steps)]
+        results = [step().kernel_launches for _ in range(args.steps)]
         e1.record(stream)
         torch.cuda.synchronize()
         step_ms = None
@@ -365,7 +372,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    launches = sum(r.kernel_launches for r in results)
+    launches = sum(results)
 
     # roofline pass (separate, after the headline): the same isvd run eagerly with every SpMM step
     # bracketed by CUDA events on the library's stream (ISVD_SVD_PROFILE) and per-phase times
@@ -431,38 +438,42 @@ def main():
                     "n x c matrix (SURVEY 8(f) f3, comparison only; north_star: M never materialised)"}
         opm.close()
         del Mx
-    # ---- variant: NE with A held dense (ISVD_DENSE_A=1, n <= 32768): every SpMM step
-    # as a tcgen05 3xTF32 product A Y plus the same epilogue.  Comparison only (same flush policy).
+    # ---- variants: NE with A held dense (n <= 32768), every SpMM step on tensor cores
+    # plus the same fp64 epilogue: the exact INT8 product (ISVD_DENSE_A=1) and 3xTF32 (=2).  Comparison
+    # only (same flush policy as the headline).
     if not args.no_variants and cfg["op"] == "NE" and world == 1 and cfg["n"] <= 32768:
-        os.environ["ISVD_DENSE_A"] = "1"
-        try:
-            gd = isvd.Graph(ctx, g.n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
-        finally:
-            del os.environ["ISVD_DENSE_A"]
-        opd = isvd.NE(gd, sp["weights"], sp["lambda_ones"])
-        for _ in range(args.warmup):
-            opd.svd(sp["k"], p, sp["q"], sp["seed"])
-        torch.cuda.synchronize()
-        junk = torch.empty(128 * 2 ** 20, dtype=torch.float32, device="cuda") if flush else None
-        tot = 0.0
-        with torch.cuda.stream(stream):
-            for _ in range(args.steps):
-                if junk is not None:
-                    junk.fill_(1.0)
-                e0.record(stream)
+        for dmode, dname, what in (
+                ("1", "dense_A_i8", "exact INT8 tensor-core product of the binary A with 3-byte fixed-point slices "
+                                    "of the gather source (dense_i8.cu)"),
+                ("2", "dense_A_tf32", "tcgen05 3xTF32 row contraction A^T Y (gram_tc.cu)")):
+            os.environ["ISVD_DENSE_A"] = dmode
+            try:
+                gd = isvd.Graph(ctx, g.n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+            finally:
+                del os.environ["ISVD_DENSE_A"]
+            opd = isvd.NE(gd, sp["weights"], sp["lambda_ones"])
+            for _ in range(args.warmup):
                 opd.svd(sp["k"], p, sp["q"], sp["seed"])
-                e1.record(stream)
-                torch.cuda.synchronize()
-                tot += e0.elapsed_time(e1)
-        rd = opd.svd(sp["k"], p, sp["q"], sp["seed"], profile=True)
-        variants["dense_A"] = {
-            "value": tot / args.steps / 1e3, "unit": "s",
-            "spmm_step_ms": rd.ms_spmm / max(rd.spmm_steps, 1),
-            "what": "NE with A held dense (n x n fp32, formed at graph creation) and every SpMM step run as a "
-                    "tcgen05 3xTF32 product A Y + the same fp64 epilogue (SURVEY 8(f) f3, comparison only)"}
-        del junk
-        opd.close()
-        gd.close()
+            torch.cuda.synchronize()
+            junk = torch.empty(128 * 2 ** 20, dtype=torch.float32, device="cuda") if flush else None
+            tot = 0.0
+            with torch.cuda.stream(stream):
+                for _ in range(args.steps):
+                    if junk is not None:
+                        junk.fill_(1.0)
+                    e0.record(stream)
+                    opd.svd(sp["k"], p, sp["q"], sp["seed"])
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    tot += e0.elapsed_time(e1)
+            rd = opd.svd(sp["k"], p, sp["q"], sp["seed"], profile=True)
+            variants[dname] = {
+                "value": tot / args.steps / 1e3, "unit": "s", "spmm_step_ms": rd.ms_spmm / max(rd.spmm_steps, 1),
+                "what": "NE with A held dense (formed at graph creation), every SpMM step as the " + what +
+                        " + the same fp64 epilogue (SURVEY 8(f) f3, comparison only)"}
+            del junk
+            opd.close()
+            gd.close()
     op.close()
     graph.close()
 
@@ -527,6 +538,7 @@ def main():
                        else "inputs larger than L2 (no flush)"),
                 "accumulate": "fp32 storage, fp64 accumulation",
             },
+            "step_ms": [round(x, 3) for x in step_ms] if step_ms else None,
             "roofline": {
                 "bound": "hbm", "kernel": "spmm_kernel (+fixup): fused CSR SpMM step",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -547,8 +559,8 @@ def main():
                     "graph_op_create_s": statistics.median(e2e_create) if e2e_create else None},
             "gpu_launches": launches,
             "variants": variants,
-            "solver": {"jacobi_sweeps": results[-1].jacobi_sweeps, "chol_fallbacks": results[-1].chol_fallbacks,
-                       "launches_per_isvd": results[-1].kernel_launches},
+            "solver": {"jacobi_sweeps": prof[-1].jacobi_sweeps, "chol_fallbacks": prof[-1].chol_fallbacks,
+                       "launches_per_isvd": results[-1]},
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

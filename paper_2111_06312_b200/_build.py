@@ -27,6 +27,7 @@ SOURCES = [
     ("dense.cu", []),
     ("gram_tc.cu", []),
     ("gemm_tc.cu", []),
+    ("dense_i8.cu", []),
     ("graph_build.cu", []),
     ("smallmat.cu", []),
     ("capi.cpp", []),

@@ -145,6 +145,8 @@ struct isvd_graph_s {
   // matrix; every SpMM step of this graph then runs as a tcgen05 3xTF32 product A^T Y = A Y (A = A^T)
   float* dense = nullptr;
   int64_t ld_dense = 0;
+  uint8_t* dense_u8 = nullptr;  // unweighted: A as bytes for the exact INT8 tensor-core product (dense_i8.cu)
+  int64_t ld_u8 = 0;
   SpmmPlan plan;
   std::vector<void*> allocs;
   std::atomic<int> refs{0};
@@ -189,6 +191,8 @@ struct isvd_op_s {
   std::vector<void*> ws_allocs;
   float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
   float* dense_ws = nullptr;  // f3 dense-A products: fp32 partial tiles of launch_tc_atb
+  void* i8_ws = nullptr;      // f3 exact INT8 dense products: fp64 integer partials + column maxima
+  uint8_t* i8_q = nullptr;    // ... and the byte slices of the fixed-point gather source
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
   float* bt_ws = nullptr;  // split B operand of the tensor-core GEMM
   float* adjbuf = nullptr;  // NE with lambda_adj != 0: lambda_adj A Q (internal row order)
@@ -510,6 +514,12 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
                                                                                             ctx->num_sms),
                                             op->ws_allocs)
                           : nullptr;
+  if (g->dense_u8) {
+    int64_t qb = 0;
+    const int64_t wb = dense_i8_ws_bytes(g->n, wpad, ctx->num_sms, &qb);
+    op->i8_ws = dmalloc(ctx, (size_t)wb, op->ws_allocs);
+    op->i8_q = (uint8_t*)dmalloc(ctx, (size_t)qb, op->ws_allocs);
+  }
   op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
                               op->ws_allocs);
   op->adjbuf = op->lambda_adj != 0.0
@@ -628,6 +638,14 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
     re.col_idx = g->ci_rem; re.val = g->val_rem;
     re.pre = op->loc_partial; re.ldpre = a.wpad;
     CK(launch_spmm(g->plan_rem, re, op->partial, ctx->num_sms, ctx->stream, 0, col_block));
+  } else if (g->dense_u8 && !a.pre) {
+    // f3 comparison, exact: A Y on the INT8 tensor cores over the fixed-point slices of Y
+    int64_t parts = 0, ws_rows = 0, ws_ld = 0;
+    const unsigned* cmax = nullptr;
+    const double* pws = nullptr;
+    CK(launch_dense_i8(g->dense_u8, g->ld_u8, g->n, a.Y, a.ldy, a.wpad, op->i8_q, op->i8_ws, ctx->num_sms,
+                       ctx->stream, &parts, &ws_rows, &ws_ld, &cmax, &pws));
+    CK(launch_spmm_dense64_epilogue(pws, parts, ws_rows, ws_ld, cmax, a, g->n_local, ctx->num_sms, ctx->stream));
   } else if (g->dense && !a.pre) {
     // f3 comparison: acc = A Y as a tensor-core product over the dense adjacency (A symmetric, so
     // A Y = A^T Y: the Gram kernel's row-contraction form), then the same epilogue
@@ -1483,11 +1501,18 @@ isvd_status isvd_graph_create(isvd_ctx ctx, int64_t n_global, int64_t row_begin,
     g->rs = (float*)dmalloc(ctx, nb, g->allocs);
     CK(launch_scales(g->row_ptr, g->val, n_local, g->inv_deg, g->s, g->s2, g->rs, ctx->stream));
     phase("scales");
-    if (env_flag("ISVD_DENSE_A", false) && !ctx->dist && n_local == n_global && n_global <= 32768 && !g->new2old &&
+    const char* dense_env = getenv("ISVD_DENSE_A");  // 1: exact INT8 (unweighted), 2: 3xTF32
+    if (dense_env && dense_env[0] != '0' && !ctx->dist && n_local == n_global && n_global <= 32768 && !g->new2old &&
         n_global >= 1) {
       g->ld_dense = round_up(n_global, 4);
       g->dense = (float*)dmalloc(ctx, sizeof(float) * (size_t)n_global * g->ld_dense, g->allocs);
       CK(launch_dense_adjacency(g->row_ptr, g->col_idx, g->val, n_global, g->ld_dense, g->dense, ctx->stream));
+      // ISVD_DENSE_A=1: the exact INT8 path for unweighted graphs; =2 forces the 3xTF32 path
+      if (!g->val && dense_env[0] != '2') {
+        g->ld_u8 = round_up(n_global, 16);
+        g->dense_u8 = (uint8_t*)dmalloc(ctx, (size_t)n_global * g->ld_u8, g->allocs);
+        CK(launch_dense_to_u8(g->dense, n_global, g->ld_dense, g->dense_u8, g->ld_u8, ctx->stream));
+      }
     }
     // SpMM segment plan: rows of <= kSegEdges edges are one segment; longer rows are
     // split, their partial sums combined by the fixup pass in segment order (graph_build.cu)

@@ -164,6 +164,20 @@ cudaError_t launch_split_fill(const int64_t* rp, const int32_t* ci, const float*
 // Dense adjacency (SURVEY 8(f) f3 comparison): out (n x ld fp32, zero-filled here) gets A_ij at (i, j).
 cudaError_t launch_dense_adjacency(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t ld,
                                    float* out, cudaStream_t st);
+// Unweighted dense adjacency as bytes (entries are small integer counts; n x ldo, zero padded columns).
+cudaError_t launch_dense_to_u8(const float* in, int64_t n, int64_t ldi, uint8_t* out, int64_t ldo, cudaStream_t st);
+// Exact A Y on the INT8 tensor cores (dense_i8.cu): A = n x n bytes (lda = round_up(n, 16)), Y n x w fp32.
+// ws: dense_i8_ws_bytes bytes (fp64 integer partials + column maxima), Qws: *q_bytes bytes.  Outputs the
+// partial layout and the column-maximum bits for launch_spmm_dense64_epilogue.
+int64_t dense_i8_ws_bytes(int64_t n, int64_t w, int num_sms, int64_t* q_bytes);
+cudaError_t launch_dense_i8(const uint8_t* A, int64_t lda, int64_t n, const float* Y, int64_t ldy, int64_t w,
+                            uint8_t* Qws, void* ws, int num_sms, cudaStream_t st, int64_t* parts, int64_t* ws_rows,
+                            int64_t* ws_ld, const unsigned** cmax_out, const double** part_out);
+// acc[row, col] = 2^(E_col - 22) * sum_p ws[p][row][col] (E_col from the column-maximum bits), then
+// the SpMM epilogue of `a`.
+cudaError_t launch_spmm_dense64_epilogue(const double* ws, int64_t parts, int64_t ws_rows, int64_t ws_ld,
+                                         const unsigned* cmax, const SpmmArgs& a, int64_t n_local, int num_sms,
+                                         cudaStream_t st);
 // Epilogue of the dense-A product (f3): acc = sum over `parts` fp32 partial tiles ws32[p][row][col]
 // (ws_lda rows, ws_ld columns per part; summed in fp64 in part order), then the SpMM epilogue of `a`
 // (self term, scales, Horner term, rank-1 correction, out_map) for rows < n_local.

@@ -211,6 +211,23 @@ __global__ void dense_adj_kernel(const int64_t* __restrict__ rp, const int32_t* 
 }
 }  // namespace
 
+namespace {
+__global__ void f32_to_u8_kernel(const float* __restrict__ in, int64_t n, int64_t ldi, uint8_t* __restrict__ out,
+                                 int64_t ldo) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * ldo; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ldo, c = t - r * ldo;
+    out[t] = c < n ? (uint8_t)fminf(in[r * ldi + c], 255.f) : 0;
+  }
+}
+}  // namespace
+
+cudaError_t launch_dense_to_u8(const float* in, int64_t n, int64_t ldi, uint8_t* out, int64_t ldo, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  f32_to_u8_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * ldo, 256), 148 * 32), 256, 0, st>>>(in, n, ldi, out, ldo);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dense_adjacency(const int64_t* rp, const int32_t* ci, const float* val, int64_t n, int64_t ld,
                                    float* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -443,6 +443,42 @@ __global__ void spmm_dense_epilogue_kernel(const float* __restrict__ ws32, int64
 }
 }  // namespace
 
+namespace {
+__global__ void spmm_dense64_epilogue_kernel(const double* __restrict__ ws, int64_t parts, int64_t ws_rows,
+                                             int64_t ws_ld, const unsigned* __restrict__ cmax, SpmmArgs a,
+                                             int64_t n_local) {
+  const int64_t c4n = a.wpad >> 2;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_local * c4n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / c4n, col = 4 * (t - row * c4n);
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t p = 0; p < parts; ++p) {
+      const double* w = ws + (p * ws_rows + row) * ws_ld + col;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] += w[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // the fixed-point scale 2^(E - 22) of the column (dense_i8.cu)
+      const float m = __uint_as_float(cmax[col + u]);
+      int e = 0;
+      if (m > 0.f) frexpf(m, &e);
+      v[u] = m > 0.f ? ldexp(v[u], e - 22) : 0.0;
+    }
+    spmm_epilogue(a, row, col, Acc4{v[0], v[1], v[2], v[3]});
+  }
+}
+}  // namespace
+
+cudaError_t launch_spmm_dense64_epilogue(const double* ws, int64_t parts, int64_t ws_rows, int64_t ws_ld,
+                                         const unsigned* cmax, const SpmmArgs& a, int64_t n_local, int num_sms,
+                                         cudaStream_t st) {
+  if (n_local <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n_local * (a.wpad >> 2), 256), (int64_t)num_sms * 8);
+  ++g_launches;
+  spmm_dense64_epilogue_kernel<<<(unsigned)blocks, 256, 0, st>>>(ws, parts, ws_rows, ws_ld, cmax, a, n_local);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_spmm_dense_epilogue(const float* ws32, int64_t parts, int64_t ws_lda, int64_t ws_ld,
                                        const SpmmArgs& a, int64_t n_local, int num_sms, cudaStream_t st) {
   if (n_local <= 0) return cudaSuccess;

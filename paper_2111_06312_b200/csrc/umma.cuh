@@ -131,4 +131,18 @@ inline bool make_map(CUtensorMap* tm, const float* base, int64_t rows, int64_t c
 }
 
 
+// Row-major byte matrix (rows x cols uint8, ld bytes) as a 2-D tensor map with boxes of box_rows x box_cols.
+inline bool make_map_u8(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                        int box_rows, CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace isvd
