@@ -750,19 +750,14 @@ F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   // shared-memory-bound.  (8 x 16 tiles need 255 registers; at 2 CTAs per SM they measured
   // slower than 8 x 8 -- 0.95 vs 0.88 s per config-4 isvd -- and are not offered.)
   // (32 x 32: the symmetric Gram's small trailing diagonal block, e.g. 16 x 16 at l = 400)
-  // (104 x 200: the d = 100, l = 400 shape in 325-thread CTAs -- 11 warps, 8 % idle lanes -- instead
-  // of 104 x 80 in 130-thread CTAs, whose fifth warp holds 2 threads: 19 % of the issued lanes idle;
-  // the cost therefore also counts the lanes of partial warps)
-  const int cand[7][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8},
-                          {32, 32, 4, 8}, {104, 200, 8, 8}};
+  // (104 x 200 in 325-thread CTAs -- 8 % idle lanes instead of the 19 % of 104 x 80's 130 threads,
+  // but 135 registers, one CTA per SM -- measured no faster: 6.45 vs 6.38 ms, round 2)
+  const int cand[6][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8},
+                          {32, 32, 4, 8}};
   F32Tiling t{64, 64, 4, 8, 0, 0, 0, 0};
   double best = -1;
-  static const bool wide = !(getenv("ISVD_ATB_WIDE") && getenv("ISVD_ATB_WIDE")[0] == '0');
   for (auto& c : cand) {
-    if (!wide && c[1] == 200) continue;
-    const int thr = (c[0] / c[2]) * (c[1] / c[3]);
-    const double lanes = (double)round_up(thr, 32) / thr;
-    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (double)(c[2] + c[3]) / (c[2] * c[3]) * lanes;
+    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (double)(c[2] + c[3]) / (c[2] * c[3]);
     if (best < 0 || cost < best) {
       best = cost;
       t.bm = c[0];
@@ -849,13 +844,6 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
       else if (t.bm == 104 && t.bn == 80 && t.tm == 8)  // no row scale (X^T Z_j with a pre-scaled X)
         atb_f32_kernel<104, 80, 8, 8, 4, false><<<grid, 130, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr, (int)t.tb,
                                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
-      else if (t.bm == 104 && t.bn == 200 && row_scale)
-        atb_f32_kernel<104, 200, 8, 8, 1><<<grid, 325, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
-                                                               t.chunk_rows, ws32, ws_lda, ws_ld, gate);
-      else if (t.bm == 104 && t.bn == 200)
-        atb_f32_kernel<104, 200, 8, 8, 1, false><<<grid, 325, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr,
-                                                                      (int)t.tb, t.chunk_rows, ws32, ws_lda, ws_ld,
-                                                                      gate);
       else ISVD_ATB_F32(128, 128, 8, 8)
 #undef ISVD_ATB_F32
     } else {
