@@ -265,7 +265,8 @@ typedef struct {
   double ms_products, ms_orth, ms_small, ms_comm;
   int32_t gram_probe_fallbacks; /* first-pass tensor-core Gram probes that fell back to the exact fp64
                                    Gram (ill-conditioned M Omega)                   */
-  int32_t pad1;
+  int32_t gram_probe_skipped;   /* 1: this call skipped the probe and took the exact first Gram
+                                   directly, because an earlier call on this op fell back       */
 } isvd_svd_report;
 
 /* Rank-k randomized SVD of M (Alg. 1) with CholeskyQR2

@@ -96,7 +96,7 @@ class SvdReport(C.Structure):
         ("ms_small", C.c_double),
         ("ms_comm", C.c_double),
         ("gram_probe_fallbacks", C.c_int32),
-        ("pad1", C.c_int32),
+        ("gram_probe_skipped", C.c_int32),
     ]
 
 

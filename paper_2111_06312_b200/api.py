@@ -198,6 +198,7 @@ class SvdResult:
     spmm_alg_bytes: float = 0.0
     phases: "dict | None" = None  # profile=True: ms by phase (products / orth / small / comm)
     gram_probe_fallbacks: int = 0  # first-pass tensor-core Gram probes that fell back to the exact Gram
+    gram_probe_skipped: int = 0  # 1: the probe was skipped (an earlier call on this op fell back)
 
 
 class _Operator:
@@ -330,7 +331,8 @@ class _Operator:
         if profile:
             phases = dict(products=rep.ms_products, orth=rep.ms_orth, small=rep.ms_small, comm=rep.ms_comm)
         return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
-                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases, rep.gram_probe_fallbacks)
+                         rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases, rep.gram_probe_fallbacks,
+                         rep.gram_probe_skipped)
 
 
 class NE(_Operator):

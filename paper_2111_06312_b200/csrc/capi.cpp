@@ -191,6 +191,9 @@ struct isvd_op_s {
   std::vector<void*> ws_allocs;
   float *full_a = nullptr, *full_b = nullptr, *full_c = nullptr, *ptmp = nullptr, *partial = nullptr;
   float* dense_ws = nullptr;  // f3 dense-A products: fp32 partial tiles of launch_tc_atb
+  // the tensor-core probe of the exact first Gram flagged on an earlier call (e.g. config 4, whose
+  // square Omega makes kappa(M Omega)^2 > 1e5 every time): later calls go straight to the exact Gram
+  bool probe_failed = false;
   void* i8_ws = nullptr;      // f3 exact INT8 dense products: fp64 integer partials + column maxima
   uint8_t* i8_q = nullptr;    // ... and the byte slices of the fixed-point gather source
   double *colsum = nullptr, *colsum_ws = nullptr, *atb_ws = nullptr, *blk64 = nullptr;
@@ -1867,7 +1870,8 @@ void cqr_pass(isvd_op op, const float* Y, float* Yout, int64_t rows, bool distri
   // Gram and the (shift-capable) Cholesky recomputed, gated on that device flag (no host sync).
   // Saves the 22.6 ms exact Gram at config 4 when Y is well conditioned.  ISVD_GRAM_PROBE=0: off.
   static const bool probe_off = getenv("ISVD_GRAM_PROBE") && getenv("ISVD_GRAM_PROBE")[0] == '0';
-  if (mode == kGramF64 && !gate && !probe_off && l <= 512 && use_tensor_cores(rows, l, l, ld, ld, true)) {
+  if (mode == kGramF64 && !gate && !probe_off && !op->probe_failed && l <= 512 &&
+      use_tensor_cores(rows, l, l, ld, ld, true)) {
     int* flag = &ctx->status->need_exact_gram;
     CK(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
     atb_fp32(op, rows, Y, ld, l, nullptr, Y, ld, l, true, s.gram, l, nullptr);
@@ -2219,7 +2223,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     ctx->stream = ctx->work;
     ctx->profiling = p->flags & ISVD_SVD_PROFILE;
     ctx->phase_tag.clear();
-    const uint64_t key = graph_key(p, l, ldk);
+    const uint64_t key = graph_key(p, l, ldk) ^ (op->probe_failed ? 0x9E3779B97F4A7C15ULL : 0);
     int64_t launches = 0;
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
     if (use_graph && (s.graph_exec == nullptr || s.graph_key != key)) {
@@ -2294,6 +2298,10 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     }
     CK(cudaEventRecord(ctx->ev_join, ctx->stream));
     CK(cudaStreamWaitEvent(user, ctx->ev_join, 0));
+    // a probe that fell back on real data (not a forced breakdown) will fall back again on the next
+    // call with the same operator: take the exact Gram directly from then on (a new graph key)
+    const bool skipped_probe = op->probe_failed;
+    if (st.probes_failed > 0 && !(p->flags & ISVD_SVD_FORCE_CHOL_FAIL)) op->probe_failed = true;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     if (rep) {
@@ -2301,6 +2309,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
       rep->ld = (int32_t)round_up(l, 4);
       rep->chol_fallbacks = st.chol_breakdown;
       rep->gram_probe_fallbacks = st.probes_failed;
+      rep->gram_probe_skipped = skipped_probe ? 1 : 0;
       rep->jacobi_sweeps = st.jacobi_sweeps;
       rep->world = ctx->world;
       rep->kernel_launches = (int32_t)launches;

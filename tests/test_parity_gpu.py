@@ -900,3 +900,17 @@ def test_dense_adjacency_products_and_isvd(ctx, i, mode):
     print(check_isvd(res, oracle_isvd_result(i), sp["k"], f"cfg{i} {mode} isvd"))
     op.close()
     graph.close()
+
+
+def test_gram_probe_sticky_skip_config4(ctx):
+    """Config 4 (l = c = 400, square Omega): kappa(M Omega)^2 is too large for the tensor-core probe
+    of the first Gram, which falls back to the exact fp64 Gram; the op remembers it and later calls
+    take the exact Gram directly (no probe), with bitwise-identical results (the exact path is the
+    same kernels either way)."""
+    op, _, cfg, sp = _op(ctx, 4)
+    r1 = op.svd(sp["k"], -1, sp["q"], sp["seed"])
+    r2 = op.svd(sp["k"], -1, sp["q"], sp["seed"])
+    assert r1.gram_probe_fallbacks > 0 or r1.gram_probe_skipped == 1
+    assert r2.gram_probe_skipped == 1 and r2.gram_probe_fallbacks == 0
+    assert np.array_equal(r1.S, r2.S)
+    assert torch.equal(r1.U, r2.U)
