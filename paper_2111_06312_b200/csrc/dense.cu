@@ -754,10 +754,18 @@ F32Tiling f32_tiling(int64_t rows, int64_t Ka, int64_t Kb, int num_sms) {
   // but 135 registers, one CTA per SM -- measured no faster: 6.45 vs 6.38 ms, round 2)
   const int cand[6][4] = {{64, 64, 4, 8}, {100, 80, 4, 8}, {128, 128, 4, 8}, {104, 80, 8, 8}, {128, 128, 8, 8},
                           {32, 32, 4, 8}};
+  // Round 2: the cost also counts idle lanes of a partial last warp (104 x 80 x (8 x 8) is 130 threads:
+  // its fifth warp issues every instruction for 2 threads) and weighs the shared-memory reads per FMA
+  // as an overhead on the FMAs rather than the bound (ncu: FMA pipe 66 % active, LSU 27 %, barrier
+  // stalls first).  At d = 100, l = 400 that picks 100 x 80 x (4 x 8), 250 threads, no padding:
+  // X^T Z_j 6.67 -> 4.70 ms (profiles/r02e_dense_check.txt).
   F32Tiling t{64, 64, 4, 8, 0, 0, 0, 0};
   double best = -1;
   for (auto& c : cand) {
-    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * (double)(c[2] + c[3]) / (c[2] * c[3]);
+    const int thr = (c[0] / c[2]) * (c[1] / c[3]);
+    const double lanes = (double)round_up(thr, 32) / thr;
+    const double cost = (double)round_up(Ka, c[0]) * round_up(Kb, c[1]) * lanes *
+                        (1.0 + (double)(c[2] + c[3]) / (c[2] * c[3]));
     if (best < 0 || cost < best) {
       best = cost;
       t.bm = c[0];
@@ -836,8 +844,12 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
         A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb, t.chunk_rows, ws32, ws_lda, ws_ld, gate);
       ISVD_ATB_F32(64, 64, 4, 8)
       else ISVD_ATB_F32(32, 32, 4, 8)
-      else ISVD_ATB_F32(100, 80, 4, 8)
-      else ISVD_ATB_F32(128, 128, 4, 8)
+      else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8 && row_scale)  // 250 threads, full warps
+        atb_f32_kernel<100, 80, 4, 8, 3><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
+                                                              t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+      else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8)  // X^T Z_j with a pre-scaled X: 4.7 ms
+        atb_f32_kernel<100, 80, 4, 8, 4, false><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr, (int)t.tb,
+                                                                     t.chunk_rows, ws32, ws_lda, ws_ld, gate);
       else if (t.bm == 104 && t.bn == 80 && t.tm == 8 && row_scale)  // 4 CTAs per SM (96 registers): 8.2 -> 7.4 ms at config 4
         atb_f32_kernel<104, 80, 8, 8, 4><<<grid, 130, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
                                                               t.chunk_rows, ws32, ws_lda, ws_ld, gate);

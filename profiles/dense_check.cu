@@ -73,6 +73,10 @@ int main(int argc, char** argv) {
       den += ref * ref;
     }
     printf("X^T s Z   : %7.3f ms  %6.1f TFLOP/s   sampled rel err %.2e\n", t, gf / t, std::sqrt(num / den));
+    // the solver's form: X pre-scaled once per op, no per-element row scale in the kernel
+    const float tn = time_ms([&] { isvd::launch_atb(dX, d, dZ, l, n, d, l, nullptr, false, ws, dOut, l, nullptr, 0, sms,
+                                                     nullptr, 0, true); });
+    printf("X^T Z     : %7.3f ms  %6.1f TFLOP/s   (pre-scaled X)\n", tn, gf / tn);
   }
   t = time_ms([&] { isvd::launch_atb(dZ, l, dZ, l, n, l, l, nullptr, true, ws, dOut, l, nullptr, 0, sms, nullptr, 0, false); });
   printf("Z^T Z fp64: %7.3f ms  %6.1f TFLOP/s (symmetric half)\n", t, 2.0 * n * l * l / 2 / 1e9 / t);
