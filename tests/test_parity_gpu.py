@@ -103,15 +103,15 @@ def _col_parallel(fn, M, cols, workers=None):
 
 def test_products_config4_sampled_columns(ctx):
     """Config 4 at full size in the bench's launch configuration (width l = 400, the relabelled
-    graph with its hub/split segments and L2 window): the oracle computes 32 of the 400 output
-    columns -- 28 random ones plus the last float4 (396..399) -- checked on every row (all hub,
+    graph with its hub/split segments and L2 window): the oracle computes 64 of the 400 output
+    columns -- 60 random ones plus the last float4 (396..399) -- checked on every row (all hub,
     split-fixup and ragged-tail rows included) and every sampled column."""
     op, ref, cfg, sp = _op(ctx, 4)
     from oracle import philox_omega
 
     l = sp["l"]
     rng = np.random.default_rng(404)
-    cols = np.sort(np.concatenate([rng.choice(l - 4, 28, replace=False), np.arange(l - 4, l)]))
+    cols = np.sort(np.concatenate([rng.choice(l - 4, 60, replace=False), np.arange(l - 4, l)]))
     G = philox_omega(99, 0, op.c_rows(), l)
     Y = _to_np(op.matmul(torch.from_numpy(G).cuda())[:, torch.from_numpy(cols).cuda()])
     Yref, _ = _col_parallel(ref.matmul, G, cols)
