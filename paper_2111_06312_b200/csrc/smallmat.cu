@@ -341,11 +341,31 @@ __global__ void __launch_bounds__(kJbThreads) jacobi_block_kernel(const double* 
         scol[q] = c < l ? c : -1;
       }
       __syncthreads();
-      for (int64_t t = tid; t < (int64_t)m2 * l; t += kJbThreads) {
-        const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+      // a warp per column (columns are contiguous): no index division, 16-byte L2 loads (.cg: the
+      // columns were written by other CTAs since the last grid barrier), several in flight per lane
+      // (round 2: the element loop with a 64-bit division per element made this copy the longest
+      // phase of an outer round)
+      for (int q = warp; q < m2; q += nw) {
         const int c = scol[q];
-        sA[t] = c >= 0 ? A[(int64_t)c * l + r] : 0.0;
-        sJ[t] = c >= 0 ? J[(int64_t)c * l + r] : 0.0;
+        double* la = sA + (int64_t)q * l;
+        double* lj = sJ + (int64_t)q * l;
+        if (c < 0) {
+          for (int r = lane; r < l; r += 32) la[r] = lj[r] = 0.0;
+        } else if ((l & 1) == 0) {
+          const double2* ga = reinterpret_cast<const double2*>(A + (int64_t)c * l);
+          const double2* gj = reinterpret_cast<const double2*>(J + (int64_t)c * l);
+#pragma unroll 4
+          for (int r = lane; r < l / 2; r += 32) {
+            const double2 x = __ldcg(ga + r), y = __ldcg(gj + r);
+            reinterpret_cast<double2*>(la)[r] = x;
+            reinterpret_cast<double2*>(lj)[r] = y;
+          }
+        } else {
+          for (int r = lane; r < l; r += 32) {
+            la[r] = __ldcg(A + (int64_t)c * l + r);
+            lj[r] = __ldcg(J + (int64_t)c * l + r);
+          }
+        }
       }
       __syncthreads();
       for (int q = warp; q < m2; q += nw) {
@@ -402,12 +422,24 @@ __global__ void __launch_bounds__(kJbThreads) jacobi_block_kernel(const double* 
         }
         __syncthreads();
       }
-      for (int64_t t = tid; t < (int64_t)m2 * l; t += kJbThreads) {
-        const int q = (int)(t / l), r = (int)(t - (int64_t)q * l);
+      for (int q = warp; q < m2; q += nw) {
         const int c = scol[q];
-        if (c >= 0) {
-          A[(int64_t)c * l + r] = sA[t];
-          J[(int64_t)c * l + r] = sJ[t];
+        if (c < 0) continue;
+        const double* la = sA + (int64_t)q * l;
+        const double* lj = sJ + (int64_t)q * l;
+        if ((l & 1) == 0) {
+          double2* ga = reinterpret_cast<double2*>(A + (int64_t)c * l);
+          double2* gj = reinterpret_cast<double2*>(J + (int64_t)c * l);
+#pragma unroll 4
+          for (int r = lane; r < l / 2; r += 32) {
+            __stcg(ga + r, reinterpret_cast<const double2*>(la)[r]);
+            __stcg(gj + r, reinterpret_cast<const double2*>(lj)[r]);
+          }
+        } else {
+          for (int r = lane; r < l; r += 32) {
+            __stcg(A + (int64_t)c * l + r, la[r]);
+            __stcg(J + (int64_t)c * l + r, lj[r]);
+          }
         }
       }
       grid.sync();
