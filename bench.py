@@ -256,10 +256,19 @@ def gather_floor(g, sp, world, alg_bytes_per_launch, avg_launch_ms):
     rest = alg_bytes_per_launch - 4.0 * g.n * ld
     peak, _ = load_peaks()
     floor_ms = (cold / 6.3e12 + rest / (peak * 1e9)) * 1e3
-    return {"floor_ms": floor_ms, "achieved_ms": avg_launch_ms, "frac": floor_ms / avg_launch_ms,
-            "hub_share_of_gathers": hub_share, "cold_gather_GB": cold / 1e9,
-            "basis": "cold-row gathers at the measured 6.3 TB/s random-1600B-row DRAM rate + the other algorithmic "
-                     "bytes at the measured copy peak (DESIGN.md §6)"}
+    out = {"floor_ms": floor_ms, "achieved_ms": avg_launch_ms, "frac": floor_ms / avg_launch_ms,
+           "hub_share_of_gathers": hub_share, "cold_gather_GB": cold / 1e9,
+           "basis": "cold-row gathers at the measured 6.3 TB/s random-1600B-row DRAM rate + the other algorithmic "
+                    "bytes at the measured copy peak (DESIGN.md §6)"}
+    if l == 400 and g.n > 2_000_000:
+        # the same gather mix as a pure-gather microbenchmark on this hardware (config 4 only):
+        # profiles/hub_gather_bench.cu, 41.5 % of 1600-B row gathers on a 78 MB hub prefix with the
+        # persisting window, the rest uniform over 3.9 GB: 24.7 ms per 198 GB (4 nnz l bytes)
+        gv = 4.0 * ld * float(deg.sum())
+        mix_ms = 24.7 * gv / 198e9
+        out["measured_gather_mix"] = {"ms": mix_ms, "frac": mix_ms / avg_launch_ms,
+                                      "source": "profiles/hub_gather_bench.cu (profiles/r02e_spmm_sorted_hint.jsonl)"}
+    return out
 
 
 def main():
