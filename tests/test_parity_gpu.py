@@ -914,3 +914,35 @@ def test_gram_probe_sticky_skip_config4(ctx):
     assert r2.gram_probe_skipped == 1 and r2.gram_probe_fallbacks == 0
     assert np.array_equal(r1.S, r2.S)
     assert torch.equal(r1.U, r2.U)
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_dense_adjacency_tiny_isolated_ragged(ctx, mode):
+    """Dense-A paths (INT8 exact / 3xTF32) on a 7-node graph with an isolated node (zero row of T,
+    reading O3), width 3 (ragged: one 16-row / 64-byte tile, zero-filled beyond n and w), and on a
+    130-node cycle plus chords (two 128-row output tiles, the second with 2 rows), both directions."""
+    import os
+
+    import paper_2111_06312_b200 as isvd_mod
+    from oracle import NEOperator, adjacency, uniform_weights
+    from synth.graphs import edges_to_graph
+
+    for n, edges, w in ((7, [(0, 1), (1, 2), (2, 3), (3, 0), (4, 5)], 3),
+                        (130, [(i, (i + 1) % 130) for i in range(130)] + [(i, (i + 17) % 130) for i in range(0, 130, 3)],
+                         20)):
+        g = edges_to_graph(n, edges)
+        os.environ["ISVD_DENSE_A"] = mode
+        try:
+            graph = isvd_mod.Graph(ctx, n, g.row_ptr, g.col_idx)
+        finally:
+            del os.environ["ISVD_DENSE_A"]
+        wts = uniform_weights(3)
+        op = isvd_mod.NE(graph, wts, 1.0 / n)
+        ref = NEOperator(adjacency(g.n, g.row_ptr, g.col_idx), wts, 1.0 / n)
+        Q = np.random.default_rng(n).standard_normal((n, w)).astype(np.float32)
+        print(assert_product(_to_np(op.matmul(torch.from_numpy(Q).cuda())), ref.matmul(Q.astype(np.float64)),
+                             f"dense{mode} n={n} M.Q"))
+        print(assert_product(_to_np(op.matmul_T(torch.from_numpy(Q).cuda())), ref.matmul_T(Q.astype(np.float64)),
+                             f"dense{mode} n={n} M^T.Q"))
+        op.close()
+        graph.close()
