@@ -503,25 +503,30 @@ void ensure_op_ws(isvd_op op, int64_t wpad) {
                              : nullptr;
   op->colsum = (double*)dmalloc(ctx, sizeof(double) * wpad, op->ws_allocs);
   op->colsum_ws = (double*)dmalloc(ctx, sizeof(double) * colsum_ws_doubles(g->n_local, wpad), op->ws_allocs);
-  int64_t ka = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : wpad;
-  int64_t atb = std::max(atb_ws_doubles(g->n_local, ka, wpad, ctx->num_sms),
-                         atb_ws_doubles(g->n_local, wpad, wpad, ctx->num_sms));
-  atb = std::max(atb, (tc_atb_ws_floats(g->n_local, ka, wpad, false, ctx->num_sms) + 1) / 2);
-  atb = std::max(atb, (tc_atb_ws_floats(g->n_local, wpad, wpad, true, ctx->num_sms) + 1) / 2);
-  if (op->lr_powers > 0) {
-    atb = std::max(atb, atb_ws_doubles(g->n_local, op->ylr, wpad, ctx->num_sms));
-    atb = std::max(atb, (tc_atb_ws_floats(g->n_local, op->ylr, wpad, false, ctx->num_sms) + 1) / 2);
+  // Workspaces are sized for every width w <= wpad a later call may use (the tilings pick more
+  // row parts for narrower products, so a narrower call can need more partial tiles than wpad)
+  int64_t ka_nc = op->kind == ISVD_OP_STACKED_PROPAGATION ? op->d : 0;
+  int64_t atb = 0, dense_f = 0, i8_b = 0, i8_q = 0;
+  for (int64_t w = 4; w <= wpad; w += 4) {
+    const int64_t ka = ka_nc ? ka_nc : w;
+    atb = std::max({atb, atb_ws_doubles(g->n_local, ka, w, ctx->num_sms), atb_ws_doubles(g->n_local, w, w, ctx->num_sms),
+                    (tc_atb_ws_floats(g->n_local, ka, w, false, ctx->num_sms) + 1) / 2,
+                    (tc_atb_ws_floats(g->n_local, w, w, true, ctx->num_sms) + 1) / 2});
+    if (op->lr_powers > 0)
+      atb = std::max({atb, atb_ws_doubles(g->n_local, op->ylr, w, ctx->num_sms),
+                      (tc_atb_ws_floats(g->n_local, op->ylr, w, false, ctx->num_sms) + 1) / 2});
+    if (g->dense) dense_f = std::max(dense_f, tc_atb_ws_floats(g->n, g->n, w, false, ctx->num_sms));
+    if (g->dense_u8) {
+      int64_t qb = 0;
+      i8_b = std::max(i8_b, dense_i8_ws_bytes(g->n, w, ctx->num_sms, &qb));
+      i8_q = std::max(i8_q, qb);
+    }
   }
-  op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * atb, op->ws_allocs);
-  op->dense_ws = g->dense ? (float*)dmalloc(ctx, sizeof(float) * (size_t)tc_atb_ws_floats(g->n, g->n, wpad, false,
-                                                                                            ctx->num_sms),
-                                            op->ws_allocs)
-                          : nullptr;
+  op->atb_ws = (double*)dmalloc(ctx, sizeof(double) * std::max<int64_t>(atb, 1), op->ws_allocs);
+  op->dense_ws = g->dense ? (float*)dmalloc(ctx, sizeof(float) * (size_t)dense_f, op->ws_allocs) : nullptr;
   if (g->dense_u8) {
-    int64_t qb = 0;
-    const int64_t wb = dense_i8_ws_bytes(g->n, wpad, ctx->num_sms, &qb);
-    op->i8_ws = dmalloc(ctx, (size_t)wb, op->ws_allocs);
-    op->i8_q = (uint8_t*)dmalloc(ctx, (size_t)qb, op->ws_allocs);
+    op->i8_ws = dmalloc(ctx, (size_t)i8_b, op->ws_allocs);
+    op->i8_q = (uint8_t*)dmalloc(ctx, (size_t)i8_q, op->ws_allocs);
   }
   op->bt_ws = (float*)dmalloc(ctx, sizeof(float) * tc_gemm_ws_floats(wpad, std::max<int64_t>(wpad, op->d)),
                               op->ws_allocs);

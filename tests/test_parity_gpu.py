@@ -946,3 +946,18 @@ def test_dense_adjacency_tiny_isolated_ragged(ctx, mode):
                              f"dense{mode} n={n} M^T.Q"))
         op.close()
         graph.close()
+
+
+def test_products_after_a_wider_call_config2(ctx):
+    """An operator first used at width 256 and then at narrower widths (160, 100, 36) reuses its
+    workspaces, which are sized for every width up to the widest seen (the tilings of a narrower
+    product can need more row parts); every product still meets the bar."""
+    op, ref, cfg, sp = _op(ctx, 2)
+    rng = np.random.default_rng(2024)
+    for w in (256, 160, 100, 36):
+        H = rng.standard_normal((op.graph.n_local, w)).astype(np.float32)
+        print(assert_product(_to_np(op.matmul_T(torch.from_numpy(H).cuda())), ref.matmul_T(H.astype(np.float64)),
+                             f"cfg2 M^T.H w={w}"))
+        G = rng.standard_normal((op.c_rows(), w)).astype(np.float32)
+        print(assert_product(_to_np(op.matmul(torch.from_numpy(G).cuda())), ref.matmul(G.astype(np.float64)),
+                             f"cfg2 M.G w={w}"))
