@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(256) quant_kernel(const float* __restrict__ Y,
     int q = 0;
     if (j < n && c < w) {
       const int E = col_exp(cmax[c]);
-      if (E > -1000) q = __float2int_rn(ldexpf(Y[j * ldy + c], 22 - E));
+      const float y = Y[j * ldy + c];
+      if (E > -1000 && isfinite(y) && isfinite(__uint_as_float(cmax[c]))) q = __float2int_rn(ldexpf(y, 22 - E));
     }
     t[0][cc][jj] = (uint8_t)(q & 0xFF);
     t[1][cc][jj] = (uint8_t)((q >> 8) & 0xFF);

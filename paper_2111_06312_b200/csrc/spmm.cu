@@ -461,8 +461,10 @@ __global__ void spmm_dense64_epilogue_kernel(const double* __restrict__ ws, int6
     for (int u = 0; u < 4; ++u) {  // the fixed-point scale 2^(E - 22) of the column (dense_i8.cu)
       const float m = __uint_as_float(cmax[col + u]);
       int e = 0;
-      if (m > 0.f) frexpf(m, &e);
-      v[u] = m > 0.f ? ldexp(v[u], e - 22) : 0.0;
+      if (m > 0.f && isfinite(m)) frexpf(m, &e);
+      // a non-finite entry of the column (its max is Inf / NaN) makes the whole column NaN, as the
+      // CSR path would propagate it, so the solver's output check reports it
+      v[u] = !isfinite(m) ? (double)NAN : (m > 0.f ? ldexp(v[u], e - 22) : 0.0);
     }
     spmm_epilogue(a, row, col, Acc4{v[0], v[1], v[2], v[3]});
   }

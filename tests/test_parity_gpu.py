@@ -944,6 +944,9 @@ def test_dense_adjacency_tiny_isolated_ragged(ctx, mode):
                              f"dense{mode} n={n} M.Q"))
         print(assert_product(_to_np(op.matmul_T(torch.from_numpy(Q).cuda())), ref.matmul_T(Q.astype(np.float64)),
                              f"dense{mode} n={n} M^T.Q"))
+        Qn = Q.copy()
+        Qn[1, 0] = np.nan  # a non-finite input must not come back as finite data
+        assert not np.isfinite(_to_np(op.matmul(torch.from_numpy(Qn).cuda()))).all()
         op.close()
         graph.close()
 
