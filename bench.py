@@ -391,6 +391,10 @@ def main():
     spmm_n = sum(r.spmm_steps for r in prof)
     spmm_bytes = sum(r.spmm_alg_bytes for r in prof)
     phases = {k_: statistics.median(r.phases[k_] for r in prof) for k_ in prof[0].phases}
+    # distributed split: all-gather time on the collectives stream and the part hidden behind the
+    # local SpMM passes (CUDA-event intervals of the profiled pass)
+    allgather = ({"ms": statistics.median(r.ms_allgather for r in prof),
+                  "hidden_ms": statistics.median(r.ms_allgather_hidden for r in prof)} if world > 1 else None)
     ms_prof = statistics.median(r.ms_total for r in prof)
 
     # ---- variant: tensor cores for every tall contraction (ISVD_TC_PRODUCTS=1), not only the
@@ -562,6 +566,7 @@ def main():
                 "gather_floor": gather_floor(g, sp, world, per_launch_bytes, spmm_ms / spmm_n if spmm_n else None),
             },
             "phases_ms": phases,
+            "allgather": allgather,
             "cpu_baseline": cpu,
             "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

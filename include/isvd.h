@@ -267,6 +267,10 @@ typedef struct {
                                    Gram (ill-conditioned M Omega)                   */
   int32_t gram_probe_skipped;   /* 1: this call skipped the probe and took the exact first Gram
                                    directly, because an earlier call on this op fell back       */
+  /* ISVD_SVD_PROFILE, distributed with the local / remote split: summed duration of the
+   * all-gathers of SpMM gather sources on the collectives stream, and the part of it that ran
+   * concurrently with the local SpMM pass issued meanwhile (CUDA-event intervals); 0 otherwise. */
+  double ms_allgather, ms_allgather_hidden;
 } isvd_svd_report;
 
 /* Rank-k randomized SVD of M (Alg. 1) with CholeskyQR2

@@ -97,6 +97,8 @@ class SvdReport(C.Structure):
         ("ms_comm", C.c_double),
         ("gram_probe_fallbacks", C.c_int32),
         ("gram_probe_skipped", C.c_int32),
+        ("ms_allgather", C.c_double),
+        ("ms_allgather_hidden", C.c_double),
     ]
 
 

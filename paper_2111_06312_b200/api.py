@@ -199,6 +199,8 @@ class SvdResult:
     phases: "dict | None" = None  # profile=True: ms by phase (products / orth / small / comm)
     gram_probe_fallbacks: int = 0  # first-pass tensor-core Gram probes that fell back to the exact Gram
     gram_probe_skipped: int = 0  # 1: the probe was skipped (an earlier call on this op fell back)
+    ms_allgather: float = 0.0  # profile=True, distributed split: all-gather time on the collectives stream
+    ms_allgather_hidden: float = 0.0  # ... the part concurrent with the local SpMM pass
 
 
 class _Operator:
@@ -332,7 +334,7 @@ class _Operator:
             phases = dict(products=rep.ms_products, orth=rep.ms_orth, small=rep.ms_small, comm=rep.ms_comm)
         return SvdResult(U, S, V, rep.l, rep.chol_fallbacks, rep.jacobi_sweeps, rep.kernel_launches, rep.ms_total,
                          rep.spmm_steps, rep.ms_spmm, rep.spmm_alg_bytes, phases, rep.gram_probe_fallbacks,
-                         rep.gram_probe_skipped)
+                         rep.gram_probe_skipped, rep.ms_allgather, rep.ms_allgather_hidden)
 
 
 class NE(_Operator):

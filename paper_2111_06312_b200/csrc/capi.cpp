@@ -114,6 +114,10 @@ struct isvd_ctx_s {
   // ISVD_SVD_PROFILE phase brackets: (phase, start event index, end event index) into phase_ev
   std::vector<cudaEvent_t> phase_ev;
   std::vector<int> phase_tag;  // per pair: 0 products, 1 orth, 2 small, 3 comm
+  // ISVD_SVD_PROFILE with the distributed split: (start, end) event pairs of every all-gather on the
+  // collectives stream and of the local SpMM pass issued while it is in flight (overlap report)
+  std::vector<cudaEvent_t> ag_ev, lp_ev;
+  size_t n_ag = 0, n_lp = 0;
   // caching device allocator: buffers released by destroyed graphs / ops / workspaces are kept
   // (by exact rounded size) and handed out again, so rebuilding a graph + operator of the same
   // shape pays no cudaMalloc/cudaFree (they cost ~ms per GB-sized buffer); trimmed on OOM and
@@ -373,6 +377,16 @@ struct Phase {
   }
 };
 
+// Next (start, end) event pair of a profiling list (created on demand); nullptr if unavailable.
+cudaEvent_t* prof_pair(std::vector<cudaEvent_t>& v, size_t& n) {
+  while (v.size() < 2 * n + 2) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    v.push_back(e);
+  }
+  return &v[2 * n++];
+}
+
 // --------------------------------------------------------------- collectives
 // In-place all-gather: rank p's `bytes_per_rank` bytes sit at recv + p * bytes_per_rank.
 void coll_allgather(isvd_ctx ctx, void* recv, size_t bytes_per_rank) {
@@ -423,6 +437,8 @@ void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld
   CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_fork, 0));
   cudaStream_t main = ctx->stream;
   ctx->stream = ctx->cstream;
+  cudaEvent_t* agp = ctx->profiling ? prof_pair(ctx->ag_ev, ctx->n_ag) : nullptr;
+  if (agp) CK(cudaEventRecord(agp[0], ctx->cstream));
   try {
     coll_allgather(ctx, full, bytes);
   } catch (...) {
@@ -430,6 +446,7 @@ void allgather_rows(isvd_ctx ctx, const isvd_graph_s* g, float* full, int64_t ld
     throw;
   }
   ctx->stream = main;
+  if (agp) CK(cudaEventRecord(agp[1], ctx->cstream));
   CK(cudaEventRecord(ctx->ev_gath, ctx->cstream));
   ctx->gather_pending = true;
 }
@@ -640,7 +657,10 @@ void spmm(isvd_ctx ctx, isvd_op op, const SpmmArgs& a) {
     lo.col_idx = g->ci_loc; lo.val = g->val_loc;
     lo.self_coef = 0.f; lo.post_vec = nullptr; lo.post_coef = 1.f; lo.T = nullptr; lo.term_vec = nullptr;
     lo.colsum = nullptr; lo.out = op->loc_partial; lo.ldo = a.wpad; lo.out_map = nullptr; lo.pre = nullptr;
+    cudaEvent_t* lpp = (ctx->profiling && ctx->gather_pending) ? prof_pair(ctx->lp_ev, ctx->n_lp) : nullptr;
+    if (lpp) CK(cudaEventRecord(lpp[0], ctx->stream));
     CK(launch_spmm(g->plan_loc, lo, op->partial, ctx->num_sms, ctx->stream, 0, col_block));
+    if (lpp) CK(cudaEventRecord(lpp[1], ctx->stream));
     join_gather(ctx);
     SpmmArgs re = a;
     re.col_idx = g->ci_rem; re.val = g->val_rem;
@@ -1341,6 +1361,9 @@ isvd_status isvd_ctx_destroy(isvd_ctx ctx) {
   if (ctx->ev_gath) cudaEventDestroy(ctx->ev_gath);
   for (cudaEvent_t e : ctx->ov_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->phase_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ag_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->lp_ev) cudaEventDestroy(e);
   delete ctx;
   return ISVD_OK;
 }
@@ -2228,6 +2251,7 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
     ctx->stream = ctx->work;
     ctx->profiling = p->flags & ISVD_SVD_PROFILE;
     ctx->phase_tag.clear();
+    ctx->n_ag = ctx->n_lp = 0;
     const uint64_t key = graph_key(p, l, ldk) ^ (op->probe_failed ? 0x9E3779B97F4A7C15ULL : 0);
     int64_t launches = 0;
     CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -2334,6 +2358,21 @@ isvd_status isvd_svd(isvd_op op, const isvd_svd_params* p, float* U, int64_t ldu
           float t = 0.f;
           CK(cudaEventElapsedTime(&t, ctx->phase_ev[2 * i], ctx->phase_ev[2 * i + 1]));
           *acc[ctx->phase_tag[i]] += t;
+        }
+        // all-gather / local-pass overlap: intervals relative to the call's start event; each
+        // split all-gather is paired with the local pass issued while it was in flight
+        rep->ms_allgather = rep->ms_allgather_hidden = 0.0;
+        for (size_t i = 0; i < ctx->n_ag; ++i) {
+          float a0 = 0.f, a1 = 0.f;
+          CK(cudaEventElapsedTime(&a0, ctx->ev0, ctx->ag_ev[2 * i]));
+          CK(cudaEventElapsedTime(&a1, ctx->ev0, ctx->ag_ev[2 * i + 1]));
+          rep->ms_allgather += a1 - a0;
+          if (i < ctx->n_lp) {
+            float l0 = 0.f, l1 = 0.f;
+            CK(cudaEventElapsedTime(&l0, ctx->ev0, ctx->lp_ev[2 * i]));
+            CK(cudaEventElapsedTime(&l1, ctx->ev0, ctx->lp_ev[2 * i + 1]));
+            rep->ms_allgather_hidden += std::max(0.f, std::min(a1, l1) - std::max(a0, l0));
+          }
         }
       }
     }
