@@ -10,6 +10,7 @@
 //                once when staged in shared memory, fp64 FMA, deterministic
 //                fixed-order reduction of the per-CTA partials (no atomics).
 //  K15 colsum    1^T Q in fp64 for the rank-1 term of Eq. 3.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -190,6 +191,201 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
             make_float4(s * acc[i][j / 2].x, s * acc[i][j / 2].y, s * acc[i][j / 2 + 1].x, s * acc[i][j / 2 + 1].y);
     }
   }
+}
+
+// ------------------------------------------------------------------ GEMM, K-resident (round 2)
+// C = alpha * diag(row_scale) * A * B for a short contraction (K <= 128: X G_j of the NC operator,
+// K = d) with the whole B panel (K x N, N <= 416) resident in shared memory for the life of a
+// persistent CTA, and 64-row A tiles streamed through a two-slot ring by bulk copies
+// (cp.async.bulk, one per row, completing on an mbarrier).  The K loop of a tile has no CTA
+// barrier at all (gemm_tn_kernel: one per 8 k-steps, its first stall reason in ncu), B is read from
+// L2 once per CTA instead of once per 128 x 80 tile, and the next tile's rows land while this one
+// computes.  Warp w owns columns {16 w + 4 t .. +3} and {NP/2 + 16 w + 4 t .. +3} (t = lane & 3) of
+// all 64 rows; lane row group r = lane >> 2 owns rows {r + 8 i}: a B fragment read touches 64
+// contiguous bytes per warp (broadcast over r), an A fragment read (float2 along k, row pitch K
+// floats, K = 4 mod 32 for K = 100) 8 distinct bank pairs (broadcast over t).
+constexpr int kResBM = 64;
+
+ISVD_DEVICE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+ISVD_DEVICE void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+ISVD_DEVICE void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+ISVD_DEVICE void mbar_wait(const uint64_t* b, uint32_t parity) {
+  for (uint32_t it = 0;; ++it) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 28)) __trap();  // a copy that never lands fails the launch instead of hanging
+  }
+}
+ISVD_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// One 64 x 32 warp tile over the whole K (K % 4 == 0).  Fragments of the next k-step are read from
+// shared memory while this step's FMAs issue.  kHalf: only the lower 16 columns (acc[.][0..1]).
+// KT / NPT: compile-time K and panel pitch (0: run-time), so every shared-memory address of the loop
+// is base + immediate (the run-time form spends one IMAD -- an FMA-pipe cycle -- per fragment load,
+// 16 % of the pipe at K = 100).
+template <bool kHalf, int KT, int NPT>
+ISVD_DEVICE void kres_tile(const float* __restrict__ a_base, const float* __restrict__ b0p,
+                           const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4]) {
+  const int K = KT ? KT : Krt, NP = NPT ? NPT : NPrt;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  auto lda2 = [&](float2 a[8], int k) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(a_base + (size_t)(8 * i) * K + k);
+  };
+  auto ldb = [&](float4& bl, float4& bh, int k) {
+    bl = *reinterpret_cast<const float4*>(b0p + (size_t)k * NP);
+    if constexpr (!kHalf) bh = *reinterpret_cast<const float4*>(b1p + (size_t)k * NP);
+  };
+  auto fma_step = [&](const float2 a[8], bool hi, float4 bl, float4 bh) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float av = hi ? a[i].y : a[i].x;
+      const float2 a2 = make_float2(av, av);
+      acc[i][0] = ffma2(a2, make_float2(bl.x, bl.y), acc[i][0]);
+      acc[i][1] = ffma2(a2, make_float2(bl.z, bl.w), acc[i][1]);
+      if constexpr (!kHalf) {
+        acc[i][2] = ffma2(a2, make_float2(bh.x, bh.y), acc[i][2]);
+        acc[i][3] = ffma2(a2, make_float2(bh.z, bh.w), acc[i][3]);
+      }
+    }
+  };
+  float2 a0[8], a1[8];
+  float4 bl0, bh0 = make_float4(0.f, 0.f, 0.f, 0.f), bl1, bh1 = bh0;
+  lda2(a0, 0);
+  ldb(bl0, bh0, 0);
+  auto block4 = [&](int k, int kn) {
+    ldb(bl1, bh1, k + 1);
+    fma_step(a0, false, bl0, bh0);
+    lda2(a1, k + 2);
+    ldb(bl0, bh0, k + 2);
+    fma_step(a0, true, bl1, bh1);
+    ldb(bl1, bh1, k + 3);
+    fma_step(a1, false, bl0, bh0);
+    lda2(a0, kn);
+    ldb(bl0, bh0, kn);
+    fma_step(a1, true, bl1, bh1);
+  };
+  if constexpr (KT != 0) {
+#pragma unroll
+    for (int k = 0; k < KT; k += 4) block4(k, k + 4 < KT ? k + 4 : k);  // the last prefetch re-reads valid data
+  } else {
+#pragma unroll 1
+    for (int k = 0; k < K; k += 4) block4(k, k + 4 < K ? k + 4 : k);
+  }
+}
+
+ISVD_DEVICE void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+// blockDim = 32 (compute warps + 1): warps 0 .. ncw-1 compute, warp ncw feeds the A ring.  No CTA
+// barrier after the start: a compute warp waits only for its tile's rows (full[slot]) and releases
+// the slot (empty[slot]) as soon as its k-loop has read them, before its stores, so the warps of
+// one SM sub-partition drift apart and one warp's epilogue overlaps the others' FMAs.  (With a
+// __syncthreads per tile, 18 % of the warp samples sat at the barrier: ncu, profiles/r02h_*.)
+// (14 warps put 4 on an SM sub-partition: at most 128 registers per thread.)
+template <int KT, int NPT>
+__global__ void __launch_bounds__(448, 1)
+    gemm_kres_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                     float* __restrict__ C, int64_t ldc, int64_t M, int N, int Krt, const float* __restrict__ row_scale,
+                     float alpha, const int* gate, const int32_t* __restrict__ out_map) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  extern __shared__ __align__(128) uint8_t kres_sm[];
+  const int ncw = (int)(blockDim.x >> 5) - 1;
+  const int K = KT ? KT : Krt;
+  const int NP = NPT ? NPT : 32 * ncw;  // 32 columns per compute warp
+  float* const Bs = reinterpret_cast<float*>(kres_sm);                       // [K][NP]
+  float* const As = Bs + (size_t)K * NP;                                      // [2][64][K]
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(As + 2 * kResBM * K);   // full[2], empty[2], bfull
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, t = lane & 3;
+  const int64_t ntile = (M + kResBM - 1) / kResBM;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], (uint32_t)ncw);
+    mbar_init(&bars[3], (uint32_t)ncw);
+    mbar_init(&bars[4], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t t0 = blockIdx.x, dt = gridDim.x;
+  if (warp == ncw) {
+    // ---------------------------------------------------------------- producer warp
+    if (lane == 0) mbar_expect_tx(&bars[4], (uint32_t)(K * N * 4));
+    __syncwarp();
+    for (int k = lane; k < K; k += 32) bulk_g2s(Bs + (size_t)k * NP, B + (int64_t)k * ldb, (uint32_t)(N * 4), &bars[4]);
+    int it = 0;
+    for (int64_t tl = t0; tl < ntile; tl += dt, ++it) {
+      const int slot = it & 1;
+      if (it >= 2) mbar_wait(&bars[2 + slot], (uint32_t)(((it >> 1) - 1) & 1));  // every compute warp released it
+      const int64_t m0 = tl * kResBM;
+      const int rows = (int)((M - m0) < kResBM ? (M - m0) : kResBM);
+      if (lane == 0) mbar_expect_tx(&bars[slot], (uint32_t)(rows * K * 4));
+      __syncwarp();
+      for (int e = lane; e < rows; e += 32)  // lane e copies rows e and e + 32
+        bulk_g2s(As + ((size_t)slot * kResBM + e) * K, A + (m0 + e) * lda, (uint32_t)(K * 4), &bars[slot]);
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ compute warps
+  const int c0 = 16 * warp + 4 * t, c1 = NP / 2 + c0;
+  const float* const b0p = Bs + c0;
+  const float* const b1p = Bs + c1;
+  mbar_wait(&bars[4], 0);
+  int it = 0;
+  for (int64_t tl = t0; tl < ntile; tl += dt, ++it) {
+    const int slot = it & 1;
+    mbar_wait(&bars[slot], (uint32_t)((it >> 1) & 1));
+    const float* const a_base = As + ((size_t)slot * kResBM + r) * K;
+    float2 acc[8][4];
+    if (NP / 2 + 16 * warp < N) kres_tile<false, KT, NPT>(a_base, b0p, b1p, K, NP, acc);
+    else kres_tile<true, KT, NPT>(a_base, b0p, b1p, K, NP, acc);  // the last warp's upper columns are padding
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[2 + slot]);  // this warp has read the slot
+    const int64_t m0 = tl * kResBM;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t gm = m0 + r + 8 * i;
+      if (gm >= M) continue;
+      float sc = alpha;
+      if (row_scale) sc *= row_scale[gm];
+      float* const crow = C + (out_map ? (int64_t)out_map[gm] : gm) * ldc;
+      if (c0 < N)
+        *reinterpret_cast<float4*>(crow + c0) =
+            make_float4(sc * acc[i][0].x, sc * acc[i][0].y, sc * acc[i][1].x, sc * acc[i][1].y);
+      if (c1 < N)
+        *reinterpret_cast<float4*>(crow + c1) =
+            make_float4(sc * acc[i][2].x, sc * acc[i][2].y, sc * acc[i][3].x, sc * acc[i][3].y);
+    }
+  }
+}
+
+// whether the K-resident kernel takes the product; *smem its dynamic shared memory
+bool gemm_kres_fits(int64_t N, int64_t K, size_t* smem) {
+  if (K < 16 || K > 128 || K % 4 || N % 4 || N <= 128 || N > 416) return false;
+  const int64_t NP = round_up(N, 32);
+  *smem = (size_t)(K * NP + 2 * kResBM * K) * 4 + 64;
+  return *smem <= 227 * 1024;
 }
 
 // ------------------------------------------------------------------ A^T B (fp64)
@@ -557,6 +753,39 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
                            int64_t N, int64_t K, const float* row_scale, float alpha, bool upper_tri_b,
                            const int* gate, cudaStream_t st, const int32_t* out_map) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  size_t kres_smem = 0;
+  static const char* kres_env = getenv("ISVD_GEMM_KRES");  // 0: the tiled kernel for short K too (A/B)
+  if (!upper_tri_b && !(kres_env && atoi(kres_env) == 0) && lda % 4 == 0 && ldb % 4 == 0 &&
+      ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && gemm_kres_fits(N, K, &kres_smem)) {
+    using KresFn = void (*)(const float*, int64_t, const float*, int64_t, float*, int64_t, int64_t, int, int,
+                            const float*, float, const int*, const int32_t*);
+    const int NP = (int)round_up(N, 32);
+    // compile-time shapes: config 4 (d = 100, l = 400) and config 2 (d = 128, l = 256)
+    KresFn fn = (K == 100 && NP == 416)   ? gemm_kres_kernel<100, 416>
+                : (K == 128 && NP == 256) ? gemm_kres_kernel<128, 256>
+                                          : gemm_kres_kernel<0, 0>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t ntile = ceil_div(M, kResBM);
+    const int grid = (int)(ntile < sms ? ntile : sms);
+    ++g_launches;
+    fn<<<grid, (unsigned)(NP + 32), kres_smem, st>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K, row_scale, alpha, gate,
+                                                     out_map);
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess && getenv("ISVD_TRACE")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, fn);
+      fprintf(stderr, "gemm_kres: %s regs %d maxthr %d static smem %zu maxdyn %d threads %d smem %zu\n",
+              cudaGetErrorString(le), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+              fa.maxDynamicSharedSizeBytes, NP + 32, kres_smem);
+    }
+    return le;
+  }
   if (N > 64 && round_up(N, 80) < round_up(N, 128)) {  // e.g. N = 400: 5 x 80 instead of 4 x 128
     // 16-deep K stages halve the CTA barriers for long K (Y R^-1: 12.0 -> 11.7 ms at config 4);
     // for short K (X G_j, K = d = 100) the 8-deep ones waste less on the ragged last stage

@@ -80,8 +80,30 @@ int main(int argc, char** argv) {
   }
   t = time_ms([&] { isvd::launch_atb(dZ, l, dZ, l, n, l, l, nullptr, true, ws, dOut, l, nullptr, 0, sms, nullptr, 0, false); });
   printf("Z^T Z fp64: %7.3f ms  %6.1f TFLOP/s (symmetric half)\n", t, 2.0 * n * l * l / 2 / 1e9 / t);
+  {
+    cudaError_t le = isvd::launch_gemm_tn(dX, d, dG, l, dC, l, n, l, d, nullptr, 1.f, false, nullptr, 0);
+    cudaError_t se = cudaDeviceSynchronize();
+    if (le != cudaSuccess || se != cudaSuccess) printf("X G launch: %s / %s\n", cudaGetErrorString(le), cudaGetErrorString(se));
+  }
   t = time_ms([&] { isvd::launch_gemm_tn(dX, d, dG, l, dC, l, n, l, d, nullptr, 1.f, false, nullptr, 0); });
-  printf("X G       : %7.3f ms  %6.1f TFLOP/s\n", t, gf / t);
+  {
+    // sampled fp64 check: rows from the first, a middle and the ragged last tile, every column
+    std::vector<float> Cs(l);
+    double worst = 0;
+    const int64_t rows[6] = {0, 63, 64, n / 2 + 7, n - 2, n - 1};
+    for (int64_t r : rows) {
+      cudaMemcpy(Cs.data(), dC + r * l, 4 * l, cudaMemcpyDeviceToHost);
+      for (int64_t j = 0; j < l; ++j) {
+        double ref = 0, mag = 0;
+        for (int64_t k = 0; k < d; ++k) {
+          ref += (double)X[r * d + k] * G[k * l + j];
+          mag += std::fabs((double)X[r * d + k] * G[k * l + j]);
+        }
+        worst = std::max(worst, std::fabs(Cs[j] - ref) / mag);
+      }
+    }
+    printf("X G       : %7.3f ms  %6.1f TFLOP/s   sampled worst err / sum|terms| %.2e\n", t, gf / t, worst);
+  }
   t = time_ms([&] { isvd::launch_gemm_tn(dZ, l, dR, l, dC, l, n, l, l, nullptr, 1.f, true, nullptr, 0); });
   printf("Y R^-1    : %7.3f ms  %6.1f TFLOP/s (triangular half)\n", t, 2.0 * n * l * l / 2 / 1e9 / t);
   cudaError_t e = cudaDeviceSynchronize();
