@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
   double* P = sm + (size_t)L.rows_max * l;         // kPanel x l (panel copy)
   double* colk = P + (size_t)kPanel * l;           // rows_max x kPanel
   __shared__ double s_misc[4];
+  __shared__ double s_pinv[kPanel], s_pblk[kPanel * kPanel];  // in-panel: 1 / r_kk, the diagonal block
   __shared__ double s_pmin, s_pmax;  // pivots factored by this CTA (probe mode)
   __shared__ int s_bad, s_remote_bad;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -690,51 +691,92 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
       const int own = B % L.CS, k0 = B * kPanel, kend = min(k0 + kPanel, l);
       const int lb = (B / L.CS) * kPanel;
       if (L.c == own) {
-        for (int kk = k0; kk < kend; ++kk) {
-          double* rk = A + (size_t)(lb + kk - k0) * l;
-          if (tid == 0) {
-            double piv = rk[kk];
-            int b = !(piv > tol) || !isfinite(piv);
-            if (b) s_bad = 1;
-            s_pmin = fmin(s_pmin, piv);
-            s_pmax = fmax(s_pmax, piv);
-            double rr = b ? 1.0 : sqrt(piv);
-            rk[kk] = rr;
-            s_misc[0] = 1.0 / rr;
+        // In-panel factorisation without a CTA barrier per column (round 2; the column-by-column
+        // form took 3 barriers and a serial pivot per column, 400 of them at l = 400): thread 0
+        // factors the nb x nb diagonal block in registers, then every other column of the panel
+        // is an independent nb-step forward substitution, one thread per column.  The operations
+        // on each entry and their order are those of the column-by-column form.
+        const int nbo = kend - k0;
+        if (tid == 0) {
+          double D[kPanel][kPanel];
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a)
+#pragma unroll
+            for (int b = 0; b < kPanel; ++b)
+              D[a][b] = (a < nbo && b < nbo && b >= a) ? A[(size_t)(lb + a) * l + k0 + b] : 0.0;
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a) {
+            if (a < nbo) {
+              const double piv = D[a][a];
+              const int b_ = !(piv > tol) || !isfinite(piv);
+              if (b_) s_bad = 1;
+              s_pmin = fmin(s_pmin, piv);
+              s_pmax = fmax(s_pmax, piv);
+              const double rr = b_ ? 1.0 : sqrt(piv);
+              const double inv = 1.0 / rr;
+              D[a][a] = rr;
+              s_pinv[a] = inv;
+#pragma unroll
+              for (int b = a + 1; b < kPanel; ++b) D[a][b] *= inv;
+#pragma unroll
+              for (int a2 = a + 1; a2 < kPanel; ++a2)
+#pragma unroll
+                for (int b = a2; b < kPanel; ++b) D[a2][b] -= D[a][a2] * D[a][b];
+            }
           }
-          __syncthreads();
-          const double inv = s_misc[0];
-          for (int j = kk + 1 + tid; j < l; j += nt) rk[j] *= inv;
-          __syncthreads();
-          const int nrem = kend - kk - 1;  // panel rows below kk
-          for (int t = tid; t < nrem * l; t += nt) {
-            int q = t / l, j = t - q * l;
-            int i2 = kk + 1 + q;
-            if (j >= i2) A[(size_t)(lb + i2 - k0) * l + j] -= rk[i2] * rk[j];
-          }
-          __syncthreads();
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a)
+#pragma unroll
+            for (int b = 0; b < kPanel; ++b) {
+              if (a < nbo && b < nbo && b >= a) A[(size_t)(lb + a) * l + k0 + b] = D[a][b];
+              s_pblk[a * kPanel + b] = D[a][b];
+            }
         }
+        __syncthreads();
+        for (int j = kend + tid; j < l; j += nt) {
+          double v[kPanel];
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a) v[a] = a < nbo ? A[(size_t)(lb + a) * l + j] : 0.0;
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a) {
+            if (a < nbo) {
+              v[a] *= s_pinv[a];
+#pragma unroll
+              for (int a2 = a + 1; a2 < kPanel; ++a2) v[a2] -= s_pblk[a * kPanel + a2] * v[a];
+            }
+          }
+#pragma unroll
+          for (int a = 0; a < kPanel; ++a)
+            if (a < nbo) A[(size_t)(lb + a) * l + j] = v[a];
+        }
+        __syncthreads();
       }
       cl.sync();  // panel B final
       const double* rem = cl.map_shared_rank(A, own) + (size_t)lb * l;
       if (tid == 0) s_remote_bad = *cl.map_shared_rank(&s_bad, own);
       const int nb = kend - k0;
-      for (int t = tid; t < nb * (l - k0); t += nt) {
-        int q = t / (l - k0), j = k0 + (t - q * (l - k0));
-        P[(size_t)q * l + j] = rem[(size_t)q * l + j];
+      {  // warp w copies panel row w % kPanel (two warps per row at 512 threads)
+        const int w = tid >> 5, q = w % kPanel, part = w / kPanel, parts = (nt >> 5) / kPanel;
+        if (q < nb && part < parts)
+          for (int j = k0 + part * 32 + (tid & 31); j < l; j += 32 * parts) P[(size_t)q * l + j] = rem[(size_t)q * l + j];
       }
       __syncthreads();
       if (s_remote_bad) { bad = 1; break; }
       // rank-nb update of own rows i >= kend, columns j >= i
-      for (int t = tid; t < my_rows * (l - kend); t += nt) {
-        int r = t / (l - kend), j = kend + (t - r * (l - kend));
-        int gi = L.global_row(r);
-        if (gi < kend || gi >= l || j < gi) continue;
-        double s = 0.0;
+      // (a warp per row, lanes over its columns j >= i: no index division per entry)
+      for (int r = tid >> 5; r < my_rows; r += nt >> 5) {
+        const int gi = L.global_row(r);
+        if (gi < kend || gi >= l) continue;
+        double pg[kPanel];
 #pragma unroll
-        for (int q = 0; q < kPanel; ++q)
-          if (q < nb) s += P[(size_t)q * l + gi] * P[(size_t)q * l + j];
-        A[(size_t)r * l + j] -= s;
+        for (int q = 0; q < kPanel; ++q) pg[q] = q < nb ? P[(size_t)q * l + gi] : 0.0;
+        for (int j = gi + (tid & 31); j < l; j += 32) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < kPanel; ++q)
+            if (q < nb) s += pg[q] * P[(size_t)q * l + j];
+          A[(size_t)r * l + j] -= s;
+        }
       }
       __syncthreads();
     }
@@ -781,30 +823,66 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
     // Cholesky (whose last panel is still being read) to the inverse needs a barrier
     if (B == L.nblk - 1) cl.sync();
     if (L.c == own) {
-      for (int kk = kend - 1; kk >= k0; --kk) {
-        double* rk = A + (size_t)(lb + kk - k0) * l;
-        const double d = rk[kk];
-        __syncthreads();
-        const double inv = 1.0 / d;
-        for (int j = kk + 1 + tid; j < l; j += nt) rk[j] *= inv;
-        if (tid == 0) rk[kk] = inv;
-        // rows of this panel above kk: save R[i][kk], then eliminate
-        for (int q = tid; q < kk - k0; q += nt) colk[q] = A[(size_t)(lb + q) * l + kk];
-        __syncthreads();
-        for (int t = tid; t < (kk - k0) * (l - kk); t += nt) {
-          int q = t / (l - kk), j = kk + (t - q * (l - kk));
-          double rik = colk[q];
-          double* ai = A + (size_t)(lb + q) * l;
-          ai[j] = (j == kk) ? -rik * inv : ai[j] - rik * rk[j];
+      // the panel's own Gauss-Jordan steps, as above: thread 0 transforms the nb x nb diagonal block
+      // in registers (keeping the original block for the others), then one thread per remaining
+      // column runs the nb-step back substitution
+      __syncthreads();
+      if (tid == 0) {
+        double D[kPanel][kPanel];
+#pragma unroll
+        for (int a = 0; a < kPanel; ++a)
+#pragma unroll
+          for (int b = 0; b < kPanel; ++b) {
+            D[a][b] = (a < nb && b < nb && b >= a) ? A[(size_t)(lb + a) * l + k0 + b] : 0.0;
+            s_pblk[a * kPanel + b] = D[a][b];
+          }
+#pragma unroll
+        for (int a = kPanel - 1; a >= 0; --a) {
+          if (a < nb) {
+            const double inv = 1.0 / D[a][a];
+            s_pinv[a] = inv;
+#pragma unroll
+            for (int b = a + 1; b < kPanel; ++b) D[a][b] *= inv;
+            D[a][a] = inv;
+#pragma unroll
+            for (int q = 0; q < a; ++q) {
+              const double rik = D[q][a];
+#pragma unroll
+              for (int b = a; b < kPanel; ++b) D[q][b] = (b == a) ? -rik * inv : D[q][b] - rik * D[a][b];
+            }
+          }
         }
-        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < kPanel; ++a)
+#pragma unroll
+          for (int b = 0; b < kPanel; ++b)
+            if (a < nb && b < nb && b >= a) A[(size_t)(lb + a) * l + k0 + b] = D[a][b];
       }
+      __syncthreads();
+      for (int j = kend + tid; j < l; j += nt) {
+        double v[kPanel];
+#pragma unroll
+        for (int a = 0; a < kPanel; ++a) v[a] = a < nb ? A[(size_t)(lb + a) * l + j] : 0.0;
+#pragma unroll
+        for (int a = kPanel - 1; a >= 0; --a) {
+          if (a < nb) {
+            v[a] *= s_pinv[a];
+#pragma unroll
+            for (int q = 0; q < a; ++q) v[q] -= s_pblk[q * kPanel + a] * v[a];
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < kPanel; ++a)
+          if (a < nb) A[(size_t)(lb + a) * l + j] = v[a];
+      }
+      __syncthreads();
     }
     cl.sync();  // panel rows of X final
     const double* rem = cl.map_shared_rank(A, own) + (size_t)lb * l;
-    for (int t = tid; t < nb * (l - k0); t += nt) {
-      int q = t / (l - k0), j = k0 + (t - q * (l - k0));
-      P[(size_t)q * l + j] = rem[(size_t)q * l + j];
+    {
+      const int w = tid >> 5, q = w % kPanel, part = w / kPanel, parts = (nt >> 5) / kPanel;
+      if (q < nb && part < parts)
+        for (int j = k0 + part * 32 + (tid & 31); j < l; j += 32 * parts) P[(size_t)q * l + j] = rem[(size_t)q * l + j];
     }
     // save R[i][k0..kend) of own rows i < k0
     for (int t = tid; t < my_rows * kPanel; t += nt) {
@@ -813,16 +891,20 @@ __global__ void __launch_bounds__(512) chol_inv_cluster_kernel(const double* __r
       colk[t] = (gi < k0 && q < nb) ? A[(size_t)r * l + k0 + q] : 0.0;
     }
     __syncthreads();
-    for (int t = tid; t < my_rows * (l - k0); t += nt) {
-      int r = t / (l - k0), j = k0 + (t - r * (l - k0));
-      int gi = L.global_row(r);
+    for (int r = tid >> 5; r < my_rows; r += nt >> 5) {
+      const int gi = L.global_row(r);
       if (gi >= k0) continue;
-      double s = 0.0;
+      double ck[kPanel];
 #pragma unroll
-      for (int q = 0; q < kPanel; ++q)
-        if (q < nb && k0 + q <= j) s += colk[(size_t)r * kPanel + q] * P[(size_t)q * l + j];
-      double* a = A + (size_t)r * l + j;
-      *a = (j >= kend ? *a : 0.0) - s;
+      for (int q = 0; q < kPanel; ++q) ck[q] = colk[(size_t)r * kPanel + q];
+      for (int j = k0 + (tid & 31); j < l; j += 32) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kPanel; ++q)
+          if (q < nb && k0 + q <= j) s += ck[q] * P[(size_t)q * l + j];
+        double* a = A + (size_t)r * l + j;
+        *a = (j >= kend ? *a : 0.0) - s;
+      }
     }
     __syncthreads();
   }

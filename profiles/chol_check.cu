@@ -3,6 +3,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I paper_2111_06312_b200/csrc -I include \
 //        profiles/chol_check.cu -L paper_2111_06312_b200 -l:libisvd.so \
 //        -Xlinker -rpath='$ORIGIN/../paper_2111_06312_b200' -o build/chol_check
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -12,7 +13,7 @@
 #include "common.cuh"
 
 int main() {
-  for (int l : {256, 400}) {
+  for (int l : {100, 250, 256, 400}) {
     const int ld = (l + 3) / 4 * 4;
     std::mt19937 rng(l);
     std::normal_distribution<double> nd;
@@ -60,8 +61,18 @@ int main() {
           num += (s - G[(size_t)i * l + j]) * (s - G[(size_t)i * l + j]);
           den += G[(size_t)i * l + j] * G[(size_t)i * l + j];
         }
-      printf("l=%d cluster %2d: %s %.3f ms  |R^T R - G| / |G| = %.2e\n", l, cs, cudaGetErrorString(e), ms / 10,
-             std::sqrt(num / den));
+      // the fp32 inverse: |R Rinv - I|_max over sampled rows (fp32 storage of Rinv: ~1e-7 kappa(R))
+      std::vector<float> Ri((size_t)ld * ld);
+      cudaMemcpy(Ri.data(), Rinv, 4 * (size_t)ld * ld, cudaMemcpyDeviceToHost);
+      double worst = 0;
+      for (int i = 0; i < l; i += 3)
+        for (int j = 0; j < l; ++j) {
+          double s = 0;
+          for (int k = i; k < l; ++k) s += R[(size_t)i * l + k] * (double)Ri[(size_t)k * ld + j];
+          worst = std::max(worst, std::fabs(s - (i == j ? 1.0 : 0.0)));
+        }
+      printf("l=%d cluster %2d: %s %.3f ms  |R^T R - G| / |G| = %.2e  max|R Rinv - I| = %.2e\n", l, cs,
+             cudaGetErrorString(e), ms / 10, std::sqrt(num / den), worst);
     }
   }
   return 0;

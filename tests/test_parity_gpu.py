@@ -480,6 +480,34 @@ def test_materialised_nc_equals_implicit(ctx):
     opm.close()
 
 
+@pytest.mark.parametrize("n,d,widths", [(1000, 100, (400, 132, 416, 200)), (777, 128, (256, 260)), (64, 36, (132,)),
+                                         (4097, 16, (400,)), (130, 124, (388,))])
+def test_k_resident_gemm_shapes(ctx, n, d, widths):
+    """The K-resident persistent SIMT GEMM (X G_j for d <= 128, widths 132 .. 416): an NC operator with
+    L = 0 is M = X, so M G = X G is that kernel alone.  Compile-time shapes (d = 100 / l = 400,
+    d = 128 / l = 256), run-time shapes, ragged last row tiles (n not a multiple of 64), a single
+    partial tile, more tiles than SMs, a last warp with padding columns; every entry against the
+    fp64 product."""
+    import paper_2111_06312_b200 as isvd_mod
+
+    rng = np.random.default_rng(n + d)
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = ((np.arange(n) + 1) % n).astype(np.int32)  # a ring: the graph is unused at L = 0
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    graph = isvd_mod.Graph(ctx, n, torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda())
+    op = isvd_mod.NC(graph, torch.from_numpy(X).cuda(), 0)
+    for w in widths:
+        G = rng.standard_normal((d, w)).astype(np.float32)
+        out = _to_np(op.matmul(torch.from_numpy(G).cuda()))
+        ref = X.astype(np.float64) @ G.astype(np.float64)
+        assert out.shape == ref.shape
+        mag = np.abs(X).astype(np.float64) @ np.abs(G).astype(np.float64)
+        assert np.max(np.abs(out - ref) / mag) <= 4e-7, (n, d, w)
+        assert_product(out, ref)
+    op.close()
+    graph.close()
+
+
 # --------------------------------------------- label re-use NC operator (SURVEY 8(f) f2)
 
 
