@@ -1067,6 +1067,13 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
     if (rows > 0) {
       dim3 grid((unsigned)(t.ta * t.tb), (unsigned)t.chunks);
       ++g_launches;
+      // 4 x 16 register tiles at 100 x 80 (125-thread CTAs): 5 shared-memory float4 reads per 32 paired
+      // FMAs instead of 3 per 16 -- the 4 x 8 form is bound by shared-memory wavefronts (a float4 read
+      // costs a wavefront per quarter-warp: ~12 per warp and k-step against 32 FMA-pipe cycles).  The
+      // same per-entry sums in the same order: X^T Z_j 4.70 -> 4.47 ms (profiles/r02h_dense_check.txt).
+      // ISVD_ATB_TN16=0: the 4 x 8 form; 2: three CTAs per SM.
+      static const char* tn16_env = getenv("ISVD_ATB_TN16");
+      const int tn16 = tn16_env ? atoi(tn16_env) : 1;
 #define ISVD_ATB_F32(BM_, BN_, TM_, TN_)                                                                \
   if (t.bm == BM_ && t.bn == BN_ && t.tm == TM_ && t.tn == TN_)                                          \
     atb_f32_kernel<BM_, BN_, TM_, TN_><<<grid, (BM_ / TM_) * (BN_ / TN_), 0, st>>>(                       \
@@ -1076,6 +1083,12 @@ cudaError_t launch_atb(const float* A, int64_t lda, const float* B, int64_t ldb,
       else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8 && row_scale)  // 250 threads, full warps
         atb_f32_kernel<100, 80, 4, 8, 3><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, row_scale, (int)t.tb,
                                                               t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+      else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8 && !row_scale && tn16 == 1)
+        atb_f32_kernel<100, 80, 4, 16, 4, false><<<grid, 125, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr, (int)t.tb,
+                                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
+      else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8 && !row_scale && tn16 == 2)
+        atb_f32_kernel<100, 80, 4, 16, 3, false><<<grid, 125, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr, (int)t.tb,
+                                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
       else if (t.bm == 100 && t.bn == 80 && t.tm == 4 && t.tn == 8)  // X^T Z_j with a pre-scaled X: 4.7 ms
         atb_f32_kernel<100, 80, 4, 8, 4, false><<<grid, 250, 0, st>>>(A, lda, B, ldb, rows, Ka, Kb, nullptr, (int)t.tb,
                                                                      t.chunk_rows, ws32, ws_lda, ws_ld, gate);
