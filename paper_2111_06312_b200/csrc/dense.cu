@@ -239,37 +239,44 @@ ISVD_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* 
 // KT / NPT: compile-time K and panel pitch (0: run-time), so every shared-memory address of the loop
 // is base + immediate (the run-time form spends one IMAD -- an FMA-pipe cycle -- per fragment load,
 // 16 % of the pipe at K = 100).
-template <bool kHalf, int KT, int NPT>
-ISVD_DEVICE void kres_tile(const float* __restrict__ a_base, const float* __restrict__ b0p,
-                           const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4]) {
+// MODE: 0 both column halves, 1 the lower 16 columns only (acc[.][0..1]), 2 the upper only
+// (acc[.][2..3]).  APT: compile-time A row pitch in floats (0: K).  ZERO: clear acc first.
+template <int MODE, int KT, int NPT, int APT = 0, bool ZERO = true>
+ISVD_DEVICE void kres_tile_m(const float* __restrict__ a_base, const float* __restrict__ b0p,
+                             const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4]) {
   const int K = KT ? KT : Krt, NP = NPT ? NPT : NPrt;
+  const int AP = APT ? APT : K;
+  if constexpr (ZERO) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  }
   auto lda2 = [&](float2 a[8], int k) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(a_base + (size_t)(8 * i) * K + k);
+    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float2*>(a_base + (size_t)(8 * i) * AP + k);
   };
   auto ldb = [&](float4& bl, float4& bh, int k) {
-    bl = *reinterpret_cast<const float4*>(b0p + (size_t)k * NP);
-    if constexpr (!kHalf) bh = *reinterpret_cast<const float4*>(b1p + (size_t)k * NP);
+    if constexpr (MODE != 2) bl = *reinterpret_cast<const float4*>(b0p + (size_t)k * NP);
+    if constexpr (MODE != 1) bh = *reinterpret_cast<const float4*>(b1p + (size_t)k * NP);
   };
   auto fma_step = [&](const float2 a[8], bool hi, float4 bl, float4 bh) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float av = hi ? a[i].y : a[i].x;
       const float2 a2 = make_float2(av, av);
-      acc[i][0] = ffma2(a2, make_float2(bl.x, bl.y), acc[i][0]);
-      acc[i][1] = ffma2(a2, make_float2(bl.z, bl.w), acc[i][1]);
-      if constexpr (!kHalf) {
+      if constexpr (MODE != 2) {
+        acc[i][0] = ffma2(a2, make_float2(bl.x, bl.y), acc[i][0]);
+        acc[i][1] = ffma2(a2, make_float2(bl.z, bl.w), acc[i][1]);
+      }
+      if constexpr (MODE != 1) {
         acc[i][2] = ffma2(a2, make_float2(bh.x, bh.y), acc[i][2]);
         acc[i][3] = ffma2(a2, make_float2(bh.z, bh.w), acc[i][3]);
       }
     }
   };
   float2 a0[8], a1[8];
-  float4 bl0, bh0 = make_float4(0.f, 0.f, 0.f, 0.f), bl1, bh1 = bh0;
+  float4 bl0 = make_float4(0.f, 0.f, 0.f, 0.f), bh0 = bl0, bl1 = bl0, bh1 = bl0;
   lda2(a0, 0);
   ldb(bl0, bh0, 0);
   auto block4 = [&](int k, int kn) {
@@ -291,6 +298,11 @@ ISVD_DEVICE void kres_tile(const float* __restrict__ a_base, const float* __rest
 #pragma unroll 1
     for (int k = 0; k < K; k += 4) block4(k, k + 4 < K ? k + 4 : k);
   }
+}
+template <bool kHalf, int KT, int NPT>
+ISVD_DEVICE void kres_tile(const float* __restrict__ a_base, const float* __restrict__ b0p,
+                           const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4]) {
+  kres_tile_m<kHalf ? 1 : 0, KT, NPT>(a_base, b0p, b1p, Krt, NPrt, acc);
 }
 
 ISVD_DEVICE void mbar_arrive(uint64_t* b) {
@@ -378,6 +390,116 @@ __global__ void __launch_bounds__(448, 1)
             make_float4(sc * acc[i][2].x, sc * acc[i][2].y, sc * acc[i][3].x, sc * acc[i][3].y);
     }
   }
+}
+
+// ------------------------------------------------------------------ GEMM, K-chunked (round 2)
+// The same warp tiling and producer / consumer ring for a long contraction (Y R^-1 of the
+// CholeskyQR apply, K = l = 400): the C tile (64 x N) stays in registers while K-chunks of KC
+// k-steps -- 64 x KC of A and KC x N of B per stage, two stages -- stream through shared memory
+// (B is re-read from L2 for every row tile: 2.5 TB/s over the GPU, inside what L2 delivers).
+// upper_tri_b: chunk c only touches columns >= KC c, so a warp skips a 16-column group whose
+// columns all lie left of the chunk (warp-uniform), and the producer copies only the columns from
+// the first live group on.  A rows are padded to KC + 4 floats in shared memory (KC = 40: pitch 44
+// = 12 mod 32, the 8 row groups of an A fragment read hit 8 distinct bank pairs).
+template <int KC, int NPT>
+__global__ void __launch_bounds__(448, 1)
+    gemm_kchunk_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
+                       float* __restrict__ C, int64_t ldc, int64_t M, int N, int K, const float* __restrict__ row_scale,
+                       float alpha, int upper_tri_b, const int* gate, const int32_t* __restrict__ out_map) {
+  if (gate && *((volatile const int*)gate) == 0) return;
+  extern __shared__ __align__(128) uint8_t kres_sm[];
+  constexpr int AP = KC + 4;
+  const int ncw = (int)(blockDim.x >> 5) - 1;
+  const int NP = NPT ? NPT : 32 * ncw;
+  float* const Bs = reinterpret_cast<float*>(kres_sm);                        // [2][KC][NP]
+  float* const As = Bs + (size_t)2 * KC * NP;                                  // [2][64][AP]
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(As + 2 * kResBM * AP);   // full[2], empty[2]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, t = lane & 3;
+  const int64_t ntile = (M + kResBM - 1) / kResBM;
+  const int nch = K / KC;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], (uint32_t)ncw);
+    mbar_init(&bars[3], (uint32_t)ncw);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t t0 = blockIdx.x, dt = gridDim.x;
+  if (warp == ncw) {
+    // ---------------------------------------------------------------- producer warp
+    uint32_t g = 0;
+    for (int64_t tl = t0; tl < ntile; tl += dt) {
+      const int64_t m0 = tl * kResBM;
+      const int rows = (int)((M - m0) < kResBM ? (M - m0) : kResBM);
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int st = (int)(g & 1u);
+        if (g >= 2) mbar_wait(&bars[2 + st], ((g >> 1) - 1) & 1u);
+        const int k0 = c * KC;
+        const int cb = upper_tri_b ? (k0 / 16) * 16 : 0;  // first live column
+        if (lane == 0) mbar_expect_tx(&bars[st], (uint32_t)(rows * KC * 4 + KC * (N - cb) * 4));
+        __syncwarp();
+        for (int e = lane; e < rows; e += 32)
+          bulk_g2s(As + ((size_t)st * kResBM + e) * AP, A + (m0 + e) * lda + k0, (uint32_t)(KC * 4), &bars[st]);
+        for (int k = lane; k < KC; k += 32)
+          bulk_g2s(Bs + ((size_t)st * KC + k) * NP + cb, B + (int64_t)(k0 + k) * ldb + cb, (uint32_t)((N - cb) * 4),
+                   &bars[st]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ compute warps
+  const int c0 = 16 * warp + 4 * t, c1 = NP / 2 + c0;
+  const bool hi_cols = NP / 2 + 16 * warp < N;  // the last warp's upper columns are padding
+  uint32_t g = 0;
+  for (int64_t tl = t0; tl < ntile; tl += dt) {
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int c = 0; c < nch; ++c, ++g) {
+      const int st = (int)(g & 1u);
+      mbar_wait(&bars[st], (g >> 1) & 1u);
+      const int k0 = c * KC;
+      const bool lo_on = !upper_tri_b || 16 * warp + 16 > k0;
+      const bool hi_on = hi_cols && (!upper_tri_b || NP / 2 + 16 * warp + 16 > k0);
+      const float* const a_base = As + ((size_t)st * kResBM + r) * AP;
+      const float* const b0p = Bs + (size_t)st * KC * NP + c0;
+      const float* const b1p = Bs + (size_t)st * KC * NP + c1;
+      if (lo_on && hi_on) kres_tile_m<0, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
+      else if (hi_on) kres_tile_m<2, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
+      else if (lo_on) kres_tile_m<1, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[2 + st]);
+    }
+    const int64_t m0 = tl * kResBM;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t gm = m0 + r + 8 * i;
+      if (gm >= M) continue;
+      float sc = alpha;
+      if (row_scale) sc *= row_scale[gm];
+      float* const crow = C + (out_map ? (int64_t)out_map[gm] : gm) * ldc;
+      if (c0 < N)
+        *reinterpret_cast<float4*>(crow + c0) =
+            make_float4(sc * acc[i][0].x, sc * acc[i][0].y, sc * acc[i][1].x, sc * acc[i][1].y);
+      if (c1 < N)
+        *reinterpret_cast<float4*>(crow + c1) =
+            make_float4(sc * acc[i][2].x, sc * acc[i][2].y, sc * acc[i][3].x, sc * acc[i][3].y);
+    }
+  }
+}
+
+// whether the K-chunked kernel takes the product (KC = 40 or 32); *smem its dynamic shared memory
+int gemm_kchunk_kc(int64_t N, int64_t K, size_t* smem) {
+  if (K < 160 || N % 4 || N <= 128 || N > 416) return 0;
+  const int kc = K % 40 == 0 ? 40 : (K % 32 == 0 ? 32 : 0);
+  if (!kc) return 0;
+  const int64_t NP = round_up(N, 32);
+  *smem = (size_t)(2 * kc * NP + 2 * kResBM * (kc + 4)) * 4 + 64;
+  return *smem <= 227 * 1024 ? kc : 0;
 }
 
 // whether the K-resident kernel takes the product; *smem its dynamic shared memory
@@ -785,6 +907,31 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
               fa.maxDynamicSharedSizeBytes, NP + 32, kres_smem);
     }
     return le;
+  }
+  size_t kch_smem = 0;
+  static const char* kch_env = getenv("ISVD_GEMM_KCHUNK");  // 0: the tiled kernel for long K (A/B)
+  const int kc = (kch_env && atoi(kch_env) == 0) || lda % 4 || ldb % 4 || (uintptr_t)A % 16 || (uintptr_t)B % 16
+                     ? 0
+                     : gemm_kchunk_kc(N, K, &kch_smem);
+  if (kc) {
+    using KchFn = void (*)(const float*, int64_t, const float*, int64_t, float*, int64_t, int64_t, int, int,
+                           const float*, float, int, const int*, const int32_t*);
+    const int NP = (int)round_up(N, 32);
+    KchFn fn = kc == 40 ? (NP == 416 ? gemm_kchunk_kernel<40, 416> : gemm_kchunk_kernel<40, 0>)
+                        : (NP == 256 ? gemm_kchunk_kernel<32, 256> : gemm_kchunk_kernel<32, 0>);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t ntile = ceil_div(M, kResBM);
+    const int grid = (int)(ntile < sms ? ntile : sms);
+    ++g_launches;
+    fn<<<grid, (unsigned)(NP + 32), kch_smem, st>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K, row_scale, alpha,
+                                                    upper_tri_b ? 1 : 0, gate, out_map);
+    return cudaGetLastError();
   }
   if (N > 64 && round_up(N, 80) < round_up(N, 128)) {  // e.g. N = 400: 5 x 80 instead of 4 x 128
     // 16-deep K stages halve the CTA barriers for long K (Y R^-1: 12.0 -> 11.7 ms at config 4);

@@ -105,7 +105,24 @@ int main(int argc, char** argv) {
     printf("X G       : %7.3f ms  %6.1f TFLOP/s   sampled worst err / sum|terms| %.2e\n", t, gf / t, worst);
   }
   t = time_ms([&] { isvd::launch_gemm_tn(dZ, l, dR, l, dC, l, n, l, l, nullptr, 1.f, true, nullptr, 0); });
-  printf("Y R^-1    : %7.3f ms  %6.1f TFLOP/s (triangular half)\n", t, 2.0 * n * l * l / 2 / 1e9 / t);
+  {
+    std::vector<float> Cs(l);
+    double worst = 0;
+    const int64_t rows[6] = {0, 63, 64, n / 2 + 7, n - 2, n - 1};
+    for (int64_t r : rows) {
+      cudaMemcpy(Cs.data(), dC + r * l, 4 * l, cudaMemcpyDeviceToHost);
+      for (int64_t j = 0; j < l; ++j) {
+        double ref = 0, mag = 0;
+        for (int64_t k = 0; k <= j; ++k) {
+          ref += (double)Z[r * l + k] * R[k * l + j];
+          mag += std::fabs((double)Z[r * l + k] * R[k * l + j]);
+        }
+        worst = std::max(worst, std::fabs(Cs[j] - ref) / mag);
+      }
+    }
+    printf("Y R^-1    : %7.3f ms  %6.1f TFLOP/s (triangular half)   sampled worst err / sum|terms| %.2e\n", t,
+           2.0 * n * l * l / 2 / 1e9 / t, worst);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;

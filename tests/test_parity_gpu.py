@@ -481,9 +481,12 @@ def test_materialised_nc_equals_implicit(ctx):
 
 
 @pytest.mark.parametrize("n,d,widths", [(1000, 100, (400, 132, 416, 200)), (777, 128, (256, 260)), (64, 36, (132,)),
-                                         (4097, 16, (400,)), (130, 124, (388,))])
+                                         (4097, 16, (400,)), (130, 124, (388,)),
+                                         # K-chunked streaming form (d >= 160; chunks of 40 or 32 k-steps)
+                                         (1000, 200, (400, 132)), (333, 192, (256, 300)), (9600, 160, (416,))])
 def test_k_resident_gemm_shapes(ctx, n, d, widths):
-    """The K-resident persistent SIMT GEMM (X G_j for d <= 128, widths 132 .. 416): an NC operator with
+    """The K-resident (d <= 128) and K-chunked (d >= 160) persistent SIMT GEMMs (widths 132 .. 416; the
+    triangular K-chunked form is the CholeskyQR apply of every isvd test with l >= 160): an NC operator with
     L = 0 is M = X, so M G = X G is that kernel alone.  Compile-time shapes (d = 100 / l = 400,
     d = 128 / l = 256), run-time shapes, ragged last row tiles (n not a multiple of 64), a single
     partial tile, more tiles than SMs, a last warp with padding columns; every entry against the
