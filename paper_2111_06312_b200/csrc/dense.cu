@@ -243,9 +243,9 @@ ISVD_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* 
 // (acc[.][2..3]).  APT: compile-time A row pitch in floats (0: K).  ZERO: clear acc first.
 template <int MODE, int KT, int NPT, int APT = 0, bool ZERO = true>
 ISVD_DEVICE void kres_tile_m(const float* __restrict__ a_base, const float* __restrict__ b0p,
-                             const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4]) {
+                             const float* __restrict__ b1p, int Krt, int NPrt, float2 acc[8][4], int APrt = 0) {
   const int K = KT ? KT : Krt, NP = NPT ? NPT : NPrt;
-  const int AP = APT ? APT : K;
+  const int AP = APT ? APT : (APrt ? APrt : K);
   if constexpr (ZERO) {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -395,84 +395,112 @@ __global__ void __launch_bounds__(448, 1)
 // ------------------------------------------------------------------ GEMM, K-chunked (round 2)
 // The same warp tiling and producer / consumer ring for a long contraction (Y R^-1 of the
 // CholeskyQR apply, K = l = 400): the C tile (64 x N) stays in registers while K-chunks of KC
-// k-steps -- 64 x KC of A and KC x N of B per stage, two stages -- stream through shared memory
+// k-steps of B (KC x N per stage, as many stages as fit beside the A tile: 3 at KC = 20, N = 400) stream through shared memory; the 64 x K row tile of A is copied once per tile
 // (B is re-read from L2 for every row tile: 2.5 TB/s over the GPU, inside what L2 delivers).
 // upper_tri_b: chunk c only touches columns >= KC c, so a warp skips a 16-column group whose
 // columns all lie left of the chunk (warp-uniform), and the producer copies only the columns from
-// the first live group on.  A rows are padded to KC + 4 floats in shared memory (KC = 40: pitch 44
-// = 12 mod 32, the 8 row groups of an A fragment read hit 8 distinct bank pairs).
-template <int KC, int NPT>
+// the first live group on.  A rows are padded to K + 4 floats in shared memory (the 8 row groups of
+// an A fragment read hit 8 distinct bank pairs).  Measured on the way: A and B per chunk in two
+// stages of 40 k-steps left the compute warps waiting for data 29 % of the time (11.1 ms; ncu), five
+// stages of 20 k-steps with per-chunk 80-byte A row copies ran 15.9 ms (1,680 small bulk copies per
+// tile): hence whole A rows once per tile.
+template <int KC, int APT, int NPT>
 __global__ void __launch_bounds__(448, 1)
     gemm_kchunk_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
                        float* __restrict__ C, int64_t ldc, int64_t M, int N, int K, const float* __restrict__ row_scale,
-                       float alpha, int upper_tri_b, const int* gate, const int32_t* __restrict__ out_map) {
+                       float alpha, int upper_tri_b, int S, const int* gate, const int32_t* __restrict__ out_map) {
   if (gate && *((volatile const int*)gate) == 0) return;
   extern __shared__ __align__(128) uint8_t kres_sm[];
-  constexpr int AP = KC + 4;
   const int ncw = (int)(blockDim.x >> 5) - 1;
   const int NP = NPT ? NPT : 32 * ncw;
-  float* const Bs = reinterpret_cast<float*>(kres_sm);                        // [2][KC][NP]
-  float* const As = Bs + (size_t)2 * KC * NP;                                  // [2][64][AP]
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(As + 2 * kResBM * AP);   // full[2], empty[2]
+  const int AP = APT ? APT : K + 4;
+  float* const Bs = reinterpret_cast<float*>(kres_sm);                        // [S][KC][NP]
+  float* const As = Bs + (size_t)S * KC * NP;                                  // [64][AP]: the whole row tile
+  uint64_t* const full = reinterpret_cast<uint64_t*>(As + (size_t)kResBM * AP);
+  uint64_t* const empty = full + S;
+  uint64_t* const a_full = empty + S;
+  uint64_t* const a_empty = a_full + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = lane >> 2, t = lane & 3;
   const int64_t ntile = (M + kResBM - 1) / kResBM;
   const int nch = K / KC;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], (uint32_t)ncw);
-    mbar_init(&bars[3], (uint32_t)ncw);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], (uint32_t)ncw);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, (uint32_t)ncw);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int64_t t0 = blockIdx.x, dt = gridDim.x;
+  int st = 0;
+  uint32_t ph = 0;  // ring slot and the parity of its current use
   if (warp == ncw) {
     // ---------------------------------------------------------------- producer warp
-    uint32_t g = 0;
-    for (int64_t tl = t0; tl < ntile; tl += dt) {
+    bool first_lap = true;
+    uint32_t it = 0;
+    for (int64_t tl = t0; tl < ntile; tl += dt, ++it) {
       const int64_t m0 = tl * kResBM;
       const int rows = (int)((M - m0) < kResBM ? (M - m0) : kResBM);
-      for (int c = 0; c < nch; ++c, ++g) {
-        const int st = (int)(g & 1u);
-        if (g >= 2) mbar_wait(&bars[2 + st], ((g >> 1) - 1) & 1u);
+      if (it > 0) mbar_wait(a_empty, (it - 1) & 1u);  // every compute warp is done with the previous tile's rows
+      if (lane == 0) mbar_expect_tx(a_full, (uint32_t)(rows * K * 4));
+      __syncwarp();
+      for (int e = lane; e < rows; e += 32) bulk_g2s(As + (size_t)e * AP, A + (m0 + e) * lda, (uint32_t)(K * 4), a_full);
+      for (int c = 0; c < nch; ++c) {
+        if (!first_lap) mbar_wait(&empty[st], ph ^ 1u);  // every compute warp released the previous use
         const int k0 = c * KC;
         const int cb = upper_tri_b ? (k0 / 16) * 16 : 0;  // first live column
-        if (lane == 0) mbar_expect_tx(&bars[st], (uint32_t)(rows * KC * 4 + KC * (N - cb) * 4));
+        if (lane == 0) mbar_expect_tx(&full[st], (uint32_t)(KC * (N - cb) * 4));
         __syncwarp();
-        for (int e = lane; e < rows; e += 32)
-          bulk_g2s(As + ((size_t)st * kResBM + e) * AP, A + (m0 + e) * lda + k0, (uint32_t)(KC * 4), &bars[st]);
         for (int k = lane; k < KC; k += 32)
           bulk_g2s(Bs + ((size_t)st * KC + k) * NP + cb, B + (int64_t)(k0 + k) * ldb + cb, (uint32_t)((N - cb) * 4),
-                   &bars[st]);
+                   &full[st]);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1u;
+          first_lap = false;
+        }
       }
     }
     return;
   }
   // ------------------------------------------------------------------ compute warps
-  const int c0 = 16 * warp + 4 * t, c1 = NP / 2 + c0;
-  const bool hi_cols = NP / 2 + 16 * warp < N;  // the last warp's upper columns are padding
-  uint32_t g = 0;
-  for (int64_t tl = t0; tl < ntile; tl += dt) {
+  // warp w owns the 16-column groups w and G - 1 - w: with a triangular B group g is live for the
+  // first ~(16 g + 16) / KC chunks, so pairing a short-lived group with a long-lived one gives every
+  // warp the same work per tile and keeps it busy to the late chunks
+  const int hi_g = NP / 16 - 1 - warp;
+  const int c0 = 16 * warp + 4 * t, c1 = 16 * hi_g + 4 * t;
+  const bool hi_cols = 16 * hi_g < N;  // the last group of a padded panel is padding
+  uint32_t it = 0;
+  for (int64_t tl = t0; tl < ntile; tl += dt, ++it) {
     float2 acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
-    for (int c = 0; c < nch; ++c, ++g) {
-      const int st = (int)(g & 1u);
-      mbar_wait(&bars[st], (g >> 1) & 1u);
+    mbar_wait(a_full, it & 1u);
+    for (int c = 0; c < nch; ++c) {
+      mbar_wait(&full[st], ph);
       const int k0 = c * KC;
       const bool lo_on = !upper_tri_b || 16 * warp + 16 > k0;
-      const bool hi_on = hi_cols && (!upper_tri_b || NP / 2 + 16 * warp + 16 > k0);
-      const float* const a_base = As + ((size_t)st * kResBM + r) * AP;
+      const bool hi_on = hi_cols && (!upper_tri_b || 16 * hi_g + 16 > k0);
+      const float* const a_base = As + (size_t)r * AP + k0;
       const float* const b0p = Bs + (size_t)st * KC * NP + c0;
       const float* const b1p = Bs + (size_t)st * KC * NP + c1;
-      if (lo_on && hi_on) kres_tile_m<0, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
-      else if (hi_on) kres_tile_m<2, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
-      else if (lo_on) kres_tile_m<1, KC, NPT, AP, false>(a_base, b0p, b1p, KC, NP, acc);
+      if (lo_on && hi_on) kres_tile_m<0, KC, NPT, APT, false>(a_base, b0p, b1p, KC, NP, acc, AP);
+      else if (hi_on) kres_tile_m<2, KC, NPT, APT, false>(a_base, b0p, b1p, KC, NP, acc, AP);
+      else if (lo_on) kres_tile_m<1, KC, NPT, APT, false>(a_base, b0p, b1p, KC, NP, acc, AP);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[2 + st]);
+      if (lane == 0) {
+        mbar_arrive(&empty[st]);
+        if (c == nch - 1) mbar_arrive(a_empty);
+      }
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
     }
     const int64_t m0 = tl * kResBM;
 #pragma unroll
@@ -492,14 +520,28 @@ __global__ void __launch_bounds__(448, 1)
   }
 }
 
-// whether the K-chunked kernel takes the product (KC = 40 or 32); *smem its dynamic shared memory
-int gemm_kchunk_kc(int64_t N, int64_t K, size_t* smem) {
-  if (K < 160 || N % 4 || N <= 128 || N > 416) return 0;
-  const int kc = K % 40 == 0 ? 40 : (K % 32 == 0 ? 32 : 0);
+// whether the K-chunked kernel takes the product (KC = 20 or 16); ring depth *stages (as many as fit,
+// at most 8) and *smem, its dynamic shared memory
+int gemm_kchunk_kc(int64_t N, int64_t K, size_t* smem, int* stages) {
+  if (K < 160 || K % 4 || N % 4 || N <= 128 || N > 416) return 0;
+  const int kc = K % 20 == 0 ? 20 : (K % 16 == 0 ? 16 : 0);
   if (!kc) return 0;
+  // the A pitch K + 4 must keep the 8 row groups of a fragment read on distinct bank pairs
+  const int64_t ap = K + 4;
+  bool used[16] = {};
+  for (int rr = 0; rr < 8; ++rr) {
+    const int b = (int)((rr * ap) % 32) / 2;
+    if ((rr * ap) % 2 || used[b]) return 0;
+    used[b] = true;
+  }
   const int64_t NP = round_up(N, 32);
-  *smem = (size_t)(2 * kc * NP + 2 * kResBM * (kc + 4)) * 4 + 64;
-  return *smem <= 227 * 1024 ? kc : 0;
+  const size_t a_bytes = (size_t)kResBM * ap * 4, stage = (size_t)kc * NP * 4;
+  if (a_bytes + 2 * stage + 512 > 227 * 1024) return 0;
+  int S = (int)((227 * 1024 - 512 - a_bytes) / (stage + 16));
+  if (S > 8) S = 8;
+  *stages = S;
+  *smem = a_bytes + (size_t)S * (stage + 16) + 64;
+  return kc;
 }
 
 // whether the K-resident kernel takes the product; *smem its dynamic shared memory
@@ -909,16 +951,18 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
     return le;
   }
   size_t kch_smem = 0;
+  int kch_stages = 0;
   static const char* kch_env = getenv("ISVD_GEMM_KCHUNK");  // 0: the tiled kernel for long K (A/B)
   const int kc = (kch_env && atoi(kch_env) == 0) || lda % 4 || ldb % 4 || (uintptr_t)A % 16 || (uintptr_t)B % 16
                      ? 0
-                     : gemm_kchunk_kc(N, K, &kch_smem);
+                     : gemm_kchunk_kc(N, K, &kch_smem, &kch_stages);
   if (kc) {
     using KchFn = void (*)(const float*, int64_t, const float*, int64_t, float*, int64_t, int64_t, int, int,
-                           const float*, float, int, const int*, const int32_t*);
+                           const float*, float, int, int, const int*, const int32_t*);
     const int NP = (int)round_up(N, 32);
-    KchFn fn = kc == 40 ? (NP == 416 ? gemm_kchunk_kernel<40, 416> : gemm_kchunk_kernel<40, 0>)
-                        : (NP == 256 ? gemm_kchunk_kernel<32, 256> : gemm_kchunk_kernel<32, 0>);
+    // compile-time shapes: config 4 (l = 400) and config 2 (l = 256)
+    KchFn fn = kc == 20 ? (NP == 416 && K == 400 ? gemm_kchunk_kernel<20, 404, 416> : gemm_kchunk_kernel<20, 0, 0>)
+                        : (NP == 256 && K == 256 ? gemm_kchunk_kernel<16, 260, 256> : gemm_kchunk_kernel<16, 0, 0>);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     static int sms = 0;
     if (!sms) {
@@ -930,7 +974,7 @@ cudaError_t launch_gemm_tn(const float* A, int64_t lda, const float* B, int64_t 
     const int grid = (int)(ntile < sms ? ntile : sms);
     ++g_launches;
     fn<<<grid, (unsigned)(NP + 32), kch_smem, st>>>(A, lda, B, ldb, C, ldc, M, (int)N, (int)K, row_scale, alpha,
-                                                    upper_tri_b ? 1 : 0, gate, out_map);
+                                                    upper_tri_b ? 1 : 0, kch_stages, gate, out_map);
     return cudaGetLastError();
   }
   if (N > 64 && round_up(N, 80) < round_up(N, 128)) {  // e.g. N = 400: 5 x 80 instead of 4 x 128
