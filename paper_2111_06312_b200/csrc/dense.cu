@@ -404,6 +404,15 @@ __global__ void __launch_bounds__(448, 1)
 // stages of 40 k-steps left the compute warps waiting for data 29 % of the time (11.1 ms; ncu), five
 // stages of 20 k-steps with per-chunk 80-byte A row copies ran 15.9 ms (1,680 small bulk copies per
 // tile): hence whole A rows once per tile.
+// Chunk order of a row tile.  With a triangular B the late chunks carry little work (few live column
+// groups) and finish before the next copy lands (ncu: 16 % of the warp samples waited on full[]), so
+// early and late chunks alternate (0, n-1, 1, n-2, ...): every pair of consecutive chunks then has
+// about the same work, which the ring's prefetch distance covers.
+ISVD_DEVICE int chunk_order(int i, int nch, int tri) {
+  if (!tri) return i;
+  return (i & 1) ? nch - 1 - (i >> 1) : (i >> 1);
+}
+
 template <int KC, int APT, int NPT>
 __global__ void __launch_bounds__(448, 1)
     gemm_kchunk_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
@@ -448,8 +457,9 @@ __global__ void __launch_bounds__(448, 1)
       if (lane == 0) mbar_expect_tx(a_full, (uint32_t)(rows * K * 4));
       __syncwarp();
       for (int e = lane; e < rows; e += 32) bulk_g2s(As + (size_t)e * AP, A + (m0 + e) * lda, (uint32_t)(K * 4), a_full);
-      for (int c = 0; c < nch; ++c) {
+      for (int i = 0; i < nch; ++i) {
         if (!first_lap) mbar_wait(&empty[st], ph ^ 1u);  // every compute warp released the previous use
+        const int c = chunk_order(i, nch, upper_tri_b);
         const int k0 = c * KC;
         const int cb = upper_tri_b ? (k0 / 16) * 16 : 0;  // first live column
         if (lane == 0) mbar_expect_tx(&full[st], (uint32_t)(KC * (N - cb) * 4));
@@ -481,8 +491,9 @@ __global__ void __launch_bounds__(448, 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
     mbar_wait(a_full, it & 1u);
-    for (int c = 0; c < nch; ++c) {
+    for (int i = 0; i < nch; ++i) {
       mbar_wait(&full[st], ph);
+      const int c = chunk_order(i, nch, upper_tri_b);
       const int k0 = c * KC;
       const bool lo_on = !upper_tri_b || 16 * warp + 16 > k0;
       const bool hi_on = hi_cols && (!upper_tri_b || 16 * hi_g + 16 > k0);
@@ -495,7 +506,7 @@ __global__ void __launch_bounds__(448, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&empty[st]);
-        if (c == nch - 1) mbar_arrive(a_empty);
+        if (i == nch - 1) mbar_arrive(a_empty);
       }
       if (++st == S) {
         st = 0;
