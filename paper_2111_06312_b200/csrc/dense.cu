@@ -851,14 +851,30 @@ __global__ void scale_rows_kernel(const float* __restrict__ in, int64_t ldi, flo
                                   int64_t rows, int64_t w4, const float* __restrict__ vec, float coef,
                                   const int* gate, const int32_t* __restrict__ in_map) {
   if (gate && *((volatile const int*)gate) == 0) return;
-  int64_t tot = rows * w4;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
-    float s = coef * (vec ? vec[i] : 1.f);
-    const int64_t src = in_map ? (int64_t)in_map[i] : i;
-    ISVD_ASSERT(src >= 0 && c + 3 < ldi && c + 3 < ldo);
-    float4 v = *reinterpret_cast<const float4*>(in + src * ldi + c);
-    *reinterpret_cast<float4*>(out + i * ldo + c) = make_float4(s * v.x, s * v.y, s * v.z, s * v.w);
+  // four independent 16-byte loads in flight per thread (one per trip ran the n x 400 passes of the
+  // solver at 2.7 TB/s: 2.9 ms where the copy rate gives 1.3 ms)
+  const int64_t tot = rows * w4, S = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < tot; t0 += 4 * S) {
+    float4 v[4];
+    float sc[4];
+    int64_t dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + u * S;
+      dst[u] = -1;
+      if (t < tot) {
+        const int64_t i = row_of(t, w4), c = (t - i * w4) * 4;
+        sc[u] = coef * (vec ? vec[i] : 1.f);
+        const int64_t src = in_map ? (int64_t)in_map[i] : i;
+        ISVD_ASSERT(src >= 0 && c + 3 < ldi && c + 3 < ldo);
+        v[u] = *reinterpret_cast<const float4*>(in + src * ldi + c);
+        dst[u] = i * ldo + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (dst[u] >= 0)
+        *reinterpret_cast<float4*>(out + dst[u]) = make_float4(sc[u] * v[u].x, sc[u] * v[u].y, sc[u] * v[u].z, sc[u] * v[u].w);
   }
 }
 

@@ -585,14 +585,31 @@ __global__ void flip_kernel(const float* __restrict__ sgn, int k, float* U, int6
   if ((k & 3) == 0 && (ldu & 3) == 0) {
     const int k4 = k >> 2;
     const int64_t tot = rows * k4;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t i = row_of(t, k4);
-      const int c = (int)(t - i * k4) * 4;
-      float4* p = reinterpret_cast<float4*>(U + i * ldu + c);
-      float4 v = *p;
-      v.x *= sgn[c]; v.y *= sgn[c + 1]; v.z *= sgn[c + 2]; v.w *= sgn[c + 3];
-      bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
-      *p = v;
+    // four independent 16-byte loads in flight per thread
+    const int64_t S = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < tot; t0 += 4 * S) {
+      float4* p[4];
+      float4 v[4];
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + u * S;
+        p[u] = nullptr;
+        if (t < tot) {
+          const int64_t i = row_of(t, k4);
+          c[u] = (int)(t - i * k4) * 4;
+          p[u] = reinterpret_cast<float4*>(U + i * ldu + c[u]);
+          v[u] = *p[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!p[u]) continue;
+        float4 w = v[u];
+        w.x *= sgn[c[u]]; w.y *= sgn[c[u] + 1]; w.z *= sgn[c[u] + 2]; w.w *= sgn[c[u] + 3];
+        bad |= !isfinite(w.x) | !isfinite(w.y) | !isfinite(w.z) | !isfinite(w.w);
+        *p[u] = w;
+      }
     }
   } else {
     const int64_t tot = rows * k;
