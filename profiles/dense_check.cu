@@ -104,6 +104,8 @@ int main(int argc, char** argv) {
     }
     printf("X G       : %7.3f ms  %6.1f TFLOP/s   sampled worst err / sum|terms| %.2e\n", t, gf / t, worst);
   }
+  t = time_ms([&] { isvd::launch_gemm_tn(dX, d, dG, l, dC, l, n, l, d, ds, 1.f, false, nullptr, 0); });
+  printf("s X G     : %7.3f ms  %6.1f TFLOP/s   (row scale in the epilogue)\n", t, gf / t);
   t = time_ms([&] { isvd::launch_gemm_tn(dZ, l, dR, l, dC, l, n, l, l, nullptr, 1.f, true, nullptr, 0); });
   {
     std::vector<float> Cs(l);
