@@ -375,26 +375,13 @@ __global__ void __launch_bounds__(448, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&bars[2 + slot]);  // this warp has read the slot
     const int64_t m0 = tl * kResBM;
-    // the eight row scales / row targets are loaded together before the stores (interleaved with the
-    // stores they ran as eight dependent round trips: X G_L with its row scale took 4.65 ms, 4.03 without)
-    float scv[8];
-    int64_t orow[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t gm = m0 + r + 8 * i;
-      scv[i] = alpha;
-      orow[i] = gm;
-      if (gm < M) {
-        if (row_scale) scv[i] *= __ldg(row_scale + gm);
-        if (out_map) orow[i] = (int64_t)__ldg(out_map + gm);
-      }
-    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int64_t gm = m0 + r + 8 * i;
       if (gm >= M) continue;
-      const float sc = scv[i];
-      float* const crow = C + orow[i] * ldc;
+      float sc = alpha;
+      if (row_scale) sc *= row_scale[gm];
+      float* const crow = C + (out_map ? (int64_t)out_map[gm] : gm) * ldc;
       if (c0 < N)
         *reinterpret_cast<float4*>(crow + c0) =
             make_float4(sc * acc[i][0].x, sc * acc[i][0].y, sc * acc[i][1].x, sc * acc[i][1].y);
@@ -527,26 +514,13 @@ __global__ void __launch_bounds__(448, 1)
       }
     }
     const int64_t m0 = tl * kResBM;
-    // the eight row scales / row targets are loaded together before the stores (interleaved with the
-    // stores they ran as eight dependent round trips: X G_L with its row scale took 4.65 ms, 4.03 without)
-    float scv[8];
-    int64_t orow[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t gm = m0 + r + 8 * i;
-      scv[i] = alpha;
-      orow[i] = gm;
-      if (gm < M) {
-        if (row_scale) scv[i] *= __ldg(row_scale + gm);
-        if (out_map) orow[i] = (int64_t)__ldg(out_map + gm);
-      }
-    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int64_t gm = m0 + r + 8 * i;
       if (gm >= M) continue;
-      const float sc = scv[i];
-      float* const crow = C + orow[i] * ldc;
+      float sc = alpha;
+      if (row_scale) sc *= row_scale[gm];
+      float* const crow = C + (out_map ? (int64_t)out_map[gm] : gm) * ldc;
       if (c0 < N)
         *reinterpret_cast<float4*>(crow + c0) =
             make_float4(sc * acc[i][0].x, sc * acc[i][0].y, sc * acc[i][1].x, sc * acc[i][1].y);
